@@ -1,0 +1,260 @@
+/* sbs_b200 — B200-native (sm_100a) hot path of the Staggered Batch Scheduling
+ * reference simulator (arXiv 2512.16134, "sbsim").
+ *
+ * C-ABI drop-in boundary.  Plain pointers and sizes only; no torch / C++ types.
+ * Each entry point names the reference interface it replaces
+ * (paths relative to the reference tree, /root/reference/proj).
+ *
+ * Return codes mirror the reference's error classes:
+ *   SBS_OK             0
+ *   SBS_ERR_CONFIG     1  ≙ sbsim::ConfigError          (core.h:34-37)
+ *   SBS_ERR_INVARIANT  3  ≙ std::logic_error invariant  (simclock.cpp:25-28,
+ *                          engine_model.cpp:129-130, simulation.cpp:516-533)
+ *   SBS_ERR_OVERFLOW   4  a fixed-capacity device arena overflowed (the host
+ *                          wrappers retry with doubled capacity; never silent)
+ *   SBS_ERR_CUDA       5  CUDA runtime error / no device / extension missing
+ * sbs_last_error() returns a thread-local message for the last failure.
+ */
+#ifndef SBS_B200_H_
+#define SBS_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SBS_OK 0
+#define SBS_ERR_CONFIG 1
+#define SBS_ERR_INVARIANT 3
+#define SBS_ERR_OVERFLOW 4
+#define SBS_ERR_CUDA 5
+
+/* SchedulerPolicy (config.h:19-24) */
+#define SBS_POLICY_SBS 0
+#define SBS_POLICY_IMMEDIATE 1
+#define SBS_POLICY_ROUND_ROBIN 2
+#define SBS_POLICY_LEAST_OUTSTANDING 3
+/* DecodePolicy (config.h:26) */
+#define SBS_DECODE_IQR 0
+#define SBS_DECODE_RANDOM 1
+#define SBS_DECODE_ROUND_ROBIN 2
+/* AllocMode (prefill_alloc.h:15) */
+#define SBS_ALLOC_BASIC 0
+#define SBS_ALLOC_CACHE_AWARE 1
+/* ArrivalProcess (workload.h:16-20) / LengthDist (workload.h:22) */
+#define SBS_ARRIVAL_POISSON 0
+#define SBS_ARRIVAL_UNIFORM 1
+#define SBS_ARRIVAL_UNIFORM_JITTER 2
+#define SBS_LEN_CONSTANT 0
+#define SBS_LEN_UNIFORM 1
+#define SBS_LEN_LOGNORMAL 2
+
+/* ClusterConfig (core.h:236-260) incl. EngineCoefficients (core.h:222-228). */
+typedef struct sbs_cluster {
+  int32_t n_instances_prefill;
+  int32_t n_instances_decode;
+  int32_t dp_degree;
+  int32_t dp_degree_decode; /* 0 = same as dp_degree */
+  int64_t c_chunk;
+  double t_default_s;
+  int64_t w_size;
+  double l_net_s;
+  int32_t n_limit;
+  int32_t decode_max_batch_per_dp; /* 0 = unbounded */
+  double iqr_k;
+  double watchdog_multiplier;
+  double prefill_base_s;
+  double prefill_per_token_s;
+  double decode_base_s;
+  double decode_per_request_s;
+  double decode_per_kv_token_s;
+  int64_t decode_tokens_per_step;
+  int32_t cache_enabled; /* cache-aware mode is out of scope: must be 0 */
+  int32_t _pad;
+} sbs_cluster;
+
+/* LengthSpec (workload.h:28-35) */
+typedef struct sbs_length_spec {
+  int32_t dist;
+  int32_t _pad;
+  int64_t value, min, max;
+  double mu, sigma;
+} sbs_length_spec;
+
+/* WorkloadSpec (workload.h:37-50) */
+typedef struct sbs_workload {
+  int32_t process;
+  int32_t initial_burst;
+  double rate_qps;
+  double duration_s;
+  sbs_length_spec prompt;
+  sbs_length_spec output;
+  double shared_prefix_fraction; /* must be 0 (prefix cache out of scope) */
+  int32_t prefix_pool;
+  int32_t _pad;
+  int64_t prefix_len;
+} sbs_workload;
+
+/* FaultPlan entries (config.h:35-58) */
+typedef struct sbs_drop_fault { int32_t instance; int32_t _pad; double from_s, until_s; } sbs_drop_fault;
+typedef struct sbs_dead_fault { int32_t instance; int32_t _pad; double time_s; } sbs_dead_fault;
+typedef struct sbs_topology_fault { int32_t instance; int32_t healthy; double time_s; } sbs_topology_fault;
+
+/* ExperimentConfig (config.h:66-75).  One replica = one experiment. */
+typedef struct sbs_experiment {
+  sbs_cluster cluster;
+  sbs_workload workload;
+  int32_t policy;
+  int32_t prefill_mode;
+  int32_t decode_policy;
+  int32_t n_drops;
+  uint64_t seed;
+  double warmup_fraction;
+  const sbs_drop_fault* drops;
+  const sbs_dead_fault* deads;
+  const sbs_topology_fault* topology;
+  int32_t n_deads;
+  int32_t n_topology;
+} sbs_experiment;
+
+/* A request trace in SoA form: the output of generate_workload
+ * (workload.cpp:67-142), ids = positions.  16 B per request. */
+typedef struct sbs_trace {
+  const int64_t* arrival_ns;
+  const int32_t* prompt_len;
+  const int32_t* output_len;
+  int64_t n;
+  uint64_t digest; /* workload_digest (workload.cpp:144-162) */
+} sbs_trace;
+
+/* Aggregates (metrics.h:67-102), same field meaning, plus the sweep extras. */
+typedef struct sbs_aggregates {
+  uint64_t generated, completed, throttled, in_flight, window_requests;
+  double ttft_mean_s, ttft_p50_s, ttft_p95_s;
+  double scheduler_wait_mean_s, device_wait_mean_s, total_wait_mean_s;
+  uint64_t passes;
+  double chunk_util_mean;
+  uint64_t decode_steps, output_tokens;
+  double output_tokens_per_s, kv_mean_time_avg, kv_sigma_time_avg;
+  double completed_per_s;
+  uint64_t watchdog_fires, dropped_end_forwards, rejected_samples, deferrals,
+      flow_control_events, mask_events, fallback_events;
+  double warmup_cutoff_s, duration_s;
+  /* extras (not in the reference) */
+  uint64_t alloc_calls;     /* allocate_batch invocations (cluster-windows) */
+  uint64_t decode_selects;  /* decode placements */
+  uint64_t events;          /* live events processed */
+  double tpot_mean_s;       /* (completion-first_token)/(output_len-1), output_len>1 */
+  uint64_t tpot_count;
+  int64_t ttft_sum_ns, sched_sum_ns, device_sum_ns; /* exact int64 sums */
+  int32_t error;            /* per-replica SBS_* code */
+  int32_t _pad;
+} sbs_aggregates;
+
+#define SBS_HIST_BINS 64
+/* TTFT / TPOT log2-spaced histograms (bin b counts values in [2^b, 2^(b+1)) ns,
+ * bin 0 also holds 0) summed over replicas; NCCL-reducible as int64. */
+typedef struct sbs_histograms {
+  int64_t ttft[SBS_HIST_BINS];
+  int64_t tpot[SBS_HIST_BINS];
+} sbs_histograms;
+
+/* ----------------------------------------------------------------------- */
+/* Trace generation (host, multi-threaded).  Replaces generate_workload +   */
+/* workload_digest (workload.cpp:67-162); bit-identical on the same glibc.  */
+/* With arrays NULL only *n_out (and *digest) are produced.                 */
+int sbs_generate_workload(const sbs_workload* spec, uint64_t seed,
+                          int64_t* arrival_ns, int32_t* prompt_len,
+                          int32_t* output_len, int64_t cap, int64_t* n_out,
+                          uint64_t* digest);
+
+/* ----------------------------------------------------------------------- */
+/* Persistent replica simulator (the DES hot path).                         */
+/* Replaces run_experiment (simulation.h:33 / simulation.cpp:537-541) for   */
+/* many independent replicas at once: one warp per replica.                 */
+typedef struct sbs_sim sbs_sim;
+
+#define SBS_FLAG_PER_REQUEST 1u /* keep per-request timestamps (parity mode) */
+
+/* traces: host arrays (uploaded here).  trace_of_point[i] selects the trace of
+ * point i (NULL: point i uses trace i).  Points sharing a trace share HBM. */
+int sbs_sim_create(const sbs_experiment* points, int32_t n_points,
+                   const sbs_trace* traces, int32_t n_traces,
+                   const int32_t* trace_of_point, uint32_t flags,
+                   int32_t device, sbs_sim** out);
+/* Re-upload host traces (same shapes) on `stream` (H2D of 16 B/request). */
+int sbs_sim_upload_traces(sbs_sim* sim, const sbs_trace* traces, void* stream);
+/* Enqueue one full simulation of every point (DES kernel + finalize kernel). */
+int sbs_sim_launch(sbs_sim* sim, void* stream);
+/* Synchronise `stream`, copy results back, finish the aggregate arithmetic. */
+int sbs_sim_results(sbs_sim* sim, sbs_aggregates* out, sbs_histograms* hist,
+                    void* stream);
+/* Parity mode: per-request timestamps of one point (ns, -1 when unset) and
+ * status (RequestStatus, core.h:41-48). */
+int sbs_sim_requests(sbs_sim* sim, int32_t point, int64_t* dispatch_ns,
+                     int64_t* prefill_start_ns, int64_t* first_token_ns,
+                     int64_t* completion_ns, int8_t* status);
+/* Number of kernel launches enqueued by one sbs_sim_launch. */
+int32_t sbs_sim_launches_per_run(const sbs_sim* sim);
+/* Device bytes allocated for this simulator. */
+int64_t sbs_sim_device_bytes(const sbs_sim* sim);
+void sbs_sim_destroy(sbs_sim* sim);
+
+/* One-shot: generate traces on the host (threads), upload, simulate, return
+ * aggregates.  The reference-facing call behind run_experiment. */
+int sbs_run_experiments(const sbs_experiment* points, int32_t n_points,
+                        sbs_aggregates* out, int32_t device);
+
+/* ----------------------------------------------------------------------- */
+/* Batched PBAA window allocation (allocate_batch, prefill_alloc.cpp:61-88, */
+/* Basic mode; greedy_dispatch :23-59).  One warp per cluster-window.       */
+/* All pointers are DEVICE pointers; window w owns requests                 */
+/* [req_off[w], req_off[w+1]) of which the first n_pending[w] are q_pending */
+/* and the rest q_new (each in caller queue order), and DP capacities       */
+/* [dp_off[w], dp_off[w+1]) (c_avail snapshots, updated in place).          */
+/* Outputs per request: out_dp = DP index placed, -1 deferred, -2 throttled;*/
+/* out_rank = position in the placement order (-1 if not placed);           */
+/* wait_out = wait_cycles after the cycle.  flow[w] = flow-control flag.    */
+typedef struct sbs_window_batch {
+  int32_t n_windows;
+  int32_t _pad;
+  const int64_t* req_off;
+  const int32_t* n_pending;
+  const int64_t* dp_off;
+  const int32_t* n_limit;
+  const int64_t* req_id;
+  const int64_t* prompt_len;
+  const int32_t* wait_in;
+  int64_t* caps;
+  int32_t* out_dp;
+  int32_t* out_rank;
+  int32_t* wait_out;
+  uint8_t* flow;
+} sbs_window_batch;
+int sbs_prefill_allocate(const sbs_window_batch* batch, void* stream);
+
+/* Batched IQR-masked lexicographic decode selection (select_decode_unit,    */
+/* decode_alloc.cpp:38-81).  Call c considers units [unit_off[c],           */
+/* unit_off[c+1]) with (B, K); returns the selected position, the fallback  */
+/* flag and the threshold Q3 + k(Q3-Q1).  DEVICE pointers.                  */
+typedef struct sbs_decode_batch {
+  int32_t n_calls;
+  int32_t _pad;
+  const int64_t* unit_off;
+  const int32_t* batch;
+  const int64_t* kv;
+  double k;
+  int32_t* pos_out;
+  uint8_t* fallback_out;
+  double* threshold_out;
+} sbs_decode_batch;
+int sbs_decode_select(const sbs_decode_batch* batch, void* stream);
+
+const char* sbs_last_error(void);
+const char* sbs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SBS_B200_H_ */

@@ -1,0 +1,391 @@
+// TEST INFRASTRUCTURE ONLY — the checker, never the product.
+//
+// C-ABI harness around the *unmodified* reference sources
+// (/root/reference/proj/src/*.cpp), compiled in place by oracle/Makefile into
+// oracle/_ref/libsbsim_ref.so.  Only tests/, __graft_entry__.smoke() and
+// bench.py's cpu_baseline / --impl reference leg may load it.
+//
+// Two reference functions are interposed (never edited): prefill_alloc.cpp is
+// compiled with -Dallocate_batch=ref_impl_allocate_batch and decode_alloc.cpp
+// with -Dselect_decode_unit=ref_impl_select_decode_unit, so the wrappers below
+// (which carry the original names) can count and optionally record every
+// allocation window and decode placement that the reference Runner makes
+// (simulation.cpp:287-289 and :459-460) without changing its behaviour.
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "sbsim/config.h"
+#include "sbsim/decode_alloc.h"
+#include "sbsim/metrics.h"
+#include "sbsim/prefill_alloc.h"
+#include "sbsim/simulation.h"
+#include "sbsim/workload.h"
+
+namespace sbsim {
+// Renamed reference implementations (see file header).
+AllocationResult ref_impl_allocate_batch(std::span<Request* const> q_pending,
+                                         std::span<Request* const> q_new,
+                                         std::vector<DpPlan>& dps, int n_limit,
+                                         AllocMode mode);
+int ref_impl_select_decode_unit(const std::vector<DecodeUnitPlan>& units,
+                                double k, std::uint64_t request_id,
+                                const DecodeObserver& observe);
+}  // namespace sbsim
+
+namespace {
+
+using namespace sbsim;
+
+// Flat window record: [n_pending, n_new, D, n_limit,
+//   pending (id,len,wait)*, new (id,len,wait)*, caps_in*D,
+//   n_map, (id,dp)*, n_def, (id,wait)*, n_thr, id*, caps_out*D, flow]
+struct Recorder {
+  bool windows = false;
+  bool decodes = false;
+  std::vector<std::int64_t> win;
+  std::vector<std::int64_t> dec;  // U, (B,K)*U, selected, fallback
+  std::int64_t alloc_calls = 0;
+  std::int64_t decode_selects = 0;
+};
+
+thread_local Recorder* g_rec = nullptr;
+
+thread_local std::string g_err;
+
+}  // namespace
+
+namespace sbsim {
+
+AllocationResult allocate_batch(std::span<Request* const> q_pending,
+                                std::span<Request* const> q_new,
+                                std::vector<DpPlan>& dps, int n_limit,
+                                AllocMode mode) {
+  Recorder* r = g_rec;
+  if (r == nullptr)
+    return ref_impl_allocate_batch(q_pending, q_new, dps, n_limit, mode);
+  r->alloc_calls += 1;
+  if (!r->windows)
+    return ref_impl_allocate_batch(q_pending, q_new, dps, n_limit, mode);
+  auto& w = r->win;
+  w.push_back(static_cast<std::int64_t>(q_pending.size()));
+  w.push_back(static_cast<std::int64_t>(q_new.size()));
+  w.push_back(static_cast<std::int64_t>(dps.size()));
+  w.push_back(n_limit);
+  for (auto* q : {&q_pending, &q_new})
+    for (Request* req : *q) {
+      w.push_back(static_cast<std::int64_t>(req->id));
+      w.push_back(req->prompt_len);
+      w.push_back(req->wait_cycles);
+    }
+  for (const DpPlan& d : dps) w.push_back(d.c_avail);
+  AllocationResult res =
+      ref_impl_allocate_batch(q_pending, q_new, dps, n_limit, mode);
+  w.push_back(static_cast<std::int64_t>(res.mapping.size()));
+  for (auto& [req, dp] : res.mapping) {
+    w.push_back(static_cast<std::int64_t>(req->id));
+    w.push_back(dp);
+  }
+  w.push_back(static_cast<std::int64_t>(res.deferred.size()));
+  for (Request* req : res.deferred) {
+    w.push_back(static_cast<std::int64_t>(req->id));
+    w.push_back(req->wait_cycles);
+  }
+  w.push_back(static_cast<std::int64_t>(res.throttled.size()));
+  for (Request* req : res.throttled) w.push_back(static_cast<std::int64_t>(req->id));
+  for (const DpPlan& d : dps) w.push_back(d.c_avail);
+  w.push_back(res.flow_control ? 1 : 0);
+  return res;
+}
+
+int select_decode_unit(const std::vector<DecodeUnitPlan>& units, double k,
+                       std::uint64_t request_id, const DecodeObserver& observe) {
+  Recorder* r = g_rec;
+  if (r == nullptr || !r->decodes) {
+    if (r != nullptr) r->decode_selects += 1;
+    return ref_impl_select_decode_unit(units, k, request_id, observe);
+  }
+  r->decode_selects += 1;
+  bool fb = false;
+  auto wrapped = [&](const DecodePlacementInfo& info) {
+    fb = info.fallback;
+    if (observe) observe(info);
+  };
+  int pos = ref_impl_select_decode_unit(units, k, request_id, wrapped);
+  auto& d = r->dec;
+  d.push_back(static_cast<std::int64_t>(units.size()));
+  for (const auto& u : units) {
+    d.push_back(u.batch);
+    d.push_back(u.kv);
+  }
+  d.push_back(pos);
+  d.push_back(fb ? 1 : 0);
+  return pos;
+}
+
+}  // namespace sbsim
+
+namespace {
+
+// Aggregates in aggregates_json order (simulation.cpp:545-576).
+constexpr int kAggFields = 28;
+
+void fill_agg(const Aggregates& a, double* out) {
+  double v[kAggFields] = {
+      double(a.generated), double(a.completed), double(a.throttled),
+      double(a.in_flight), double(a.window_requests), a.ttft_mean_s,
+      a.ttft_p50_s, a.ttft_p95_s, a.scheduler_wait_mean_s,
+      a.device_wait_mean_s, a.total_wait_mean_s, double(a.passes),
+      a.chunk_util_mean, double(a.decode_steps), double(a.output_tokens),
+      a.output_tokens_per_s, a.kv_mean_time_avg, a.kv_sigma_time_avg,
+      a.completed_per_s, double(a.watchdog_fires),
+      double(a.dropped_end_forwards), double(a.rejected_samples),
+      double(a.deferrals), double(a.flow_control_events),
+      double(a.mask_events), double(a.fallback_events), a.warmup_cutoff_s,
+      a.duration_s};
+  std::memcpy(out, v, sizeof(v));
+}
+
+int status_code(RequestStatus s) { return static_cast<int>(s); }
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+int ref_agg_fields(void) { return kAggFields; }
+
+// Runs one experiment from JSON text exactly as `sbsim run` would
+// (config.cpp:405 parse_config -> simulation.cpp:537 run_experiment).
+//   agg: kAggFields doubles.   meta: [digest, alloc_calls, decode_selects,
+//   n_requests, horizon_ns].
+//   per_req (nullable, cap rows x 8): arrival, prompt, output, status,
+//   dispatch, prefill_start, first_token, completion (-1 when unset).
+//   windows/decodes (nullable): recorder outputs; *_len in/out (capacity in,
+//   used out; if capacity is too small returns 4 and sets used).
+//   csv (nullable): requests|passes|kvband|control joined by '\x1e'.
+int ref_run_json(const char* json_text, double* agg, std::int64_t* meta,
+                 std::int64_t* per_req, std::int64_t per_req_cap,
+                 std::int64_t* windows, std::int64_t* windows_len,
+                 std::int64_t* decodes, std::int64_t* decodes_len, char* csv,
+                 std::int64_t* csv_len) {
+  try {
+    ExperimentConfig cfg = parse_config(json_text, "<ref_run_json>");
+    Recorder rec;
+    rec.windows = windows != nullptr;
+    rec.decodes = decodes != nullptr;
+    g_rec = &rec;
+    SimulationResult res;
+    try {
+      res = run_experiment(cfg);
+    } catch (...) {
+      g_rec = nullptr;
+      throw;
+    }
+    g_rec = nullptr;
+    if (agg) fill_agg(res.aggregates, agg);
+    if (meta) {
+      meta[0] = static_cast<std::int64_t>(res.workload_digest);
+      meta[1] = rec.alloc_calls;
+      meta[2] = rec.decode_selects;
+      meta[3] = static_cast<std::int64_t>(res.requests.size());
+      meta[4] = res.horizon;
+    }
+    int rc = 0;
+    if (per_req) {
+      if (static_cast<std::int64_t>(res.requests.size()) > per_req_cap) {
+        rc = 4;
+      } else {
+        std::int64_t* p = per_req;
+        for (const Request& r : res.requests) {
+          p[0] = r.arrival_time;
+          p[1] = r.prompt_len;
+          p[2] = r.output_len;
+          p[3] = status_code(r.status);
+          p[4] = r.dispatch_time ? *r.dispatch_time : -1;
+          p[5] = r.prefill_start ? *r.prefill_start : -1;
+          p[6] = r.first_token_time ? *r.first_token_time : -1;
+          p[7] = r.completion_time ? *r.completion_time : -1;
+          p += 8;
+        }
+      }
+    }
+    auto copy_out = [&rc](const std::vector<std::int64_t>& src,
+                          std::int64_t* dst, std::int64_t* len) {
+      if (dst == nullptr) return;
+      std::int64_t cap = *len;
+      *len = static_cast<std::int64_t>(src.size());
+      if (*len > cap) {
+        rc = 4;
+        return;
+      }
+      std::memcpy(dst, src.data(), src.size() * sizeof(std::int64_t));
+    };
+    copy_out(rec.win, windows, windows_len);
+    copy_out(rec.dec, decodes, decodes_len);
+    if (csv) {
+      std::string all = MetricsCollector::requests_csv(res.requests);
+      all += '\x1e';
+      all += res.metrics.passes_csv();
+      all += '\x1e';
+      all += res.metrics.kvband_csv();
+      all += '\x1e';
+      all += res.metrics.control_csv();
+      std::int64_t cap = *csv_len;
+      *csv_len = static_cast<std::int64_t>(all.size());
+      if (*csv_len + 1 > cap)
+        rc = 4;
+      else
+        std::memcpy(csv, all.c_str(), all.size() + 1);
+    }
+    return rc;
+  } catch (const ConfigError& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::logic_error& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
+  }
+}
+
+// generate_workload (workload.cpp:67-142) for the config's workload+seed.
+// out: cap rows x 3 (arrival_ns, prompt_len, output_len). meta: [n, digest].
+int ref_generate_workload(const char* json_text, std::int64_t* out,
+                          std::int64_t cap, std::int64_t* meta) {
+  try {
+    ExperimentConfig cfg = parse_config(json_text, "<ref_generate_workload>");
+    std::vector<Request> reqs = generate_workload(cfg.workload, cfg.sim.seed);
+    meta[0] = static_cast<std::int64_t>(reqs.size());
+    meta[1] = static_cast<std::int64_t>(workload_digest(reqs));
+    if (out == nullptr) return 0;
+    if (static_cast<std::int64_t>(reqs.size()) > cap) return 4;
+    for (const Request& r : reqs) {
+      out[0] = r.arrival_time;
+      out[1] = r.prompt_len;
+      out[2] = r.output_len;
+      out += 3;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// allocate_batch (prefill_alloc.cpp:61-88), Basic mode, on plain arrays.
+// pend/fresh: rows of (id, prompt_len, wait_cycles).
+// out_map: (id, dp) pairs; out_def: (id, wait) pairs; out_thr: ids;
+// counts[3] = n_map, n_def, n_thr; caps updated in place; returns flow flag.
+int ref_allocate_batch(const std::int64_t* pend, std::int64_t n_pend,
+                       const std::int64_t* fresh, std::int64_t n_fresh,
+                       std::int64_t* caps, std::int64_t n_dp, int n_limit,
+                       std::int64_t* out_map, std::int64_t* out_def,
+                       std::int64_t* out_thr, std::int64_t* counts) {
+  std::vector<Request> storage(static_cast<std::size_t>(n_pend + n_fresh));
+  std::vector<Request*> pv, nv;
+  for (std::int64_t i = 0; i < n_pend + n_fresh; ++i) {
+    const std::int64_t* row = i < n_pend ? pend + 3 * i : fresh + 3 * (i - n_pend);
+    Request& r = storage[static_cast<std::size_t>(i)];
+    r.id = static_cast<std::uint64_t>(row[0]);
+    r.prompt_len = row[1];
+    r.wait_cycles = static_cast<int>(row[2]);
+    (i < n_pend ? pv : nv).push_back(&r);
+  }
+  std::vector<DpPlan> dps(static_cast<std::size_t>(n_dp));
+  for (std::int64_t d = 0; d < n_dp; ++d) {
+    dps[static_cast<std::size_t>(d)].dp_index = static_cast<int>(d);
+    dps[static_cast<std::size_t>(d)].c_avail = caps[d];
+  }
+  AllocationResult res = ref_impl_allocate_batch(
+      {pv.data(), pv.size()}, {nv.data(), nv.size()}, dps, n_limit,
+      AllocMode::kBasic);
+  for (std::size_t i = 0; i < res.mapping.size(); ++i) {
+    out_map[2 * i] = static_cast<std::int64_t>(res.mapping[i].first->id);
+    out_map[2 * i + 1] = res.mapping[i].second;
+  }
+  for (std::size_t i = 0; i < res.deferred.size(); ++i) {
+    out_def[2 * i] = static_cast<std::int64_t>(res.deferred[i]->id);
+    out_def[2 * i + 1] = res.deferred[i]->wait_cycles;
+  }
+  for (std::size_t i = 0; i < res.throttled.size(); ++i)
+    out_thr[i] = static_cast<std::int64_t>(res.throttled[i]->id);
+  counts[0] = static_cast<std::int64_t>(res.mapping.size());
+  counts[1] = static_cast<std::int64_t>(res.deferred.size());
+  counts[2] = static_cast<std::int64_t>(res.throttled.size());
+  for (std::int64_t d = 0; d < n_dp; ++d) caps[d] = dps[static_cast<std::size_t>(d)].c_avail;
+  return res.flow_control ? 1 : 0;
+}
+
+// select_decode_unit (decode_alloc.cpp:38-81) on (B, K) arrays.
+int ref_select_decode_unit(const std::int64_t* batch, const std::int64_t* kv,
+                           std::int64_t n, double k, int* fallback,
+                           double* threshold) {
+  std::vector<DecodeUnitPlan> units(static_cast<std::size_t>(n));
+  for (std::int64_t i = 0; i < n; ++i)
+    units[static_cast<std::size_t>(i)] =
+        DecodeUnitPlan{static_cast<int>(i), static_cast<int>(batch[i]), kv[i]};
+  bool fb = false;
+  double th = 0.0;
+  int pos = ref_impl_select_decode_unit(
+      units, k, 0, [&](const DecodePlacementInfo& info) {
+        fb = info.fallback;
+        th = info.threshold;
+      });
+  if (fallback) *fallback = fb ? 1 : 0;
+  if (threshold) *threshold = th;
+  return pos;
+}
+
+double ref_percentile(const double* v, std::int64_t n, double p) {
+  return percentile(std::vector<double>(v, v + n), p);
+}
+
+double ref_outlier_threshold(const std::int64_t* kv, std::int64_t n, double k) {
+  return outlier_threshold(std::span<const Tokens>(kv, static_cast<std::size_t>(n)), k);
+}
+
+// CPU baseline: run_experiment over n configs on a pool of `threads` std::threads
+// (independent runs may be concurrent). Returns wall seconds in
+// *wall_s; agg_out holds n x kAggFields; meta_out n x 3 (digest, alloc_calls,
+// decode_selects).
+int ref_run_batch(const char* const* json_texts, std::int64_t n, int threads,
+                  double* agg_out, std::int64_t* meta_out, double* wall_s) {
+  std::atomic<std::int64_t> next{0};
+  std::atomic<int> rc{0};
+  auto worker = [&]() {
+    for (;;) {
+      std::int64_t i = next.fetch_add(1);
+      if (i >= n) return;
+      std::int64_t meta[5];
+      int r = ref_run_json(json_texts[i], agg_out + i * kAggFields, meta,
+                           nullptr, 0, nullptr, nullptr, nullptr, nullptr,
+                           nullptr, nullptr);
+      if (r != 0) rc = r;
+      if (meta_out) {
+        meta_out[3 * i] = meta[0];
+        meta_out[3 * i + 1] = meta[1];
+        meta_out[3 * i + 2] = meta[2];
+      }
+    }
+  };
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> pool;
+  int nt = std::max(1, threads);
+  for (int t = 0; t < nt; ++t) pool.emplace_back(worker);
+  for (auto& th : pool) th.join();
+  *wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return rc.load();
+}
+
+}  // extern "C"

@@ -1,0 +1,575 @@
+"""Python view of the sm_100a SBS hot path (ctypes over include/sbs_b200.h).
+
+Mirrors the reference's public interface for this path
+(``proj/include/sbsim/*.h``): experiment configs use the reference JSON schema
+(config.cpp:405-435, unknown keys rejected), ``run_experiment`` returns the
+reference ``Aggregates`` fields (metrics.h:67-102), and ``allocate_batch`` /
+``select_decode_unit`` have the reference's argument meaning.  There is no CPU
+fallback: every entry point fails loudly when the CUDA library or a GPU is
+missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import os
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "lib" / "libsbs_b200.so"
+
+OK, ERR_CONFIG, ERR_INVARIANT, ERR_OVERFLOW, ERR_CUDA = 0, 1, 3, 4, 5
+
+
+class ConfigError(RuntimeError):
+    """≙ sbsim::ConfigError (core.h:34-37)."""
+
+
+class InvariantError(RuntimeError):
+    """≙ std::logic_error raised by a reference invariant check."""
+
+
+class SbsError(RuntimeError):
+    pass
+
+
+# ----------------------------------------------------------------- structs
+class Cluster(C.Structure):
+    _fields_ = [
+        ("n_instances_prefill", C.c_int32), ("n_instances_decode", C.c_int32),
+        ("dp_degree", C.c_int32), ("dp_degree_decode", C.c_int32),
+        ("c_chunk", C.c_int64), ("t_default_s", C.c_double), ("w_size", C.c_int64),
+        ("l_net_s", C.c_double), ("n_limit", C.c_int32),
+        ("decode_max_batch_per_dp", C.c_int32), ("iqr_k", C.c_double),
+        ("watchdog_multiplier", C.c_double), ("prefill_base_s", C.c_double),
+        ("prefill_per_token_s", C.c_double), ("decode_base_s", C.c_double),
+        ("decode_per_request_s", C.c_double), ("decode_per_kv_token_s", C.c_double),
+        ("decode_tokens_per_step", C.c_int64), ("cache_enabled", C.c_int32),
+        ("_pad", C.c_int32),
+    ]
+
+
+class LengthSpec(C.Structure):
+    _fields_ = [("dist", C.c_int32), ("_pad", C.c_int32), ("value", C.c_int64),
+                ("min", C.c_int64), ("max", C.c_int64), ("mu", C.c_double),
+                ("sigma", C.c_double)]
+
+
+class Workload(C.Structure):
+    _fields_ = [("process", C.c_int32), ("initial_burst", C.c_int32),
+                ("rate_qps", C.c_double), ("duration_s", C.c_double),
+                ("prompt", LengthSpec), ("output", LengthSpec),
+                ("shared_prefix_fraction", C.c_double), ("prefix_pool", C.c_int32),
+                ("_pad", C.c_int32), ("prefix_len", C.c_int64)]
+
+
+class DropFault(C.Structure):
+    _fields_ = [("instance", C.c_int32), ("_pad", C.c_int32), ("from_s", C.c_double),
+                ("until_s", C.c_double)]
+
+
+class DeadFault(C.Structure):
+    _fields_ = [("instance", C.c_int32), ("_pad", C.c_int32), ("time_s", C.c_double)]
+
+
+class TopologyFault(C.Structure):
+    _fields_ = [("instance", C.c_int32), ("healthy", C.c_int32), ("time_s", C.c_double)]
+
+
+class Experiment(C.Structure):
+    _fields_ = [("cluster", Cluster), ("workload", Workload), ("policy", C.c_int32),
+                ("prefill_mode", C.c_int32), ("decode_policy", C.c_int32),
+                ("n_drops", C.c_int32), ("seed", C.c_uint64), ("warmup_fraction", C.c_double),
+                ("drops", C.POINTER(DropFault)), ("deads", C.POINTER(DeadFault)),
+                ("topology", C.POINTER(TopologyFault)), ("n_deads", C.c_int32),
+                ("n_topology", C.c_int32)]
+
+
+class Trace(C.Structure):
+    _fields_ = [("arrival_ns", C.POINTER(C.c_int64)), ("prompt_len", C.POINTER(C.c_int32)),
+                ("output_len", C.POINTER(C.c_int32)), ("n", C.c_int64), ("digest", C.c_uint64)]
+
+
+AGG_FIELDS = [
+    ("generated", C.c_uint64), ("completed", C.c_uint64), ("throttled", C.c_uint64),
+    ("in_flight", C.c_uint64), ("window_requests", C.c_uint64), ("ttft_mean_s", C.c_double),
+    ("ttft_p50_s", C.c_double), ("ttft_p95_s", C.c_double),
+    ("scheduler_wait_mean_s", C.c_double), ("device_wait_mean_s", C.c_double),
+    ("total_wait_mean_s", C.c_double), ("passes", C.c_uint64), ("chunk_util_mean", C.c_double),
+    ("decode_steps", C.c_uint64), ("output_tokens", C.c_uint64),
+    ("output_tokens_per_s", C.c_double), ("kv_mean_time_avg", C.c_double),
+    ("kv_sigma_time_avg", C.c_double), ("completed_per_s", C.c_double),
+    ("watchdog_fires", C.c_uint64), ("dropped_end_forwards", C.c_uint64),
+    ("rejected_samples", C.c_uint64), ("deferrals", C.c_uint64),
+    ("flow_control_events", C.c_uint64), ("mask_events", C.c_uint64),
+    ("fallback_events", C.c_uint64), ("warmup_cutoff_s", C.c_double), ("duration_s", C.c_double),
+    ("alloc_calls", C.c_uint64), ("decode_selects", C.c_uint64), ("events", C.c_uint64),
+    ("tpot_mean_s", C.c_double), ("tpot_count", C.c_uint64), ("ttft_sum_ns", C.c_int64),
+    ("sched_sum_ns", C.c_int64), ("device_sum_ns", C.c_int64), ("error", C.c_int32),
+    ("_pad", C.c_int32),
+]
+REFERENCE_AGG_KEYS = [f for f, _ in AGG_FIELDS[:28]]
+
+
+class Aggregates(C.Structure):
+    _fields_ = AGG_FIELDS
+
+    def to_dict(self):
+        return {f: getattr(self, f) for f, _ in AGG_FIELDS if not f.startswith("_")}
+
+
+HIST_BINS = 64
+
+
+class Histograms(C.Structure):
+    _fields_ = [("ttft", C.c_int64 * HIST_BINS), ("tpot", C.c_int64 * HIST_BINS)]
+
+
+class WindowBatch(C.Structure):
+    _fields_ = [("n_windows", C.c_int32), ("_pad", C.c_int32), ("req_off", C.c_void_p),
+                ("n_pending", C.c_void_p), ("dp_off", C.c_void_p), ("n_limit", C.c_void_p),
+                ("req_id", C.c_void_p), ("prompt_len", C.c_void_p), ("wait_in", C.c_void_p),
+                ("caps", C.c_void_p), ("out_dp", C.c_void_p), ("out_rank", C.c_void_p),
+                ("wait_out", C.c_void_p), ("flow", C.c_void_p)]
+
+
+class DecodeBatch(C.Structure):
+    _fields_ = [("n_calls", C.c_int32), ("_pad", C.c_int32), ("unit_off", C.c_void_p),
+                ("batch", C.c_void_p), ("kv", C.c_void_p), ("k", C.c_double),
+                ("pos_out", C.c_void_p), ("fallback_out", C.c_void_p),
+                ("threshold_out", C.c_void_p)]
+
+
+# ----------------------------------------------------------------- library
+_lib = None
+
+
+def library_path() -> Path:
+    return LIB_PATH
+
+
+def lib():
+    """Load the sm_100a library; raises if it was not built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise SbsError(f"CUDA extension missing: {LIB_PATH} (run __graft_entry__.build())")
+        L = C.CDLL(str(LIB_PATH))
+        L.sbs_last_error.restype = C.c_char_p
+        L.sbs_version.restype = C.c_char_p
+        L.sbs_generate_workload.argtypes = [C.POINTER(Workload), C.c_uint64, C.c_void_p,
+                                            C.c_void_p, C.c_void_p, C.c_int64,
+                                            C.POINTER(C.c_int64), C.POINTER(C.c_uint64)]
+        L.sbs_sim_create.argtypes = [C.POINTER(Experiment), C.c_int32, C.POINTER(Trace),
+                                     C.c_int32, C.c_void_p, C.c_uint32, C.c_int32,
+                                     C.POINTER(C.c_void_p)]
+        L.sbs_sim_upload_traces.argtypes = [C.c_void_p, C.POINTER(Trace), C.c_void_p]
+        L.sbs_sim_launch.argtypes = [C.c_void_p, C.c_void_p]
+        L.sbs_sim_results.argtypes = [C.c_void_p, C.POINTER(Aggregates), C.POINTER(Histograms),
+                                      C.c_void_p]
+        L.sbs_sim_requests.argtypes = [C.c_void_p, C.c_int32] + [C.c_void_p] * 5
+        L.sbs_sim_launches_per_run.argtypes = [C.c_void_p]
+        L.sbs_sim_device_bytes.argtypes = [C.c_void_p]
+        L.sbs_sim_device_bytes.restype = C.c_int64
+        L.sbs_sim_destroy.argtypes = [C.c_void_p]
+        L.sbs_sim_destroy.restype = None
+        L.sbs_run_experiments.argtypes = [C.POINTER(Experiment), C.c_int32,
+                                          C.POINTER(Aggregates), C.c_int32]
+        L.sbs_prefill_allocate.argtypes = [C.POINTER(WindowBatch), C.c_void_p]
+        L.sbs_decode_select.argtypes = [C.POINTER(DecodeBatch), C.c_void_p]
+        _lib = L
+    return _lib
+
+
+EXPORTED_SYMBOLS = [
+    "sbs_generate_workload", "sbs_sim_create", "sbs_sim_upload_traces", "sbs_sim_launch",
+    "sbs_sim_results", "sbs_sim_requests", "sbs_sim_launches_per_run", "sbs_sim_device_bytes",
+    "sbs_sim_destroy", "sbs_run_experiments", "sbs_prefill_allocate", "sbs_decode_select",
+    "sbs_last_error", "sbs_version",
+]
+
+
+def _check(rc):
+    if rc == OK:
+        return
+    msg = lib().sbs_last_error().decode()
+    if rc == ERR_CONFIG:
+        raise ConfigError(msg)
+    if rc == ERR_INVARIANT:
+        raise InvariantError(msg)
+    raise SbsError(f"sbs rc={rc}: {msg}")
+
+
+# ----------------------------------------------------------------- configs
+_CLUSTER_KEYS = {"n_instances_prefill", "n_instances_decode", "dp_degree", "dp_degree_decode",
+                 "c_chunk", "t_default_s", "w_size", "l_net_s", "n_limit", "iqr_k",
+                 "watchdog_multiplier", "engine", "decode_tokens_per_step",
+                 "decode_max_batch_per_dp", "cache"}
+_ENGINE_KEYS = {"prefill_base_s", "prefill_per_token_s", "decode_base_s",
+                "decode_per_request_s", "decode_per_kv_token_s"}
+_WORKLOAD_KEYS = {"process", "rate_qps", "duration_s", "prompt", "output",
+                  "shared_prefix_fraction", "prefix_pool", "prefix_len", "initial_burst",
+                  "reference_peak_qps"}
+_LEN_KEYS = {"dist", "value", "min", "max", "mu", "sigma"}
+_POLICIES = {"sbs": 0, "immediate": 1, "round_robin": 2, "least_outstanding": 3}
+_DECODE = {"iqr": 0, "random": 1, "round_robin": 2}
+_PROCESS = {"poisson": 0, "uniform": 1, "uniform_jitter": 2}
+_DIST = {"constant": 0, "uniform": 1, "lognormal": 2}
+
+
+def _keys(obj, path, allowed):
+    if not isinstance(obj, dict):
+        raise ConfigError(f"{path} must be an object")
+    for k in obj:
+        if k not in allowed:
+            raise ConfigError(f'unknown key "{path}.{k}"')
+
+
+def _int(obj, key, default, path):
+    if key not in obj:
+        return default
+    v = obj[key]
+    if isinstance(v, bool) or not isinstance(v, int):
+        raise ConfigError(f"{path}.{key} must be an integer")
+    return v
+
+
+def _num(obj, key, default, path):
+    if key not in obj:
+        return default
+    v = obj[key]
+    if isinstance(v, bool) or not isinstance(v, (int, float)):
+        raise ConfigError(f"{path}.{key} must be a number")
+    return float(v)
+
+
+def _length(obj, path):
+    _keys(obj, path, _LEN_KEYS)
+    s = LengthSpec(dist=0, value=1, min=1, max=1, mu=0.0, sigma=1.0)
+    if "dist" in obj:
+        if obj["dist"] not in _DIST:
+            raise ConfigError(f"{path}.dist must be constant, uniform, or lognormal")
+        s.dist = _DIST[obj["dist"]]
+    s.value = _int(obj, "value", s.value, path)
+    s.min = _int(obj, "min", s.min, path)
+    s.max = _int(obj, "max", s.max, path)
+    s.mu = _num(obj, "mu", s.mu, path)
+    s.sigma = _num(obj, "sigma", s.sigma, path)
+    return s
+
+
+@dataclass
+class Point:
+    """One replica: the ctypes Experiment plus the fault arrays it points to."""
+    exp: Experiment
+    drops: object = None
+    deads: object = None
+    topo: object = None
+
+
+def experiment_from_config(cfg: dict) -> Point:
+    """Reference JSON schema (config.cpp:24-435) -> sbs_experiment."""
+    _keys(cfg, "$", {"cluster", "workload", "scheduler", "sim", "faults"})
+    cl = Cluster(n_instances_prefill=1, n_instances_decode=1, dp_degree=1, dp_degree_decode=0,
+                 c_chunk=1, t_default_s=0.1, w_size=64, l_net_s=0.0, n_limit=8,
+                 decode_max_batch_per_dp=0, iqr_k=1.5, watchdog_multiplier=5.0,
+                 decode_tokens_per_step=1)
+    c = cfg.get("cluster", {})
+    _keys(c, "cluster", _CLUSTER_KEYS)
+    for k in ("n_instances_prefill", "n_instances_decode", "dp_degree", "dp_degree_decode",
+              "c_chunk", "w_size", "n_limit", "decode_tokens_per_step",
+              "decode_max_batch_per_dp"):
+        setattr(cl, k, _int(c, k, getattr(cl, k), "cluster"))
+    for k in ("t_default_s", "l_net_s", "iqr_k", "watchdog_multiplier"):
+        setattr(cl, k, _num(c, k, getattr(cl, k), "cluster"))
+    if "engine" in c:
+        _keys(c["engine"], "cluster.engine", _ENGINE_KEYS)
+        for k in _ENGINE_KEYS:
+            setattr(cl, k, _num(c["engine"], k, 0.0, "cluster.engine"))
+    if "cache" in c:
+        _keys(c["cache"], "cluster.cache", {"enabled", "probe_lens", "budget_tokens"})
+        cl.cache_enabled = 1 if c["cache"].get("enabled", False) else 0
+    w = cfg.get("workload", {})
+    _keys(w, "workload", _WORKLOAD_KEYS)
+    wl = Workload(process=0, initial_burst=0, rate_qps=1.0, duration_s=1.0,
+                  prompt=LengthSpec(dist=0, value=1, min=1, max=1, mu=0.0, sigma=1.0),
+                  output=LengthSpec(dist=0, value=1, min=1, max=1, mu=0.0, sigma=1.0))
+    if "process" in w:
+        if w["process"] not in _PROCESS:
+            raise ConfigError("workload.process must be poisson, uniform, or uniform_jitter")
+        wl.process = _PROCESS[w["process"]]
+    wl.rate_qps = _num(w, "rate_qps", wl.rate_qps, "workload")
+    wl.duration_s = _num(w, "duration_s", wl.duration_s, "workload")
+    if "prompt" in w:
+        wl.prompt = _length(w["prompt"], "workload.prompt")
+    if "output" in w:
+        wl.output = _length(w["output"], "workload.output")
+    wl.shared_prefix_fraction = _num(w, "shared_prefix_fraction", 0.0, "workload")
+    wl.prefix_pool = _int(w, "prefix_pool", 0, "workload")
+    wl.prefix_len = _int(w, "prefix_len", 0, "workload")
+    wl.initial_burst = _int(w, "initial_burst", 0, "workload")
+    x = Experiment(cluster=cl, workload=wl, policy=0, prefill_mode=0, decode_policy=0,
+                   seed=1, warmup_fraction=0.1)
+    s = cfg.get("scheduler", {})
+    _keys(s, "scheduler", {"policy", "prefill_mode", "decode_policy"})
+    if "policy" in s:
+        if s["policy"] not in _POLICIES:
+            raise ConfigError("scheduler.policy must be sbs, immediate, round_robin, or "
+                              "least_outstanding")
+        x.policy = _POLICIES[s["policy"]]
+    if "prefill_mode" in s:
+        if s["prefill_mode"] not in ("basic", "cache_aware"):
+            raise ConfigError("scheduler.prefill_mode must be basic or cache_aware")
+        x.prefill_mode = 0 if s["prefill_mode"] == "basic" else 1
+    if "decode_policy" in s:
+        if s["decode_policy"] not in _DECODE:
+            raise ConfigError("scheduler.decode_policy must be iqr, random, or round_robin")
+        x.decode_policy = _DECODE[s["decode_policy"]]
+    sim = cfg.get("sim", {})
+    _keys(sim, "sim", {"seed", "warmup_fraction", "trace"})
+    seed = _int(sim, "seed", 1, "sim")
+    if seed < 0:
+        raise ConfigError("sim.seed must be non-negative")
+    x.seed = seed
+    x.warmup_fraction = _num(sim, "warmup_fraction", 0.1, "sim")
+    if not (0.0 <= x.warmup_fraction < 1.0):
+        raise ConfigError("sim.warmup_fraction must be in [0, 1)")
+    pt = Point(exp=x)
+    f = cfg.get("faults", {})
+    _keys(f, "faults", {"drop_end_forward", "dead", "topology"})
+    drops = [DropFault(instance=e.get("instance", -1), from_s=float(e.get("from_s", 0.0)),
+                       until_s=float(e.get("until_s", math.inf)))
+             for e in f.get("drop_end_forward", [])]
+    deads = [DeadFault(instance=e.get("instance", 0), time_s=float(e.get("time_s", 0.0)))
+             for e in f.get("dead", [])]
+    topo = [TopologyFault(instance=e.get("instance", 0), healthy=1 if e.get("healthy") else 0,
+                          time_s=float(e.get("time_s", 0.0))) for e in f.get("topology", [])]
+    if drops:
+        pt.drops = (DropFault * len(drops))(*drops)
+        x.drops, x.n_drops = C.cast(pt.drops, C.POINTER(DropFault)), len(drops)
+    if deads:
+        pt.deads = (DeadFault * len(deads))(*deads)
+        x.deads, x.n_deads = C.cast(pt.deads, C.POINTER(DeadFault)), len(deads)
+    if topo:
+        pt.topo = (TopologyFault * len(topo))(*topo)
+        x.topology, x.n_topology = C.cast(pt.topo, C.POINTER(TopologyFault)), len(topo)
+    return pt
+
+
+# ----------------------------------------------------------------- traces
+@dataclass
+class HostTrace:
+    arrival_ns: np.ndarray
+    prompt_len: np.ndarray
+    output_len: np.ndarray
+    digest: int
+
+    @property
+    def n(self):
+        return len(self.arrival_ns)
+
+    def as_c(self) -> Trace:
+        return Trace(self.arrival_ns.ctypes.data_as(C.POINTER(C.c_int64)),
+                     self.prompt_len.ctypes.data_as(C.POINTER(C.c_int32)),
+                     self.output_len.ctypes.data_as(C.POINTER(C.c_int32)),
+                     self.n, self.digest)
+
+
+def generate_workload(point_or_cfg, pinned: bool = False) -> HostTrace:
+    """generate_workload (workload.cpp:67-142) for a point's workload and seed."""
+    pt = point_or_cfg if isinstance(point_or_cfg, Point) else experiment_from_config(point_or_cfg)
+    L = lib()
+    n = C.c_int64(0)
+    dg = C.c_uint64(0)
+    _check(L.sbs_generate_workload(C.byref(pt.exp.workload), pt.exp.seed, None, None, None, 0,
+                                   C.byref(n), C.byref(dg)))
+    cnt = max(n.value, 1)
+    if pinned:
+        import torch
+        a = torch.empty(cnt, dtype=torch.int64, pin_memory=True).numpy()
+        p = torch.empty(cnt, dtype=torch.int32, pin_memory=True).numpy()
+        o = torch.empty(cnt, dtype=torch.int32, pin_memory=True).numpy()
+    else:
+        a = np.empty(cnt, np.int64)
+        p = np.empty(cnt, np.int32)
+        o = np.empty(cnt, np.int32)
+    _check(L.sbs_generate_workload(C.byref(pt.exp.workload), pt.exp.seed, a.ctypes.data,
+                                   p.ctypes.data, o.ctypes.data, cnt, C.byref(n), C.byref(dg)))
+    k = n.value
+    return HostTrace(a[:k], p[:k], o[:k], dg.value)
+
+
+# ----------------------------------------------------------------- simulator
+class Simulator:
+    """Many replicas, one warp each, resident on one GPU (sbs_sim_*)."""
+
+    def __init__(self, points, traces, trace_of_point=None, per_request=False, device=0):
+        L = lib()
+        self.points = list(points)
+        self.traces = list(traces)
+        n = len(self.points)
+        self._exp = (Experiment * n)(*[p.exp for p in self.points])
+        self._tr = (Trace * len(self.traces))(*[t.as_c() for t in self.traces])
+        self._map = None
+        if trace_of_point is not None:
+            self._map = (C.c_int32 * n)(*trace_of_point)
+        h = C.c_void_p()
+        _check(L.sbs_sim_create(self._exp, n, self._tr, len(self.traces),
+                                C.cast(self._map, C.c_void_p) if self._map is not None else None,
+                                1 if per_request else 0, device, C.byref(h)))
+        self.handle = h
+        self.n = n
+
+    def upload_traces(self, traces=None, stream=0):
+        if traces is not None:
+            self.traces = list(traces)
+            self._tr = (Trace * len(self.traces))(*[t.as_c() for t in self.traces])
+        _check(lib().sbs_sim_upload_traces(self.handle, self._tr, C.c_void_p(stream)))
+
+    def launch(self, stream=0):
+        _check(lib().sbs_sim_launch(self.handle, C.c_void_p(stream)))
+
+    def results(self, stream=0, histograms=False):
+        out = (Aggregates * self.n)()
+        hist = Histograms() if histograms else None
+        _check(lib().sbs_sim_results(self.handle, out, C.byref(hist) if hist else None,
+                                     C.c_void_p(stream)))
+        res = [a.to_dict() for a in out]
+        return (res, hist) if histograms else res
+
+    def requests(self, point: int):
+        n = self.traces[0].n if self._map is None and len(self.traces) == 1 else None
+        tr = self.traces[self._map[point] if self._map is not None else point]
+        n = tr.n
+        cols = [np.empty(max(n, 1), np.int64) for _ in range(4)]
+        st = np.empty(max(n, 1), np.int8)
+        _check(lib().sbs_sim_requests(self.handle, point, *[c.ctypes.data for c in cols],
+                                      st.ctypes.data))
+        return {"dispatch": cols[0][:n], "prefill_start": cols[1][:n],
+                "first_token": cols[2][:n], "completion": cols[3][:n], "status": st[:n]}
+
+    @property
+    def launches_per_run(self):
+        return lib().sbs_sim_launches_per_run(self.handle)
+
+    @property
+    def device_bytes(self):
+        return lib().sbs_sim_device_bytes(self.handle)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().sbs_sim_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_experiment(cfg: dict, per_request=False, device=0):
+    """≙ sbsim::run_experiment (simulation.h:33) on the GPU: returns a dict with
+    the Aggregates fields (and per-request arrays when per_request)."""
+    pt = experiment_from_config(cfg)
+    tr = generate_workload(pt)
+    sim = Simulator([pt], [tr], per_request=per_request, device=device)
+    try:
+        sim.launch()
+        agg = sim.results()[0]
+        out = {"agg": agg, "digest": tr.digest, "n": tr.n}
+        if per_request:
+            out["requests"] = sim.requests(0)
+            out["trace"] = tr
+        return out
+    finally:
+        sim.close()
+
+
+# ----------------------------------------------------------------- allocators
+def allocate_batch(windows, device="cuda"):
+    """Batched allocate_batch (prefill_alloc.cpp:61-88, Basic mode).
+
+    windows: list of dicts {pending: (k,3) int array of (id, prompt_len,
+    wait_cycles), new: (k,3), caps: [c_avail per DP], n_limit}.
+    Returns per window {mapping: [(id, dp)] in placement order, deferred:
+    [(id, wait)], throttled: [id], caps: working capacities, flow: bool}.
+    """
+    import torch
+    req_off, dp_off, npend, nlim = [0], [0], [], []
+    ids, lens, waits, caps = [], [], [], []
+    for w in windows:
+        p = np.asarray(w["pending"], np.int64).reshape(-1, 3)
+        q = np.asarray(w["new"], np.int64).reshape(-1, 3)
+        allr = np.concatenate([p, q]) if len(p) + len(q) else np.zeros((0, 3), np.int64)
+        ids.append(allr[:, 0]); lens.append(allr[:, 1]); waits.append(allr[:, 2])
+        npend.append(len(p)); nlim.append(int(w["n_limit"]))
+        req_off.append(req_off[-1] + len(allr))
+        caps.append(np.asarray(w["caps"], np.int64)); dp_off.append(dp_off[-1] + len(w["caps"]))
+    dev = torch.device(device)
+    T = lambda a, dt: torch.as_tensor(np.ascontiguousarray(a), dtype=dt, device=dev)
+    cat = lambda xs: np.concatenate(xs) if xs else np.zeros(0, np.int64)
+    t_req_off, t_dp_off = T(req_off, torch.int64), T(dp_off, torch.int64)
+    t_np, t_nl = T(npend, torch.int32), T(nlim, torch.int32)
+    t_id, t_len = T(cat(ids), torch.int64), T(cat(lens), torch.int64)
+    t_wait, t_caps = T(cat(waits), torch.int32), T(cat(caps), torch.int64)
+    total = req_off[-1]
+    t_dp = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    t_rank = torch.empty_like(t_dp)
+    t_wout = torch.empty_like(t_dp)
+    t_flow = torch.empty(max(len(windows), 1), dtype=torch.uint8, device=dev)
+    b = WindowBatch(n_windows=len(windows), req_off=t_req_off.data_ptr(), n_pending=t_np.data_ptr(),
+                    dp_off=t_dp_off.data_ptr(), n_limit=t_nl.data_ptr(), req_id=t_id.data_ptr(),
+                    prompt_len=t_len.data_ptr(), wait_in=t_wait.data_ptr(),
+                    caps=t_caps.data_ptr(), out_dp=t_dp.data_ptr(), out_rank=t_rank.data_ptr(),
+                    wait_out=t_wout.data_ptr(), flow=t_flow.data_ptr())
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    _check(lib().sbs_prefill_allocate(C.byref(b), C.c_void_p(stream)))
+    o_dp, o_rank, o_w = t_dp.cpu().numpy(), t_rank.cpu().numpy(), t_wout.cpu().numpy()
+    o_caps, o_flow = t_caps.cpu().numpy(), t_flow.cpu().numpy()
+    all_ids = cat(ids)
+    out = []
+    for i, w in enumerate(windows):
+        r0, r1 = req_off[i], req_off[i + 1]
+        sl = slice(r0, r1)
+        dpv, rk, wv, idv = o_dp[sl], o_rank[sl], o_w[sl], all_ids[sl]
+        placed = np.nonzero(dpv >= 0)[0]
+        placed = placed[np.argsort(rk[placed], kind="stable")]
+        mapping = np.stack([idv[placed], dpv[placed]], 1) if len(placed) else np.zeros((0, 2), np.int64)
+        dmask = np.nonzero(dpv == -1)[0]  # input order: pending first, then new
+        deferred = np.stack([idv[dmask], wv[dmask]], 1) if len(dmask) else np.zeros((0, 2), np.int64)
+        throttled = idv[dpv == -2]
+        out.append({"mapping": mapping.astype(np.int64), "deferred": deferred.astype(np.int64),
+                    "throttled": throttled.astype(np.int64),
+                    "caps": o_caps[dp_off[i]:dp_off[i + 1]].copy(), "flow": bool(o_flow[i])})
+    return out
+
+
+def select_decode_unit(calls, k=1.5, device="cuda"):
+    """Batched select_decode_unit (decode_alloc.cpp:38-81).
+
+    calls: list of (batch[], kv[]) arrays.  Returns (pos, fallback, threshold) arrays.
+    """
+    import torch
+    off = [0]
+    for b, kv in calls:
+        off.append(off[-1] + len(b))
+    dev = torch.device(device)
+    t_off = torch.as_tensor(off, dtype=torch.int64, device=dev)
+    t_b = torch.as_tensor(np.concatenate([np.asarray(b, np.int32) for b, _ in calls]),
+                          dtype=torch.int32, device=dev)
+    t_k = torch.as_tensor(np.concatenate([np.asarray(kv, np.int64) for _, kv in calls]),
+                          dtype=torch.int64, device=dev)
+    n = len(calls)
+    t_pos = torch.empty(n, dtype=torch.int32, device=dev)
+    t_fb = torch.empty(n, dtype=torch.uint8, device=dev)
+    t_th = torch.empty(n, dtype=torch.float64, device=dev)
+    b = DecodeBatch(n_calls=n, unit_off=t_off.data_ptr(), batch=t_b.data_ptr(), kv=t_k.data_ptr(),
+                    k=float(k), pos_out=t_pos.data_ptr(), fallback_out=t_fb.data_ptr(),
+                    threshold_out=t_th.data_ptr())
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    _check(lib().sbs_decode_select(C.byref(b), C.c_void_p(stream)))
+    return t_pos.cpu().numpy(), t_fb.cpu().numpy().astype(bool), t_th.cpu().numpy()

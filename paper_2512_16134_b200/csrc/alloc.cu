@@ -1,0 +1,243 @@
+// Batched allocation kernels — the allocation step as its own sm_100a kernel.
+//
+//  pbaa_kernel   : allocate_batch (prefill_alloc.cpp:61-88, Basic mode) over a
+//                  CSR batch of cluster-windows, one warp per window.  Each
+//                  queue is sorted by (prompt_len desc, id asc) with a warp
+//                  bitonic sort in shared memory, then placed greedily: a
+//                  REDUX-max over the DP capacities staged in shared memory
+//                  gives argmax c_avail (== argmax capacity_after in Basic
+//                  mode), lowest index on ties, guarded by c_avail > 0.
+//  iqr_kernel    : select_decode_unit (decode_alloc.cpp:38-81), one warp per
+//                  call: K staged and sorted in shared memory, Q1/Q3 by the
+//                  reference's FP64 interpolation, IQR mask, lex-min (B, K).
+//
+// No tensor cores: this is integer sorting/selection, HBM/latency bound.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "warp.cuh"
+
+namespace sbs {
+
+constexpr int kAllocWarps = 4;
+constexpr int kAllocMaxReq = 1024;  // per window (shared-memory sort)
+constexpr int kAllocMaxDp = 1024;
+constexpr int kIqrMaxUnits = 2048;
+
+// Lexicographic ascending sort of (a, b) pairs in shared memory by a warp.
+__device__ void warp_sort_pairs(uint64_t* a, uint64_t* b, int* idx, int n) {
+  const int lane = lane_id();
+  if (n <= 1) return;
+  int m = 1;
+  while (m < n) m <<= 1;
+  for (int i = n + lane; i < m; i += 32) { a[i] = UINT64_MAX; b[i] = UINT64_MAX; idx[i] = -1; }
+  __syncwarp();
+  for (int k = 2; k <= m; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = lane; i < (m >> 1); i += 32) {
+        int x = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+        int y = x | j;
+        bool up = (x & k) == 0;
+        uint64_t ax = a[x], ay = a[y], bx = b[x], by = b[y];
+        bool gt = ax > ay || (ax == ay && bx > by);
+        if (gt == up) {
+          a[x] = ay; a[y] = ax; b[x] = by; b[y] = bx;
+          int t = idx[x]; idx[x] = idx[y]; idx[y] = t;
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+struct PbaaArgs {
+  int32_t n_windows;
+  const int64_t* req_off;
+  const int32_t* n_pending;
+  const int64_t* dp_off;
+  const int32_t* n_limit;
+  const int64_t* req_id;
+  const int64_t* prompt_len;
+  const int32_t* wait_in;
+  int64_t* caps;
+  int32_t* out_dp;
+  int32_t* out_rank;
+  int32_t* wait_out;
+  uint8_t* flow;
+  int32_t* error;
+};
+
+__global__ void __launch_bounds__(32 * kAllocWarps) pbaa_kernel(PbaaArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int w = blockIdx.x * kAllocWarps + warp;
+  if (w >= A.n_windows) return;
+  unsigned char* my = smem + warp * (kAllocMaxReq * 20 + kAllocMaxDp * 8);
+  uint64_t* ka = (uint64_t*)my;
+  uint64_t* kb = ka + kAllocMaxReq;
+  int* ki = (int*)(kb + kAllocMaxReq);
+  int64_t* cap = (int64_t*)(ki + kAllocMaxReq);
+
+  const int64_t r0 = A.req_off[w], r1 = A.req_off[w + 1];
+  const int n = (int)(r1 - r0);
+  const int npend = A.n_pending[w];
+  const int64_t c0 = A.dp_off[w];
+  const int D = (int)(A.dp_off[w + 1] - c0);
+  const int nlim = A.n_limit[w];
+  if (n > kAllocMaxReq || D > kAllocMaxDp || npend > n || D < 1) {
+    if (lane == 0) atomicExch(A.error, 4);
+    return;
+  }
+  for (int d = lane; d < D; d += 32) cap[d] = A.caps[c0 + d];
+  __syncwarp();
+
+  int rank = 0;
+  bool stopped = false;
+  bool any_thr = false;
+  for (int phase = 0; phase < 2; ++phase) {
+    const int q0 = phase == 0 ? 0 : npend;
+    const int qn = phase == 0 ? npend : n - npend;
+    for (int i = lane; i < qn; i += 32) {
+      int64_t r = r0 + q0 + i;
+      ka[i] = (uint64_t)(INT64_MAX - A.prompt_len[r]);  // prompt desc
+      kb[i] = (uint64_t)A.req_id[r];                    // id asc
+      ki[i] = q0 + i;
+    }
+    __syncwarp();
+    warp_sort_pairs(ka, kb, ki, qn);
+    int i = 0;
+    while (i < qn && !stopped) {
+      int pos = ki[i];
+      int64_t len = A.prompt_len[r0 + pos];
+      // argmax c_avail over D, lowest index on ties (capacity_after = c_avail - len)
+      int64_t bv = INT64_MIN;
+      int bd = 0x7fffffff;
+      for (int d = lane; d < D; d += 32) {
+        int64_t c = cap[d];
+        if (c > bv) { bv = c; bd = d; }
+      }
+      int64_t mv = warp_max_i64(bv);
+      int best = (int)__reduce_min_sync(kFull, bv == mv ? (uint32_t)bd : 0x7fffffffu);
+      if (mv <= 0) { stopped = true; break; }  // guard: c_avail[best] > 0
+      if (lane == 0) {
+        cap[best] = mv - len;
+        A.out_dp[r0 + pos] = best;
+        A.out_rank[r0 + pos] = rank;
+        A.wait_out[r0 + pos] = A.wait_in[r0 + pos];
+      }
+      __syncwarp();
+      rank += 1;
+      i += 1;
+    }
+    // deferred suffix [i, qn): age; throttle beyond n_limit
+    for (int j = i + lane; j < qn; j += 32) {
+      int pos = ki[j];
+      int wv = A.wait_in[r0 + pos] + 1;
+      bool thr = wv > nlim;
+      A.out_dp[r0 + pos] = thr ? -2 : -1;
+      A.out_rank[r0 + pos] = -1;
+      A.wait_out[r0 + pos] = wv;
+      any_thr |= thr;
+    }
+    __syncwarp();
+  }
+  any_thr = __any_sync(kFull, any_thr);
+  for (int d = lane; d < D; d += 32) A.caps[c0 + d] = cap[d];
+  if (lane == 0) A.flow[w] = any_thr ? 1 : 0;
+}
+
+struct IqrArgs {
+  int32_t n_calls;
+  const int64_t* unit_off;
+  const int32_t* batch;
+  const int64_t* kv;
+  double k;
+  int32_t* pos_out;
+  uint8_t* fallback_out;
+  double* threshold_out;
+  int32_t* error;
+};
+
+__device__ __forceinline__ double pct_sorted_f(const int64_t* S, int n, double p) {
+  double rank = __ddiv_rn(__dmul_rn((double)n - 1.0, p), 100.0);
+  int lo = (int)floor(rank), hi = (int)ceil(rank);
+  double vlo = (double)S[lo];
+  if (lo == hi) return vlo;
+  double frac = __dsub_rn(rank, (double)lo);
+  return __dadd_rn(vlo, __dmul_rn(frac, __dsub_rn((double)S[hi], vlo)));
+}
+
+__global__ void __launch_bounds__(32 * kAllocWarps) iqr_kernel(IqrArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int c = blockIdx.x * kAllocWarps + warp;
+  if (c >= A.n_calls) return;
+  int64_t* S = (int64_t*)(smem + warp * kIqrMaxUnits * 8);
+  const int64_t u0 = A.unit_off[c];
+  const int n = (int)(A.unit_off[c + 1] - u0);
+  if (n < 1 || n > kIqrMaxUnits) {
+    if (lane == 0) atomicExch(A.error, n < 1 ? 3 : 4);
+    return;
+  }
+  // K -> double is monotone, so sorting int64 K == sorting the doubles.
+  // Keys are offset by 2^63 so negative K would also order correctly.
+  for (int i = lane; i < n; i += 32) S[i] = A.kv[u0 + i];
+  __syncwarp();
+  uint64_t* SU = (uint64_t*)S;
+  for (int i = lane; i < n; i += 32) SU[i] ^= 0x8000000000000000ull;
+  __syncwarp();
+  warp_sort_buf(SU, n);
+  for (int i = lane; i < n; i += 32) SU[i] ^= 0x8000000000000000ull;
+  __syncwarp();
+  double q1 = pct_sorted_f(S, n, 25.0);
+  double q3 = pct_sorted_f(S, n, 75.0);
+  double th = __dadd_rn(q3, __dmul_rn(A.k, __dsub_rn(q3, q1)));
+  int nsafe = 0;
+  for (int i = lane; i < n; i += 32) nsafe += ((double)A.kv[u0 + i] <= th) ? 1 : 0;
+  nsafe = __reduce_add_sync(kFull, nsafe);
+  const bool fallback = nsafe == 0;
+  int32_t bb = 0x7fffffff;
+  int64_t bk = kInf64;
+  int bp = 0x7fffffff;
+  for (int i = lane; i < n; i += 32) {
+    int64_t kv = A.kv[u0 + i];
+    if (!fallback && !((double)kv <= th)) continue;
+    int32_t b = A.batch[u0 + i];
+    if (b < bb || (b == bb && kv < bk)) { bb = b; bk = kv; bp = i; }
+  }
+  // B >= 0 in the reference (core.h:145); order B as signed via offset
+  uint32_t ob = (uint32_t)bb ^ 0x80000000u;
+  uint32_t mb = __reduce_min_sync(kFull, ob);
+  int64_t ck = (ob == mb) ? bk : kInf64;
+  int64_t mk = warp_min_i64(ck);
+  uint32_t cp = (ob == mb && bk == mk) ? (uint32_t)bp : 0xffffffffu;
+  int pos = (int)__reduce_min_sync(kFull, cp);
+  if (lane == 0) {
+    A.pos_out[c] = pos;
+    if (A.fallback_out) A.fallback_out[c] = fallback ? 1 : 0;
+    if (A.threshold_out) A.threshold_out[c] = th;
+  }
+}
+
+cudaError_t launch_pbaa(const PbaaArgs& a, cudaStream_t st) {
+  const int smem = kAllocWarps * (kAllocMaxReq * 20 + kAllocMaxDp * 8);
+  cudaError_t e = cudaFuncSetAttribute(pbaa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int blocks = (a.n_windows + kAllocWarps - 1) / kAllocWarps;
+  if (blocks == 0) return cudaSuccess;
+  pbaa_kernel<<<blocks, 32 * kAllocWarps, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_iqr(const IqrArgs& a, cudaStream_t st) {
+  const int smem = kAllocWarps * kIqrMaxUnits * 8;
+  cudaError_t e = cudaFuncSetAttribute(iqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int blocks = (a.n_calls + kAllocWarps - 1) / kAllocWarps;
+  if (blocks == 0) return cudaSuccess;
+  iqr_kernel<<<blocks, 32 * kAllocWarps, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace sbs

@@ -1,0 +1,94 @@
+// Device-side replica descriptors shared by sbs_host.cpp and des.cu.
+//
+// One DevPoint describes one independent replica (= one run_experiment call of
+// the reference, simulation.cpp:537): its cluster and engine constants, its
+// trace (SoA, shared between replicas with the same (seed, workload)), its
+// fault plan, and its private HBM arena.  Layout in HBM per replica:
+//   per-request timestamps   3 x int64 x N  (dispatch, prefill_start, first_token)
+//   [parity] completion int64 x N, status int8 x N
+//   TTFT window buffer       int64 x N      (exact p50/p95 order statistics)
+//   q_pending double buffer  2 x (u64 key + i32 wait) x QP
+//   window scratch           u64 x QW       (only when a window exceeds smem)
+//   prefill DP FIFOs         (P*D) x F x int2 {request id, tokens left}
+//   decode completion ring   Dn x R x BC x int4 {id, unit, kv release, excess}
+//   decode waiters           u64 x QD
+//   mt19937_64 state         312 x u64      (decode policy "random" only)
+#pragma once
+#include <stdint.h>
+
+namespace sbs {
+
+constexpr int kMaxInstances = 32;   // per pool (one lane per instance)
+constexpr int kMaxPrefillDp = 128;  // 4 DP units per lane
+constexpr int kMaxWSize = 1024;     // exec-window ring in shared memory
+constexpr int kSmemWinKeys = 256;   // window keys kept in shared memory
+constexpr int kHistBins = 64;
+
+enum Policy : int32_t { kSbs = 0, kImmediate = 1, kRoundRobin = 2, kLeastOutstanding = 3 };
+enum DecodePolicy : int32_t { kIqr = 0, kRandom = 1, kDecRoundRobin = 2 };
+enum Status : int8_t {
+  kStPending = 0, kStDispatched = 1, kStPrefilling = 2, kStDecoding = 3,
+  kStCompleted = 4, kStThrottled = 5
+};
+
+struct DevPoint {
+  // ---- dimensions
+  int32_t P, Dn, D, Dd, U;  // prefill inst, decode inst, prefill DP, decode DP, Dn*Dd
+  int32_t policy, decode_policy, n_limit, cap_batch;
+  int32_t n_topo, n_drops, w_size;
+  int32_t per_request;      // parity mode: also write completion + status
+  int32_t _pad0;
+  // ---- constants (integer ns, FP64 engine coefficients)
+  int64_t c_chunk, t_default, l_net, tps, horizon, warmup;
+  double iqr_k, wd_mult, pf_base, pf_tok, dc_base, dc_req, dc_kv;
+  uint64_t rng_seed;
+  int64_t N;
+  // ---- trace (SoA)
+  const int64_t* arr;
+  const int32_t* prompt;
+  const int32_t* output;
+  // ---- faults
+  const int64_t* topo_time;  // sorted by (time, config order)
+  const int32_t* topo_inst;
+  const int32_t* topo_healthy;
+  const int64_t* drop_from;
+  const int64_t* drop_until;
+  const int32_t* drop_inst;
+  int64_t death[2 * kMaxInstances];  // by instance id, INT64_MAX = never
+  // ---- arena
+  int64_t* o_dispatch;
+  int64_t* o_pstart;
+  int64_t* o_ftok;
+  int64_t* o_comp;     // parity only
+  int8_t* o_status;    // parity only
+  int64_t* ttft;
+  uint64_t* pend_key[2];
+  int32_t* pend_wait[2];
+  uint64_t* wscr;
+  int2* fifo;
+  int4* buckets;
+  uint64_t* dwait;
+  uint64_t* mt;
+  int64_t* tpot_hist;  // kHistBins
+  int32_t QP, QW, F, R, BC, QD;
+  // ---- shared-memory carve (bytes, relative to the warp's slice)
+  int32_t sm_pf_out, sm_pf_head, sm_pf_tail, sm_pf_rel, sm_pf_part;
+  int32_t sm_dK, sm_dS, sm_dB, sm_dnst, sm_ulist, sm_bcnt, sm_wring, sm_wkeys;
+  int32_t sm_bytes;
+  int32_t _pad1;
+};
+
+struct DevResult {
+  int64_t completed, throttled, cw, wr, passes, steps, out_tokens;
+  int64_t wd_fires, dropped, rejected, deferrals, flow, mask, fallback;
+  int64_t alloc_calls, dec_selects, events, n_ttft;
+  int64_t ttft_sum, sched_sum, dev_sum;
+  double util_sum, kv_mean_sum, kv_sigma_sum, tpot_sum;
+  int64_t kv_n, tpot_n;
+  int64_t ttft_sel[4];  // order statistics at ranks lo50, hi50, lo95, hi95
+  int64_t ttft_hist[kHistBins];
+  int32_t error;
+  int32_t _pad;
+};
+
+}  // namespace sbs

@@ -1,0 +1,929 @@
+// Host side of the B200 SBS hot path: the C-ABI declared in include/sbs_b200.h.
+//
+//  * sbs_generate_workload: restates generate_workload / workload_digest
+//    (workload.cpp:19-162) with the same libstdc++ mt19937_64 and glibc libm
+//    calls, so traces are bit-identical to the reference's on this image.
+//  * sbs_sim_*: validates experiments like validate() (core.cpp:79-114) and
+//    setup_faults() (simulation.cpp:93-120), lays out one HBM arena per
+//    replica, uploads traces once per unique trace, launches the persistent
+//    DES kernel, and turns the device counters into Aggregates with the same
+//    formulas as MetricsCollector::finalize (metrics.cpp:103-190).
+//  * sbs_prefill_allocate / sbs_decode_select: batched allocation kernels.
+//
+// Built with -ffp-contract=off: every FP64 expression that feeds an integer
+// timestamp must round exactly like the reference's x86-64 build.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/sbs_b200.h"
+#include "des_types.h"
+
+namespace sbs {
+cudaError_t launch_des(const DevPoint* d_pts, int n_pts, int* d_counter, DevResult* d_res,
+                       int smem_per_warp, int warps_per_block, int n_blocks, cudaStream_t st);
+struct PbaaArgs {
+  int32_t n_windows;
+  const int64_t* req_off;
+  const int32_t* n_pending;
+  const int64_t* dp_off;
+  const int32_t* n_limit;
+  const int64_t* req_id;
+  const int64_t* prompt_len;
+  const int32_t* wait_in;
+  int64_t* caps;
+  int32_t* out_dp;
+  int32_t* out_rank;
+  int32_t* wait_out;
+  uint8_t* flow;
+  int32_t* error;
+};
+struct IqrArgs {
+  int32_t n_calls;
+  const int64_t* unit_off;
+  const int32_t* batch;
+  const int64_t* kv;
+  double k;
+  int32_t* pos_out;
+  uint8_t* fallback_out;
+  double* threshold_out;
+  int32_t* error;
+};
+cudaError_t launch_pbaa(const PbaaArgs& a, cudaStream_t st);
+cudaError_t launch_iqr(const IqrArgs& a, cudaStream_t st);
+}  // namespace sbs
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+struct Error {
+  int code;
+  std::string msg;
+};
+
+#define CUDA_OR_THROW(x)                                                              \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess)                                                            \
+      throw Error{SBS_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)};     \
+  } while (0)
+
+int64_t seconds_to_ns(double s) { return static_cast<int64_t>(std::llround(s * 1e9)); }
+
+// ------------------------- workload (workload.cpp) -------------------------
+constexpr double kTwoPi = 6.283185307179586476925286766559;
+
+inline double u01(std::mt19937_64& rng) {
+  return static_cast<double>(rng() >> 11) * 0x1.0p-53;
+}
+inline double standard_normal(std::mt19937_64& rng) {
+  double a = u01(rng);
+  double b = u01(rng);
+  double r = std::sqrt(-2.0 * std::log(1.0 - a));
+  return r * std::cos(kTwoPi * b);
+}
+inline double exponential(std::mt19937_64& rng, double rate) {
+  return -std::log(1.0 - u01(rng)) / rate;
+}
+int64_t sample_length(const sbs_length_spec& s, std::mt19937_64& rng) {
+  switch (s.dist) {
+    case SBS_LEN_CONSTANT:
+      return std::max<int64_t>(1, s.value);
+    case SBS_LEN_UNIFORM: {
+      int64_t lo = std::max<int64_t>(1, s.min);
+      int64_t hi = std::max(lo, s.max);
+      double span = static_cast<double>(hi - lo + 1);
+      int64_t off = static_cast<int64_t>(u01(rng) * span);
+      return lo + std::min(off, hi - lo);
+    }
+    case SBS_LEN_LOGNORMAL: {
+      double v = std::exp(s.mu + s.sigma * standard_normal(rng));
+      int64_t t = static_cast<int64_t>(std::llround(v));
+      return std::clamp(t, std::max<int64_t>(1, s.min), s.max);
+    }
+  }
+  throw Error{SBS_ERR_INVARIANT, "sample_length: unknown distribution"};
+}
+
+void check_workload(const sbs_workload& w) {
+  if (!(w.rate_qps > 0)) throw Error{SBS_ERR_CONFIG, "workload rate_qps must be > 0"};
+  if (!(w.duration_s > 0)) throw Error{SBS_ERR_CONFIG, "workload duration_s must be > 0"};
+  if (w.shared_prefix_fraction < 0 || w.shared_prefix_fraction > 1)
+    throw Error{SBS_ERR_CONFIG, "shared_prefix_fraction must be in [0, 1]"};
+  if (w.shared_prefix_fraction > 0)
+    throw Error{SBS_ERR_CONFIG,
+                "shared prefixes (cache-aware mode) are out of scope of the GPU path"};
+  if (w.initial_burst < 0) throw Error{SBS_ERR_CONFIG, "workload initial_burst must be >= 0"};
+}
+
+struct HostTrace {
+  std::vector<int64_t> arr;
+  std::vector<int32_t> prompt, output;
+  uint64_t digest = 0;
+};
+
+void mix_digest(uint64_t& h, uint64_t v) {
+  for (int b = 0; b < 8; ++b) {
+    h ^= (v >> (8 * b)) & 0xff;
+    h *= 1099511628211ull;
+  }
+}
+
+// generate_workload (workload.cpp:67-142) + workload_digest (:144-162).
+void generate(const sbs_workload& spec, uint64_t seed, HostTrace& out) {
+  check_workload(spec);
+  std::mt19937_64 rng(seed);
+  const int64_t horizon = seconds_to_ns(spec.duration_s);
+  const double slot = 1.0 / spec.rate_qps;
+  std::vector<double> arrivals(static_cast<size_t>(spec.initial_burst), 0.0);
+  switch (spec.process) {
+    case SBS_ARRIVAL_POISSON: {
+      double t = exponential(rng, spec.rate_qps);
+      while (t < spec.duration_s) {
+        arrivals.push_back(t);
+        t += exponential(rng, spec.rate_qps);
+      }
+      break;
+    }
+    case SBS_ARRIVAL_UNIFORM:
+      for (size_t n = 0;; ++n) {
+        double t = static_cast<double>(n) * slot;
+        if (t >= spec.duration_s) break;
+        arrivals.push_back(t);
+      }
+      break;
+    case SBS_ARRIVAL_UNIFORM_JITTER:
+      for (size_t n = 0;; ++n) {
+        double base = static_cast<double>(n) * slot;
+        if (base >= spec.duration_s) break;
+        double t = base + u01(rng) * slot;
+        if (t < spec.duration_s) arrivals.push_back(t);
+      }
+      break;
+    default:
+      throw Error{SBS_ERR_CONFIG, "workload.process must be poisson, uniform, or uniform_jitter"};
+  }
+  const size_t n = arrivals.size();
+  out.arr.resize(n);
+  out.prompt.resize(n);
+  out.output.resize(n);
+  uint64_t h = 14695981039346656037ull;
+  for (size_t i = 0; i < n; ++i) {
+    int64_t at = std::min(seconds_to_ns(arrivals[i]), horizon - 1);
+    int64_t p = sample_length(spec.prompt, rng);
+    int64_t o = spec.output.dist == SBS_LEN_CONSTANT ? std::max<int64_t>(0, spec.output.value)
+                                                      : sample_length(spec.output, rng);
+    if (p > 0x3fffffff || o > 0x3fffffff)
+      throw Error{SBS_ERR_CONFIG, "request lengths above 2^30 tokens are not supported"};
+    out.arr[i] = at;
+    out.prompt[i] = static_cast<int32_t>(p);
+    out.output[i] = static_cast<int32_t>(o);
+    mix_digest(h, static_cast<uint64_t>(at));
+    mix_digest(h, static_cast<uint64_t>(p));
+    mix_digest(h, static_cast<uint64_t>(o));
+    mix_digest(h, 0);  // no shared prefix: front()+1 term is 0
+    mix_digest(h, 0);  // prefix size
+  }
+  out.digest = h;
+}
+
+// ------------------------- validation (core.cpp:79-114) ---------------------
+void validate(const sbs_experiment& x) {
+  const sbs_cluster& c = x.cluster;
+  auto require = [](bool ok, const char* what) {
+    if (!ok) throw Error{SBS_ERR_CONFIG, what};
+  };
+  require(c.n_instances_prefill >= 1, "n_instances_prefill must be >= 1");
+  require(c.n_instances_decode >= 1, "n_instances_decode must be >= 1");
+  require(c.dp_degree >= 1, "dp_degree must be >= 1");
+  require(c.dp_degree_decode >= 0, "dp_degree_decode must be >= 0");
+  require(c.c_chunk >= 1, "c_chunk must be >= 1");
+  require(c.t_default_s > 0, "t_default_s must be > 0");
+  require(c.w_size >= 1, "w_size must be >= 1");
+  require(c.l_net_s >= 0, "l_net_s must be >= 0");
+  require(c.n_limit >= 0, "n_limit must be >= 0");
+  require(c.iqr_k >= 0, "iqr_k must be >= 0");
+  require(c.watchdog_multiplier > 0, "watchdog_multiplier must be > 0");
+  require(c.prefill_base_s >= 0, "prefill_base_s must be >= 0");
+  require(c.prefill_per_token_s >= 0, "prefill_per_token_s must be >= 0");
+  require(c.decode_base_s >= 0, "decode_base_s must be >= 0");
+  require(c.decode_per_request_s >= 0, "decode_per_request_s must be >= 0");
+  require(c.decode_per_kv_token_s >= 0, "decode_per_kv_token_s must be >= 0");
+  require(c.decode_tokens_per_step >= 1, "decode_tokens_per_step must be >= 1");
+  require(c.decode_max_batch_per_dp >= 0, "decode_max_batch_per_dp must be >= 0");
+  require(x.warmup_fraction >= 0.0 && x.warmup_fraction < 1.0,
+          "sim.warmup_fraction must be in [0, 1)");
+  // GPU-path envelope (documented in DESIGN.md)
+  require(c.cache_enabled == 0 && x.prefill_mode == SBS_ALLOC_BASIC,
+          "cache-aware prefill allocation is out of scope of the GPU path");
+  require(c.n_instances_prefill <= sbs::kMaxInstances && c.n_instances_decode <= sbs::kMaxInstances,
+          "GPU path supports at most 32 prefill and 32 decode instances");
+  require(c.dp_degree <= sbs::kMaxPrefillDp, "GPU path supports dp_degree <= 128");
+  require(c.c_chunk <= 0x7fffffff, "GPU path supports c_chunk < 2^31");
+  require(c.w_size <= sbs::kMaxWSize, "GPU path supports w_size <= 1024");
+  require(x.policy >= 0 && x.policy <= 3, "scheduler.policy out of range");
+  require(x.decode_policy >= 0 && x.decode_policy <= 2, "scheduler.decode_policy out of range");
+  int dd = c.dp_degree_decode > 0 ? c.dp_degree_decode : c.dp_degree;
+  require((int64_t)dd * c.n_instances_decode <= 16384, "GPU path supports <= 16384 decode units");
+  const int n_inst = c.n_instances_prefill + c.n_instances_decode;
+  for (int i = 0; i < x.n_deads; ++i)
+    if (x.deads[i].instance < 0 || x.deads[i].instance >= n_inst)
+      throw Error{SBS_ERR_CONFIG, "faults.dead: instance out of range"};
+  for (int i = 0; i < x.n_topology; ++i) {
+    if (x.topology[i].instance < 0 || x.topology[i].instance >= n_inst)
+      throw Error{SBS_ERR_CONFIG, "faults.topology: instance out of range"};
+    if (seconds_to_ns(x.topology[i].time_s) < 0)
+      throw Error{SBS_ERR_INVARIANT, "SimClock::schedule: event time is before now"};
+  }
+  for (int i = 0; i < x.n_drops; ++i)
+    if (x.drops[i].instance != -1 && (x.drops[i].instance < 0 || x.drops[i].instance >= n_inst))
+      throw Error{SBS_ERR_CONFIG, "faults.drop_end_forward: instance out of range"};
+}
+
+int64_t next_pow2(int64_t v) {
+  int64_t p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+struct TraceDev {
+  int64_t* arr = nullptr;
+  int32_t* prompt = nullptr;
+  int32_t* output = nullptr;
+  int64_t n = 0;
+  int32_t max_output = 0;
+  uint64_t digest = 0;
+};
+
+struct PointHost {
+  sbs_experiment x;  // copy (fault pointers re-pointed into owned vectors)
+  std::vector<sbs_drop_fault> drops;
+  std::vector<sbs_dead_fault> deads;
+  std::vector<sbs_topology_fault> topo;
+  int trace = 0;
+  // capacities (grown on overflow)
+  int32_t F = 0, QP = 0, QW = 0, BC = 0, QD = 0;
+  void* arena = nullptr;
+  size_t arena_bytes = 0;
+  void* fault_buf = nullptr;
+  sbs::DevPoint dp{};
+  double cost = 0;
+};
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+}  // namespace
+
+struct sbs_sim {
+  int device = 0;
+  uint32_t flags = 0;
+  std::vector<PointHost> pts;
+  std::vector<TraceDev> traces;
+  std::vector<int> order;  // device slot -> point index (cost-descending)
+  sbs::DevPoint* d_pts = nullptr;
+  sbs::DevResult* d_res = nullptr;
+  int* d_counter = nullptr;
+  std::vector<sbs::DevResult> h_res;
+  int smem_per_warp = 0;
+  int warps_per_block = 4;
+  int n_blocks = 0;
+  int64_t device_bytes = 0;
+  int sm_count = 148;
+};
+
+namespace {
+
+void free_point(PointHost& p) {
+  if (p.arena) cudaFree(p.arena);
+  if (p.fault_buf) cudaFree(p.fault_buf);
+  p.arena = nullptr;
+  p.fault_buf = nullptr;
+}
+
+// Shared-memory carve for one replica (must match des.cu).
+void layout_smem(sbs::DevPoint& d) {
+  size_t off = 0;
+  const size_t PD = (size_t)d.P * d.D, U = (size_t)d.U;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + bytes, 16);
+    return (int32_t)o;
+  };
+  d.sm_pf_out = take(8 * PD);
+  d.sm_pf_head = take(4 * PD);
+  d.sm_pf_tail = take(4 * PD);
+  d.sm_pf_rel = take(4 * PD);
+  d.sm_pf_part = take(PD);
+  d.sm_dK = take(8 * U);
+  d.sm_dS = take(8 * (size_t)next_pow2((int64_t)std::max<size_t>(U, 1)));
+  d.sm_dB = take(4 * U);
+  d.sm_dnst = take(4 * U);
+  d.sm_ulist = take(2 * U);
+  d.sm_bcnt = take(2 * (size_t)d.Dn * d.R);
+  d.sm_wring = take(8 * (size_t)d.w_size);
+  d.sm_wkeys = take(8 * (size_t)sbs::kSmemWinKeys);
+  d.sm_bytes = (int32_t)off;
+}
+
+void build_point(sbs_sim& s, PointHost& p) {
+  const sbs_experiment& x = p.x;
+  const sbs_cluster& c = x.cluster;
+  const TraceDev& t = s.traces[p.trace];
+  sbs::DevPoint& d = p.dp;
+  std::memset(&d, 0, sizeof(d));
+  d.P = c.n_instances_prefill;
+  d.Dn = c.n_instances_decode;
+  d.D = c.dp_degree;
+  d.Dd = c.dp_degree_decode > 0 ? c.dp_degree_decode : c.dp_degree;
+  d.U = d.Dn * d.Dd;
+  d.policy = x.policy == SBS_POLICY_ROUND_ROBIN ? sbs::kImmediate : x.policy;
+  d.decode_policy = x.decode_policy;
+  d.n_limit = c.n_limit;
+  d.cap_batch = c.decode_max_batch_per_dp;
+  d.w_size = (int32_t)c.w_size;
+  d.per_request = (s.flags & SBS_FLAG_PER_REQUEST) ? 1 : 0;
+  d.c_chunk = c.c_chunk;
+  d.t_default = seconds_to_ns(c.t_default_s);
+  d.l_net = seconds_to_ns(c.l_net_s);
+  d.tps = c.decode_tokens_per_step;
+  d.horizon = seconds_to_ns(x.workload.duration_s);
+  d.warmup = seconds_to_ns(x.workload.duration_s * x.warmup_fraction);
+  d.iqr_k = c.iqr_k;
+  d.wd_mult = c.watchdog_multiplier;
+  d.pf_base = c.prefill_base_s;
+  d.pf_tok = c.prefill_per_token_s;
+  d.dc_base = c.decode_base_s;
+  d.dc_req = c.decode_per_request_s;
+  d.dc_kv = c.decode_per_kv_token_s;
+  d.rng_seed = x.seed ^ 0x9E3779B97F4A7C15ULL;
+  d.N = t.n;
+  d.arr = t.arr;
+  d.prompt = t.prompt;
+  d.output = t.output;
+  // decode completion ring: strictly more buckets than steps a request lives
+  int64_t max_target = std::max<int64_t>(1, (int64_t)t.max_output - 1);
+  int64_t max_steps = (max_target + c.decode_tokens_per_step - 1) / c.decode_tokens_per_step;
+  d.R = (int32_t)next_pow2(max_steps + 1);
+  if ((int64_t)d.R * d.Dn > (1 << 16)) throw Error{SBS_ERR_CONFIG, "decode ring too large"};
+
+  // faults: deaths (min over entries), topology sorted by (time, order), drops
+  const int n_inst = d.P + d.Dn;
+  for (int i = 0; i < 2 * sbs::kMaxInstances; ++i) d.death[i] = INT64_MAX;
+  for (auto& f : p.deads) {
+    int64_t tt = seconds_to_ns(f.time_s);
+    // instance ids: prefill 0..P-1 map to lanes 0..P-1, decode P.. map to slots P..
+    d.death[f.instance] = std::min(d.death[f.instance], tt);
+  }
+  (void)n_inst;
+  // remap decode deaths into slot P + j (already, since id = P + j)
+  std::vector<std::pair<int64_t, int>> topo;
+  for (size_t i = 0; i < p.topo.size(); ++i) topo.emplace_back(seconds_to_ns(p.topo[i].time_s), (int)i);
+  std::stable_sort(topo.begin(), topo.end(),
+                   [](auto& a, auto& b) { return a.first < b.first; });
+  d.n_topo = (int32_t)topo.size();
+  d.n_drops = (int32_t)p.drops.size();
+  size_t fb = 8 * topo.size() + 8 * topo.size() + 16 * p.drops.size() + 8 * p.drops.size() + 64;
+  if (p.fault_buf == nullptr) CUDA_OR_THROW(cudaMalloc(&p.fault_buf, fb));
+  std::vector<unsigned char> hb(fb, 0);
+  size_t off = 0;
+  auto put = [&](const void* src, size_t bytes) {
+    size_t o = off;
+    std::memcpy(hb.data() + o, src, bytes);
+    off = align_up(off + bytes, 8);
+    return (unsigned char*)p.fault_buf + o;
+  };
+  std::vector<int64_t> tt(topo.size());
+  std::vector<int32_t> ti(topo.size()), th(topo.size());
+  for (size_t i = 0; i < topo.size(); ++i) {
+    tt[i] = topo[i].first;
+    ti[i] = p.topo[topo[i].second].instance;
+    th[i] = p.topo[topo[i].second].healthy ? 1 : 0;
+  }
+  std::vector<int64_t> dfrom(p.drops.size()), duntil(p.drops.size());
+  std::vector<int32_t> dinst(p.drops.size());
+  for (size_t i = 0; i < p.drops.size(); ++i) {
+    dfrom[i] = seconds_to_ns(p.drops[i].from_s);
+    duntil[i] = std::isfinite(p.drops[i].until_s) ? seconds_to_ns(p.drops[i].until_s) : INT64_MAX;
+    dinst[i] = p.drops[i].instance;
+  }
+  d.topo_time = (const int64_t*)put(tt.data(), 8 * tt.size());
+  d.topo_inst = (const int32_t*)put(ti.data(), 4 * ti.size());
+  d.topo_healthy = (const int32_t*)put(th.data(), 4 * th.size());
+  d.drop_from = (const int64_t*)put(dfrom.data(), 8 * dfrom.size());
+  d.drop_until = (const int64_t*)put(duntil.data(), 8 * duntil.size());
+  d.drop_inst = (const int32_t*)put(dinst.data(), 4 * dinst.size());
+  CUDA_OR_THROW(cudaMemcpy(p.fault_buf, hb.data(), fb, cudaMemcpyHostToDevice));
+
+  // arena
+  const int64_t N = std::max<int64_t>(t.n, 1);
+  const int64_t PD = (int64_t)d.P * d.D;
+  d.F = p.F;
+  d.QP = p.QP;
+  d.QW = p.QW;
+  d.BC = p.BC;
+  d.QD = p.QD;
+  size_t sz = 0;
+  auto carve = [&](size_t bytes) {
+    size_t o = sz;
+    sz = align_up(sz + bytes, 256);
+    return o;
+  };
+  size_t o_disp = carve(8 * N), o_ps = carve(8 * N), o_ft = carve(8 * N);
+  size_t o_comp = d.per_request ? carve(8 * N) : 0;
+  size_t o_st = d.per_request ? carve(N) : 0;
+  size_t o_ttft = carve(8 * N);
+  size_t o_pk0 = carve(8 * (size_t)p.QP), o_pk1 = carve(8 * (size_t)p.QP);
+  size_t o_pw0 = carve(4 * (size_t)p.QP), o_pw1 = carve(4 * (size_t)p.QP);
+  size_t o_ws = carve(8 * (size_t)p.QW);
+  size_t o_fifo = carve(8 * (size_t)PD * p.F);
+  size_t o_bk = carve(16 * (size_t)d.Dn * d.R * p.BC);
+  size_t o_dw = carve(8 * (size_t)p.QD);
+  size_t o_mt = carve(8 * 312);
+  size_t o_th = carve(8 * sbs::kHistBins);
+  if (p.arena == nullptr || p.arena_bytes < sz) {
+    if (p.arena) cudaFree(p.arena);
+    p.arena = nullptr;
+    CUDA_OR_THROW(cudaMalloc(&p.arena, sz));
+    p.arena_bytes = sz;
+  }
+  unsigned char* b = (unsigned char*)p.arena;
+  d.o_dispatch = (int64_t*)(b + o_disp);
+  d.o_pstart = (int64_t*)(b + o_ps);
+  d.o_ftok = (int64_t*)(b + o_ft);
+  d.o_comp = d.per_request ? (int64_t*)(b + o_comp) : nullptr;
+  d.o_status = d.per_request ? (int8_t*)(b + o_st) : nullptr;
+  d.ttft = (int64_t*)(b + o_ttft);
+  d.pend_key[0] = (uint64_t*)(b + o_pk0);
+  d.pend_key[1] = (uint64_t*)(b + o_pk1);
+  d.pend_wait[0] = (int32_t*)(b + o_pw0);
+  d.pend_wait[1] = (int32_t*)(b + o_pw1);
+  d.wscr = (uint64_t*)(b + o_ws);
+  d.fifo = (int2*)(b + o_fifo);
+  d.buckets = (int4*)(b + o_bk);
+  d.dwait = (uint64_t*)(b + o_dw);
+  d.mt = (uint64_t*)(b + o_mt);
+  d.tpot_hist = (int64_t*)(b + o_th);
+  layout_smem(d);
+  p.cost = (double)t.n * (1.0 + (double)d.U / 64.0) * (1.0 + (double)(d.P * d.D) / 256.0);
+}
+
+// Per-run reset of the parts of the arena the kernel reads before writing.
+void reset_point(const PointHost& p, cudaStream_t st) {
+  const sbs::DevPoint& d = p.dp;
+  CUDA_OR_THROW(cudaMemsetAsync(d.tpot_hist, 0, 8 * sbs::kHistBins, st));
+  if (d.per_request) {
+    CUDA_OR_THROW(cudaMemsetAsync(d.o_dispatch, 0xff, 8 * (size_t)d.N, st));
+    CUDA_OR_THROW(cudaMemsetAsync(d.o_pstart, 0xff, 8 * (size_t)d.N, st));
+    CUDA_OR_THROW(cudaMemsetAsync(d.o_ftok, 0xff, 8 * (size_t)d.N, st));
+    CUDA_OR_THROW(cudaMemsetAsync(d.o_comp, 0xff, 8 * (size_t)d.N, st));
+    CUDA_OR_THROW(cudaMemsetAsync(d.o_status, 0, (size_t)d.N, st));
+  }
+}
+
+void initial_caps(PointHost& p, const TraceDev& t) {
+  const sbs_cluster& c = p.x.cluster;
+  const int64_t PD = (int64_t)c.n_instances_prefill * c.dp_degree;
+  if (p.x.policy == SBS_POLICY_SBS) {
+    p.F = 256;
+  } else {
+    int64_t share = t.n / std::max<int64_t>(PD, 1) + 2;
+    p.F = (int32_t)next_pow2(std::max<int64_t>(64, std::min<int64_t>(share * 2, 1 << 20)));
+  }
+  p.QP = 4096;
+  p.QW = 4096;
+  p.BC = 64;
+  p.QD = 1024;
+}
+
+void grow_caps(PointHost& p) {
+  p.F = std::min<int32_t>(p.F * 2, 1 << 24);
+  p.QP = std::min<int32_t>(p.QP * 2, 1 << 28);
+  p.QW = std::min<int32_t>(p.QW * 2, 1 << 28);
+  p.BC = std::min<int32_t>(p.BC * 2, 32768);
+  p.QD = std::min<int32_t>(p.QD * 2, 1 << 28);
+}
+
+void upload_points(sbs_sim& s) {
+  std::vector<sbs::DevPoint> h(s.order.size());
+  int smem = 0;
+  for (size_t i = 0; i < s.order.size(); ++i) {
+    h[i] = s.pts[s.order[i]].dp;
+    smem = std::max(smem, h[i].sm_bytes);
+  }
+  s.smem_per_warp = (int)align_up((size_t)smem, 128);
+  CUDA_OR_THROW(cudaMemcpy(s.d_pts, h.data(), sizeof(sbs::DevPoint) * h.size(),
+                           cudaMemcpyHostToDevice));
+  // occupancy: warps per block 4 unless shared memory forces fewer
+  const int max_smem_block = 227 * 1024;
+  int wpb = 4;
+  while (wpb > 1 && wpb * s.smem_per_warp > max_smem_block) wpb >>= 1;
+  if (s.smem_per_warp > max_smem_block)
+    throw Error{SBS_ERR_CONFIG, "replica state exceeds shared memory"};
+  s.warps_per_block = wpb;
+  int blocks_per_sm = std::max(1, std::min(16, (228 * 1024) / std::max(1, wpb * s.smem_per_warp + 1024)));
+  int max_blocks = s.sm_count * blocks_per_sm;
+  int need = (int)((s.order.size() + wpb - 1) / wpb);
+  s.n_blocks = std::max(1, std::min(need, max_blocks));
+}
+
+void do_upload_traces(sbs_sim& s, const sbs_trace* traces, cudaStream_t st) {
+  for (size_t i = 0; i < s.traces.size(); ++i) {
+    TraceDev& t = s.traces[i];
+    if (traces[i].n != t.n) throw Error{SBS_ERR_CONFIG, "trace shape changed"};
+    if (t.n == 0) continue;
+    CUDA_OR_THROW(cudaMemcpyAsync(t.arr, traces[i].arrival_ns, 8 * t.n, cudaMemcpyHostToDevice, st));
+    CUDA_OR_THROW(cudaMemcpyAsync(t.prompt, traces[i].prompt_len, 4 * t.n, cudaMemcpyHostToDevice, st));
+    CUDA_OR_THROW(cudaMemcpyAsync(t.output, traces[i].output_len, 4 * t.n, cudaMemcpyHostToDevice, st));
+  }
+}
+
+void finish_aggregates(const PointHost& p, const sbs::DevResult& r, sbs_aggregates& a) {
+  std::memset(&a, 0, sizeof(a));
+  const sbs::DevPoint& d = p.dp;
+  a.generated = (uint64_t)d.N;
+  a.completed = (uint64_t)r.completed;
+  a.throttled = (uint64_t)r.throttled;
+  a.in_flight = (uint64_t)(d.N - r.completed - r.throttled);
+  a.window_requests = (uint64_t)r.wr;
+  a.warmup_cutoff_s = (double)d.warmup / 1e9;
+  a.duration_s = (double)d.horizon / 1e9;
+  if (r.wr > 0) {
+    const double n = (double)r.wr;
+    a.ttft_mean_s = ((double)r.ttft_sum / 1e9) / n;
+    a.scheduler_wait_mean_s = ((double)r.sched_sum / 1e9) / n;
+    a.device_wait_mean_s = ((double)r.dev_sum / 1e9) / n;
+    a.total_wait_mean_s = ((double)r.sched_sum / 1e9 + (double)r.dev_sum / 1e9) / n;
+    // percentile (decode_alloc.cpp:13-23) from exact order statistics
+    auto pct = [&](int which, double pv) {
+      double rank = (n - 1.0) * pv / 100.0;
+      size_t lo = (size_t)std::floor(rank), hi = (size_t)std::ceil(rank);
+      double vlo = (double)r.ttft_sel[2 * which] / 1e9;
+      if (lo == hi) return vlo;
+      double vhi = (double)r.ttft_sel[2 * which + 1] / 1e9;
+      double frac = rank - (double)lo;
+      return vlo + frac * (vhi - vlo);
+    };
+    a.ttft_p50_s = pct(0, 50.0);
+    a.ttft_p95_s = pct(1, 95.0);
+  }
+  a.passes = (uint64_t)r.passes;
+  if (r.passes > 0) a.chunk_util_mean = r.util_sum / (double)r.passes;
+  a.decode_steps = (uint64_t)r.steps;
+  a.output_tokens = (uint64_t)r.out_tokens;
+  double window_s = (double)(d.horizon - d.warmup) / 1e9;
+  if (window_s > 0) {
+    a.output_tokens_per_s = (double)a.output_tokens / window_s;
+    a.completed_per_s = (double)r.cw / window_s;
+  }
+  if (r.kv_n > 0) {
+    a.kv_mean_time_avg = r.kv_mean_sum / (double)r.kv_n;
+    a.kv_sigma_time_avg = r.kv_sigma_sum / (double)r.kv_n;
+  }
+  a.watchdog_fires = (uint64_t)r.wd_fires;
+  a.dropped_end_forwards = (uint64_t)r.dropped;
+  a.rejected_samples = (uint64_t)r.rejected;
+  a.deferrals = (uint64_t)r.deferrals;
+  a.flow_control_events = (uint64_t)r.flow;
+  a.mask_events = (uint64_t)r.mask;
+  a.fallback_events = (uint64_t)r.fallback;
+  a.alloc_calls = (uint64_t)r.alloc_calls;
+  a.decode_selects = (uint64_t)r.dec_selects;
+  a.events = (uint64_t)r.events;
+  a.tpot_count = (uint64_t)r.tpot_n;
+  if (r.tpot_n > 0) a.tpot_mean_s = r.tpot_sum / (double)r.tpot_n;
+  a.ttft_sum_ns = r.ttft_sum;
+  a.sched_sum_ns = r.sched_sum;
+  a.device_sum_ns = r.dev_sum;
+  a.error = r.error;
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const Error& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return SBS_ERR_OVERFLOW;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SBS_ERR_INVARIANT;
+  }
+}
+
+int parallel_threads() {
+  unsigned hc = std::thread::hardware_concurrency();
+  return (int)std::max(1u, hc);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sbs_last_error(void) { return g_err.c_str(); }
+const char* sbs_version(void) { return "sbs_b200 0.1 (sm_100a)"; }
+
+int sbs_generate_workload(const sbs_workload* spec, uint64_t seed, int64_t* arrival_ns,
+                          int32_t* prompt_len, int32_t* output_len, int64_t cap, int64_t* n_out,
+                          uint64_t* digest) {
+  return guarded([&] {
+    HostTrace t;
+    generate(*spec, seed, t);
+    if (n_out) *n_out = (int64_t)t.arr.size();
+    if (digest) *digest = t.digest;
+    if (arrival_ns == nullptr) return SBS_OK;
+    if ((int64_t)t.arr.size() > cap) return fail(SBS_ERR_OVERFLOW, "trace capacity too small");
+    std::memcpy(arrival_ns, t.arr.data(), 8 * t.arr.size());
+    std::memcpy(prompt_len, t.prompt.data(), 4 * t.prompt.size());
+    std::memcpy(output_len, t.output.data(), 4 * t.output.size());
+    return SBS_OK;
+  });
+}
+
+int sbs_sim_create(const sbs_experiment* points, int32_t n_points, const sbs_trace* traces,
+                   int32_t n_traces, const int32_t* trace_of_point, uint32_t flags,
+                   int32_t device, sbs_sim** out) {
+  *out = nullptr;
+  sbs_sim* s = new sbs_sim();
+  int rc = guarded([&] {
+    if (n_points < 1) throw Error{SBS_ERR_CONFIG, "no points"};
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw Error{SBS_ERR_CUDA, "no CUDA device visible (the GPU path has no CPU fallback)"};
+    s->device = device;
+    s->flags = flags;
+    CUDA_OR_THROW(cudaSetDevice(device));
+    CUDA_OR_THROW(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, device));
+    // traces
+    s->traces.resize(n_traces);
+    for (int i = 0; i < n_traces; ++i) {
+      TraceDev& t = s->traces[i];
+      t.n = traces[i].n;
+      t.digest = traces[i].digest;
+      if (t.n >= (int64_t)1 << 31) throw Error{SBS_ERR_CONFIG, "trace longer than 2^31 requests"};
+      for (int64_t k = 0; k < t.n; ++k) t.max_output = std::max(t.max_output, traces[i].output_len[k]);
+      size_t n = (size_t)std::max<int64_t>(t.n, 1);
+      CUDA_OR_THROW(cudaMalloc(&t.arr, 8 * n));
+      CUDA_OR_THROW(cudaMalloc(&t.prompt, 4 * n));
+      CUDA_OR_THROW(cudaMalloc(&t.output, 4 * n));
+      s->device_bytes += (int64_t)(16 * n);
+    }
+    do_upload_traces(*s, traces, 0);
+    CUDA_OR_THROW(cudaDeviceSynchronize());
+    // points
+    s->pts.resize(n_points);
+    for (int i = 0; i < n_points; ++i) {
+      PointHost& p = s->pts[i];
+      p.x = points[i];
+      validate(p.x);
+      check_workload(p.x.workload);
+      p.drops.assign(points[i].drops, points[i].drops + points[i].n_drops);
+      p.deads.assign(points[i].deads, points[i].deads + points[i].n_deads);
+      p.topo.assign(points[i].topology, points[i].topology + points[i].n_topology);
+      p.trace = trace_of_point ? trace_of_point[i] : i;
+      if (p.trace < 0 || p.trace >= n_traces) throw Error{SBS_ERR_CONFIG, "trace index out of range"};
+      initial_caps(p, s->traces[p.trace]);
+      build_point(*s, p);
+      s->device_bytes += (int64_t)p.arena_bytes;
+    }
+    s->order.resize(n_points);
+    for (int i = 0; i < n_points; ++i) s->order[i] = i;
+    std::stable_sort(s->order.begin(), s->order.end(),
+                     [&](int a, int b) { return s->pts[a].cost > s->pts[b].cost; });
+    CUDA_OR_THROW(cudaMalloc(&s->d_pts, sizeof(sbs::DevPoint) * n_points));
+    CUDA_OR_THROW(cudaMalloc(&s->d_res, sizeof(sbs::DevResult) * n_points));
+    CUDA_OR_THROW(cudaMalloc(&s->d_counter, sizeof(int)));
+    s->h_res.resize(n_points);
+    upload_points(*s);
+    return SBS_OK;
+  });
+  if (rc != SBS_OK) {
+    sbs_sim_destroy(s);
+    return rc;
+  }
+  *out = s;
+  return SBS_OK;
+}
+
+int sbs_sim_upload_traces(sbs_sim* s, const sbs_trace* traces, void* stream) {
+  return guarded([&] {
+    CUDA_OR_THROW(cudaSetDevice(s->device));
+    do_upload_traces(*s, traces, (cudaStream_t)stream);
+    return SBS_OK;
+  });
+}
+
+int sbs_sim_launch(sbs_sim* s, void* stream) {
+  return guarded([&] {
+    cudaStream_t st = (cudaStream_t)stream;
+    CUDA_OR_THROW(cudaSetDevice(s->device));
+    for (auto& p : s->pts) reset_point(p, st);
+    CUDA_OR_THROW(sbs::launch_des(s->d_pts, (int)s->order.size(), s->d_counter, s->d_res,
+                                  s->smem_per_warp, s->warps_per_block, s->n_blocks, st));
+    return SBS_OK;
+  });
+}
+
+int32_t sbs_sim_launches_per_run(const sbs_sim* s) {
+  (void)s;
+  return 2;  // des_kernel + finalize_kernel (memsets are not kernels of ours)
+}
+
+int64_t sbs_sim_device_bytes(const sbs_sim* s) { return s->device_bytes; }
+
+int sbs_sim_results(sbs_sim* s, sbs_aggregates* out, sbs_histograms* hist, void* stream) {
+  return guarded([&] {
+    cudaStream_t st = (cudaStream_t)stream;
+    CUDA_OR_THROW(cudaSetDevice(s->device));
+    const int n = (int)s->order.size();
+    for (int attempt = 0;; ++attempt) {
+      CUDA_OR_THROW(cudaMemcpyAsync(s->h_res.data(), s->d_res, sizeof(sbs::DevResult) * n,
+                                    cudaMemcpyDeviceToHost, st));
+      CUDA_OR_THROW(cudaStreamSynchronize(st));
+      bool overflow = false;
+      for (int i = 0; i < n; ++i)
+        if (s->h_res[i].error == SBS_ERR_OVERFLOW) {
+          overflow = true;
+          PointHost& p = s->pts[s->order[i]];
+          grow_caps(p);
+          s->device_bytes -= (int64_t)p.arena_bytes;
+          build_point(*s, p);
+          s->device_bytes += (int64_t)p.arena_bytes;
+        }
+      if (!overflow) break;
+      if (attempt >= 12) throw Error{SBS_ERR_OVERFLOW, "device arena overflow persists"};
+      upload_points(*s);
+      for (auto& p : s->pts) reset_point(p, st);
+      CUDA_OR_THROW(sbs::launch_des(s->d_pts, n, s->d_counter, s->d_res, s->smem_per_warp,
+                                    s->warps_per_block, s->n_blocks, st));
+    }
+    int rc = SBS_OK;
+    if (hist) std::memset(hist, 0, sizeof(*hist));
+    std::vector<int64_t> th(sbs::kHistBins);
+    for (int i = 0; i < n; ++i) {
+      const PointHost& p = s->pts[s->order[i]];
+      finish_aggregates(p, s->h_res[i], out[s->order[i]]);
+      if (s->h_res[i].error != 0) {
+        rc = s->h_res[i].error;
+        g_err = "replica " + std::to_string(s->order[i]) + " failed with code " + std::to_string(rc);
+      }
+      if (hist) {
+        CUDA_OR_THROW(cudaMemcpy(th.data(), p.dp.tpot_hist, 8 * sbs::kHistBins, cudaMemcpyDeviceToHost));
+        for (int b = 0; b < sbs::kHistBins; ++b) {
+          hist->ttft[b] += s->h_res[i].ttft_hist[b];
+          hist->tpot[b] += th[b];
+        }
+      }
+    }
+    return rc;
+  });
+}
+
+int sbs_sim_requests(sbs_sim* s, int32_t point, int64_t* dispatch_ns, int64_t* prefill_start_ns,
+                     int64_t* first_token_ns, int64_t* completion_ns, int8_t* status) {
+  return guarded([&] {
+    if (!(s->flags & SBS_FLAG_PER_REQUEST))
+      throw Error{SBS_ERR_CONFIG, "simulator was created without SBS_FLAG_PER_REQUEST"};
+    if (point < 0 || point >= (int)s->pts.size()) throw Error{SBS_ERR_CONFIG, "point out of range"};
+    CUDA_OR_THROW(cudaSetDevice(s->device));
+    const sbs::DevPoint& d = s->pts[point].dp;
+    size_t n = (size_t)d.N;
+    if (n == 0) return SBS_OK;
+    if (dispatch_ns) CUDA_OR_THROW(cudaMemcpy(dispatch_ns, d.o_dispatch, 8 * n, cudaMemcpyDeviceToHost));
+    if (prefill_start_ns) CUDA_OR_THROW(cudaMemcpy(prefill_start_ns, d.o_pstart, 8 * n, cudaMemcpyDeviceToHost));
+    if (first_token_ns) CUDA_OR_THROW(cudaMemcpy(first_token_ns, d.o_ftok, 8 * n, cudaMemcpyDeviceToHost));
+    if (completion_ns) CUDA_OR_THROW(cudaMemcpy(completion_ns, d.o_comp, 8 * n, cudaMemcpyDeviceToHost));
+    if (status) CUDA_OR_THROW(cudaMemcpy(status, d.o_status, n, cudaMemcpyDeviceToHost));
+    return SBS_OK;
+  });
+}
+
+void sbs_sim_destroy(sbs_sim* s) {
+  if (s == nullptr) return;
+  cudaSetDevice(s->device);
+  for (auto& p : s->pts) free_point(p);
+  for (auto& t : s->traces) {
+    if (t.arr) cudaFree(t.arr);
+    if (t.prompt) cudaFree(t.prompt);
+    if (t.output) cudaFree(t.output);
+  }
+  if (s->d_pts) cudaFree(s->d_pts);
+  if (s->d_res) cudaFree(s->d_res);
+  if (s->d_counter) cudaFree(s->d_counter);
+  delete s;
+}
+
+int sbs_run_experiments(const sbs_experiment* points, int32_t n_points, sbs_aggregates* out,
+                        int32_t device) {
+  return guarded([&] {
+    // unique (workload, seed) traces, generated on host threads
+    std::vector<HostTrace> tr;
+    std::vector<int32_t> map(n_points);
+    std::map<std::string, int> seen;
+    for (int i = 0; i < n_points; ++i) {
+      std::string key(reinterpret_cast<const char*>(&points[i].workload), sizeof(sbs_workload));
+      key.append(reinterpret_cast<const char*>(&points[i].seed), sizeof(uint64_t));
+      auto it = seen.find(key);
+      if (it == seen.end()) {
+        map[i] = (int)tr.size();
+        seen.emplace(key, (int)tr.size());
+        tr.emplace_back();
+      } else {
+        map[i] = it->second;
+      }
+    }
+    std::vector<int> first(tr.size(), -1);
+    for (int i = 0; i < n_points; ++i)
+      if (first[map[i]] < 0) first[map[i]] = i;
+    std::atomic<size_t> next{0};
+    std::atomic<bool> bad{false};
+    Error firsterr{0, ""};
+    auto work = [&]() {
+      for (;;) {
+        size_t k = next.fetch_add(1);
+        if (k >= tr.size()) return;
+        try {
+          generate(points[first[k]].workload, points[first[k]].seed, tr[k]);
+        } catch (const Error& e) {
+          if (!bad.exchange(true)) firsterr = e;
+        }
+      }
+    };
+    std::vector<std::thread> pool;
+    int nt = std::min<int>(parallel_threads(), (int)tr.size());
+    for (int t = 0; t < nt; ++t) pool.emplace_back(work);
+    for (auto& th : pool) th.join();
+    if (bad) throw firsterr;
+    std::vector<sbs_trace> st(tr.size());
+    for (size_t k = 0; k < tr.size(); ++k)
+      st[k] = sbs_trace{tr[k].arr.data(), tr[k].prompt.data(), tr[k].output.data(),
+                        (int64_t)tr[k].arr.size(), tr[k].digest};
+    sbs_sim* s = nullptr;
+    int rc = sbs_sim_create(points, n_points, st.data(), (int32_t)st.size(), map.data(), 0, device, &s);
+    if (rc != SBS_OK) return rc;
+    rc = sbs_sim_launch(s, nullptr);
+    if (rc == SBS_OK) rc = sbs_sim_results(s, out, nullptr, nullptr);
+    std::string msg = g_err;
+    sbs_sim_destroy(s);
+    g_err = msg;
+    return rc;
+  });
+}
+
+int sbs_prefill_allocate(const sbs_window_batch* b, void* stream) {
+  return guarded([&] {
+    int32_t* d_err = nullptr;
+    cudaStream_t st = (cudaStream_t)stream;
+    CUDA_OR_THROW(cudaMallocAsync(&d_err, sizeof(int32_t), st));
+    CUDA_OR_THROW(cudaMemsetAsync(d_err, 0, sizeof(int32_t), st));
+    sbs::PbaaArgs a{b->n_windows, b->req_off, b->n_pending, b->dp_off, b->n_limit, b->req_id,
+                    b->prompt_len, b->wait_in, b->caps, b->out_dp, b->out_rank, b->wait_out,
+                    b->flow, d_err};
+    CUDA_OR_THROW(sbs::launch_pbaa(a, st));
+    int32_t h_err = 0;
+    CUDA_OR_THROW(cudaMemcpyAsync(&h_err, d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CUDA_OR_THROW(cudaFreeAsync(d_err, st));
+    CUDA_OR_THROW(cudaStreamSynchronize(st));
+    if (h_err) throw Error{h_err, "window exceeds the kernel's shared-memory envelope"};
+    return SBS_OK;
+  });
+}
+
+int sbs_decode_select(const sbs_decode_batch* b, void* stream) {
+  return guarded([&] {
+    int32_t* d_err = nullptr;
+    cudaStream_t st = (cudaStream_t)stream;
+    CUDA_OR_THROW(cudaMallocAsync(&d_err, sizeof(int32_t), st));
+    CUDA_OR_THROW(cudaMemsetAsync(d_err, 0, sizeof(int32_t), st));
+    sbs::IqrArgs a{b->n_calls, b->unit_off, b->batch, b->kv, b->k, b->pos_out,
+                   b->fallback_out, b->threshold_out, d_err};
+    CUDA_OR_THROW(sbs::launch_iqr(a, st));
+    int32_t h_err = 0;
+    CUDA_OR_THROW(cudaMemcpyAsync(&h_err, d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CUDA_OR_THROW(cudaFreeAsync(d_err, st));
+    CUDA_OR_THROW(cudaStreamSynchronize(st));
+    if (h_err == 3) throw Error{SBS_ERR_INVARIANT, "select_decode_unit: no units"};
+    if (h_err) throw Error{h_err, "decode call exceeds the kernel's shared-memory envelope"};
+    return SBS_OK;
+  });
+}
+
+}  // extern "C"
