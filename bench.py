@@ -1,0 +1,417 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 SBS hot path (simulated requests/s and allocations/s).
+
+Workload (default ``cfg5``): the DeepSeek-V3-shaped
+P/D cluster (4 prefill x DP 8 = 32 prefill DP units, 1 decode x DP 320),
+Poisson 200 qps x 5000 s (~1M requests per replica), lognormal prompts and
+outputs, SBS + PBAA + IQR; 512 seed replicas per GPU (seeds 11 + rank + N*i),
+i.e. the per-GPU slice of the 4096-replica sweep.  Weak scaling: at N GPUs the
+job simulates 512*N replicas.
+
+One step = one pass of the hot path over the whole per-GPU batch: the
+persistent DES kernel (one warp per replica) + the finalize kernel, and at N>1
+an NCCL all-reduce of the fixed-size summary/histogram buffer.
+
+  value : simulated requests/s, traces already resident in HBM (CUDA events on
+          the launching stream, max over ranks).
+  e2e   : same metric through the C-ABI with host traces: H2D of every trace
+          (16 B/request, pinned), simulate, D2H of the aggregates, per step.
+  --impl reference : the reference C++ simulator (oracle/_ref, unmodified
+          sources) on all host cores over a bounded sample of the workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+SBS_CLUSTER_CFG2 = {
+    "n_instances_prefill": 4, "n_instances_decode": 1, "dp_degree": 8,
+    "dp_degree_decode": 320, "c_chunk": 3000, "t_default_s": 0.35, "w_size": 64,
+    "l_net_s": 0.002, "n_limit": 64,
+    "engine": {"prefill_base_s": 0.05, "prefill_per_token_s": 1e-4, "decode_base_s": 0.004,
+               "decode_per_request_s": 2e-4, "decode_per_kv_token_s": 1e-6},
+}
+
+
+def cfg2(seed=11, duration=500.0):
+    """SURVEY.md §8d config 2 (config 5 = this with duration 5000 s)."""
+    return {
+        "cluster": dict(SBS_CLUSTER_CFG2),
+        "workload": {"process": "poisson", "rate_qps": 200, "duration_s": duration,
+                     "prompt": {"dist": "lognormal", "mu": 6.2, "sigma": 1.2, "min": 1, "max": 3000},
+                     "output": {"dist": "lognormal", "mu": 5.0, "sigma": 0.8, "min": 1, "max": 2000}},
+        "scheduler": {"policy": "sbs", "decode_policy": "iqr"},
+        "sim": {"seed": seed, "warmup_fraction": 0.1},
+    }
+
+
+def short3k(seed=7, duration=23.25, rate=430.0, dp=8, l_net=0.002, policy="sbs"):
+    c = json.load(open(ROOT / "tests" / "golden" / "configs" / "short_3k.json"))
+    c["workload"]["duration_s"] = duration
+    c["workload"]["rate_qps"] = rate
+    c["cluster"]["dp_degree"] = dp
+    c["cluster"]["l_net_s"] = l_net
+    c["scheduler"]["policy"] = policy
+    c["sim"]["seed"] = seed
+    return c
+
+
+def cfg3(seed=11):
+    c = json.load(open(ROOT / "tests" / "golden" / "configs" / "decode_dp32.json"))
+    c["workload"].update({"rate_qps": 10.4, "duration_s": 600, "initial_burst": 256,
+                          "prompt": {"dist": "lognormal", "mu": 7.5, "sigma": 0.45, "min": 300, "max": 3500},
+                          "output": {"dist": "lognormal", "mu": 6.5, "sigma": 1.0, "min": 1, "max": 8000}})
+    c["sim"].update({"seed": seed, "warmup_fraction": 0.2})
+    return c
+
+
+def workload_points(name, rank, world, replicas=None, duration=None):
+    """Configs of one rank's slice. Returns (description, [cfg])."""
+    if name == "cfg5":
+        R = replicas or 512
+        d = duration or 5000.0
+        cfgs = [cfg2(seed=11 + rank + world * i, duration=d) for i in range(R)]
+        return (f"cfg5: DeepSeek-shaped P/D cluster (prefill 4xDP8, decode 1xDP320), Poisson "
+                f"200 qps x {d:g} s, {R} seed replicas per GPU", cfgs)
+    if name == "cfg2":
+        d = duration or 500.0
+        return (f"cfg2: DeepSeek-shaped P/D cluster, 1 replica, {d:g} s", [cfg2(11, d)])
+    if name == "cfg3":
+        R = replicas or 256
+        cfgs = [cfg3(seed=11 + rank + world * i) for i in range(R)]
+        return (f"cfg3: decode DP32 heavy-tailed outputs + burst 256, {R} replicas per GPU, iqr",
+                cfgs)
+    if name == "cfg4":
+        # 1024-point grid l_net x rate x dp, 128 per GPU at 8 GPUs (i mod 8 == rank)
+        pts = []
+        for ln in [0, 1, 2, 5, 10, 20, 50, 100]:
+            for rate in range(200, 520, 20):
+                for dp in [1, 2, 4, 8, 16, 32, 64, 128]:
+                    pts.append((ln / 1000.0, float(rate), dp))
+        per = replicas or 128
+        mine = [p for i, p in enumerate(pts) if i % 8 == rank % 8][:per]
+        cfgs = [short3k(seed=7, duration=duration or 50000.0 / r, rate=r, dp=dp, l_net=ln)
+                for (ln, r, dp) in mine]
+        return (f"cfg4: sweep l_net x rate x dp_degree on short_3k, {len(cfgs)} points per GPU",
+                cfgs)
+    if name == "cfg1":
+        R = replicas or 512
+        cfgs = [short3k(seed=7 + rank + world * i) for i in range(R)]
+        return (f"cfg1: short_3k @ 23.25 s (~10k requests), SBS, {R} replicas per GPU", cfgs)
+    raise SystemExit(f"unknown workload {name}")
+
+
+# --------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                util = float(f[7])
+                s = float(f[0])
+                mx = float(f[1])
+            except ValueError:
+                continue
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+            if util > 0:
+                sm.append(s)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(self.lines)}
+
+
+# --------------------------------------------------------------- reference arm
+def cpu_reference(cfgs, threads, sample_replicas=None, sample_duration=None):
+    """Run the reference simulator (oracle/_ref) over a bounded sample."""
+    from oracle import ref
+    import copy
+    sample = []
+    for c in cfgs[: (sample_replicas or len(cfgs))]:
+        c = copy.deepcopy(c)
+        if sample_duration:
+            c["workload"]["duration_s"] = sample_duration
+        sample.append(c)
+    wall, agg, meta = ref.run_batch(sample, threads)
+    gen = float(agg[:, 0].sum())
+    allocs = float(meta[:, 1].sum())
+    dsel = float(meta[:, 2].sum())
+    return wall, gen, allocs, dsel, len(sample)
+
+
+def cpu_sample_spec(workload):
+    # bounded samples (~10-30 s of CPU work on the GPU box's cores)
+    if workload in ("cfg5", "cfg2"):
+        return {"replicas_per_core": 1, "duration": 500.0}
+    if workload == "cfg3":
+        return {"replicas_per_core": 2, "duration": None}
+    return {"replicas_per_core": 2, "duration": None}
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return 0
+    from oracle import ref
+    ref.lib()
+    threads = os.cpu_count() or 1
+    desc, cfgs = workload_points(args.workload, 0, 1, args.replicas, args.duration)
+    spec = cpu_sample_spec(args.workload)
+    nrep = min(len(cfgs), threads * spec["replicas_per_core"])
+    times = []
+    for i in range(args.warmup + args.steps):
+        wall, gen, allocs, dsel, n = cpu_reference(cfgs, threads, nrep, spec["duration"])
+        if i >= args.warmup:
+            times.append((wall, gen, allocs, dsel, n))
+    wall = sum(t[0] for t in times)
+    gen = sum(t[1] for t in times)
+    allocs = sum(t[2] for t in times)
+    v = gen / wall
+    sample = (f"{nrep} replicas of the {args.workload} workload"
+              + (f" at duration {spec['duration']:g} s" if spec["duration"] else "")
+              + f" per step ({times[0][1]:.0f} simulated requests), run_experiment on a "
+              f"{threads}-thread std::thread pool")
+    line = {
+        "impl": "reference", "metric": "simulated_requests_per_s", "value": v,
+        "unit": "sim-req/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000.0 * wall / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": desc, "sample": sample},
+        "allocations_per_s": allocs / wall,
+        "cpu_baseline": {"value": v, "unit": "sim-req/s", "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "sim-req/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--replicas", type=int, default=None, help="dev override (not a bench line)")
+    ap.add_argument("--duration", type=float, default=None, help="dev override (not a bench line)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus == 1 else 1)))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference_arm(args, rank, world)
+
+    import numpy as np
+    import torch
+    import paper_2512_16134_b200 as P
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+
+    desc, cfgs = workload_points(args.workload, rank, world, args.replicas, args.duration)
+    t0 = time.time()
+    points = [P.experiment_from_config(c) for c in cfgs]
+    # host trace generation (pinned, for the e2e H2D leg); one trace per seed
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, (os.cpu_count() or 2) // max(1, world))) as ex:
+        traces = list(ex.map(lambda p: P.generate_workload(p, pinned=True), points))
+    gen_s = time.time() - t0
+    n_req = sum(t.n for t in traces)
+    sim = P.Simulator(points, traces, device=local)
+    h2d_bytes = 16 * n_req
+
+    def step(upload):
+        if upload:
+            sim.upload_traces(stream=stream.cuda_stream)
+        sim.launch(stream=stream.cuda_stream)
+
+    # warm-up (also grows any arena that overflowed)
+    for _ in range(args.warmup):
+        step(False)
+        res = sim.results(stream=stream.cuda_stream)
+    errs = [r["error"] for r in res if r["error"]]
+    if errs:
+        raise SystemExit(f"replica errors: {errs[:5]}")
+
+    def summary_buf(res, hist):
+        # fixed-size int64 buffer: exact sums + histograms (NCCL-reduced)
+        keys = ["generated", "completed", "alloc_calls", "decode_selects", "events",
+                "ttft_sum_ns", "window_requests", "output_tokens"]
+        v = [sum(int(r[k]) for r in res) for k in keys]
+        v += list(hist.ttft) + list(hist.tpot)
+        return torch.tensor(v, dtype=torch.int64, device=dev)
+
+    # ---- timed: device-resident traces
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    gpu = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local]) \
+        if os.environ.get("CUDA_VISIBLE_DEVICES") else local
+    times = []
+    with ClockSampler(gpu) as clk:
+        for _ in range(args.steps):
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            step(False)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            times.append(ev0.elapsed_time(ev1))
+        res, hist = sim.results(stream=stream.cuda_stream, histograms=True)
+        buf = summary_buf(res, hist)
+        if dist:
+            dist.all_reduce(buf)
+    clocks = clk.summary()
+    ms = statistics.mean(times)
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_req = int(buf[0].item())
+    total_alloc = int(buf[2].item())
+    total_dsel = int(buf[3].item())
+    value = total_req / (ms / 1000.0)
+
+    # ---- e2e: host traces -> H2D -> simulate -> D2H aggregates
+    e2e = None
+    if not args.no_e2e:
+        e_times = []
+        for _ in range(max(1, min(args.steps, 3))):
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t_a = time.perf_counter()
+            step(True)
+            res2 = sim.results(stream=stream.cuda_stream)
+            t_b = time.perf_counter()
+            e_times.append(t_b - t_a)
+        es = statistics.mean(e_times)
+        if dist:
+            t = torch.tensor([es], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            es = float(t.item())
+        import ctypes
+        e2e = {"value": total_req / es, "unit": "sim-req/s", "h2d_bytes_per_step": h2d_bytes * world,
+               "d2h_bytes_per_step": ctypes.sizeof(P.api.Aggregates) * len(points) * world,
+               "ms_per_step": es * 1000.0,
+               "host_trace_generation_s": gen_s}
+
+    # ---- roofline: algorithmic bytes = 16 B/request (trace read), SURVEY §8d
+    peaks = {}
+    try:
+        peaks = json.load(open(ROOT / "MEASURED_PEAKS.json"))
+    except Exception:
+        pass
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = 16.0 * (total_req / world) / (ms / 1000.0) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        try:
+            tj = json.load(open(tf))
+            traffic = tj.get(args.workload)
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            spec = cpu_sample_spec(args.workload)
+            nrep = min(len(cfgs), threads * spec["replicas_per_core"])
+            wall, gen, allocs, dsel, n = cpu_reference(cfgs, threads, nrep, spec["duration"])
+            cpu = {"value": gen / wall, "unit": "sim-req/s", "cores": threads, "kind": "reference",
+                   "sample": f"{n} replicas of {args.workload}"
+                             + (f" at duration {spec['duration']:g} s" if spec["duration"] else "")
+                             + f" ({gen:.0f} simulated requests) on {threads} threads, "
+                               f"{wall:.1f} s wall"}
+        except Exception as e:  # the baseline must never block the line
+            cpu = {"value": None, "unit": "sim-req/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    line = {
+        "metric": "simulated_requests_per_s", "value": value, "unit": "sim-req/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic",
+        "config": {"workload": desc, "replicas_per_gpu": len(points),
+                   "requests_per_gpu": n_req, "l2": "inputs (16 B/request traces) far larger than L2",
+                   "parallelism": f"replicas sharded over {world} GPU(s), one warp per replica"},
+        "allocations_per_s": total_alloc / (ms / 1000.0),
+        "decode_placements_per_s": total_dsel / (ms / 1000.0),
+        "gpu_launches": args.steps * sim.launches_per_run,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "note": "algorithmic bytes = 16 B/request trace read; serial per-replica "
+                             "event chains make this latency-bound"},
+        "clocks": clocks,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    sim.close()
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -665,6 +665,10 @@ int sbs_sim_create(const sbs_experiment* points, int32_t n_points, const sbs_tra
   sbs_sim* s = new sbs_sim();
   int rc = guarded([&] {
     if (n_points < 1) throw Error{SBS_ERR_CONFIG, "no points"};
+    for (int i = 0; i < n_points; ++i) {
+      validate(points[i]);
+      check_workload(points[i].workload);
+    }
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
       throw Error{SBS_ERR_CUDA, "no CUDA device visible (the GPU path has no CPU fallback)"};

@@ -1,0 +1,111 @@
+"""GPU: the batched allocation kernels (sbs_prefill_allocate, sbs_decode_select)
+against the pinned C oracle and the recorded reference windows."""
+import itertools
+
+import numpy as np
+import pytest
+
+import paper_2512_16134_b200 as P
+from oracle import orc
+from tests.common import GOLD, records_decodes, records_windows
+
+pytestmark = pytest.mark.gpu
+
+
+def _csr(windows):
+    req_off, dp_off, npend, nlim, ids, lens, waits, caps = [0], [0], [], [], [], [], [], []
+    for w in windows:
+        rows = list(w["pending"]) + list(w["new"])
+        for r in rows:
+            ids.append(r[0]); lens.append(r[1]); waits.append(r[2])
+        req_off.append(req_off[-1] + len(rows))
+        npend.append(len(w["pending"])); nlim.append(w["n_limit"])
+        caps.extend(w["caps"]); dp_off.append(dp_off[-1] + len(w["caps"]))
+    return req_off, npend, dp_off, nlim, ids, lens, waits, caps
+
+
+def test_recorded_windows_short_3k():
+    wins = records_windows(np.load(GOLD / "windows_short_3k.npz")["records"])
+    got = P.allocate_batch([{k: w[k] for k in ("pending", "new", "caps", "n_limit")} for w in wins])
+    for w, g in zip(wins, got):
+        assert g["mapping"].tolist() == w["mapping"]
+        assert g["deferred"].tolist() == w["deferred"]
+        assert g["throttled"].tolist() == w["throttled"]
+        assert g["caps"].tolist() == w["caps_out"]
+        assert g["flow"] == w["flow"]
+
+
+def test_pbaa_exhaustive_grid():
+    """All 1,007,748 cases of the reference's allocator grid (acceptance.cpp:415-446)
+    in one launch, checked against the C oracle."""
+    wins = []
+    for dp in (1, 2, 3):
+        for k in range(1, 7):
+            for lens in itertools.product((1, 2, 3, 4, 5, 7), repeat=k):
+                rows = [[j, L, 0] for j, L in enumerate(lens)]
+                for split in (0, k // 2, k):
+                    for nl in (0, 2):
+                        wins.append({"pending": rows[:split], "new": rows[split:],
+                                     "caps": [7] * dp, "n_limit": nl})
+    assert len(wins) == 1007748
+    req_off, npend, dp_off, nlim, ids, lens, waits, caps = _csr(wins)
+    e_dp, e_rank, e_wait, e_caps, e_flow = orc.allocate_many(req_off, npend, dp_off, nlim, ids,
+                                                             lens, waits, caps)
+    got = P.allocate_batch(wins)
+    g_caps = np.concatenate([g["caps"] for g in got])
+    assert np.array_equal(g_caps, e_caps)
+    assert np.array_equal(np.array([g["flow"] for g in got]), e_flow.astype(bool))
+    # mapping order and deferred/throttled sets via the oracle's per-request outputs
+    for i in range(0, len(wins), 997):
+        r0, r1 = req_off[i], req_off[i + 1]
+        pl = [(ids[j], e_dp[j], e_rank[j]) for j in range(r0, r1) if e_dp[j] >= 0]
+        pl.sort(key=lambda t: t[2])
+        assert got[i]["mapping"].tolist() == [[a, b] for a, b, _ in pl]
+
+
+def test_pbaa_random_vs_oracle():
+    rng = np.random.default_rng(99)
+    wins = []
+    for _ in range(4000):
+        D = int(rng.integers(1, 129))
+        k = int(rng.integers(0, 300))
+        ids = rng.permutation(10 * k + 10)[:k]
+        lens = np.where(rng.random(k) < 0.1, 1, rng.integers(1, 5000, k))
+        waits = rng.integers(0, 6, k)
+        rows = [[int(a), int(b), int(c)] for a, b, c in zip(ids, lens, waits)]
+        split = int(rng.integers(0, k + 1))
+        wins.append({"pending": rows[:split], "new": rows[split:],
+                     "caps": rng.integers(-4000, 4000, D).tolist(), "n_limit": int(rng.integers(0, 6))})
+    got = P.allocate_batch(wins)
+    for w, g in zip(wins, got):
+        e = orc.allocate_batch(w["pending"], w["new"], w["caps"], w["n_limit"])
+        for key in ("mapping", "deferred", "throttled", "caps"):
+            assert np.array_equal(g[key], e[key]), key
+        assert g["flow"] == e["flow"]
+
+
+def test_iqr_recorded_decodes():
+    calls = records_decodes(np.load(GOLD / "decodes_decode_dp32.npz")["records"])
+    pos, fb, th = P.select_decode_unit([(c["batch"], c["kv"]) for c in calls], k=1.5)
+    assert pos.tolist() == [c["selected"] for c in calls]
+    assert fb.tolist() == [c["fallback"] for c in calls]
+
+
+def test_iqr_kats_and_random():
+    pos, fb, th = P.select_decode_unit([([0] * 4, [10, 20, 30, 40]), ([0] * 4, [10, 10, 10, 100]),
+                                        ([0] * 4, [7, 7, 7, 7])])
+    assert th.tolist() == [55.0, 66.25, 7.0]
+    rng = np.random.default_rng(5)
+    calls = []
+    for _ in range(3000):
+        U = int(rng.integers(1, 2049))
+        B = rng.integers(0, 4, U)
+        K = rng.integers(0, 60, U) if rng.random() < 0.5 else rng.integers(0, 10**7, U)
+        if rng.random() < 0.3:
+            K[rng.integers(0, U, 3)] = 10**10
+        calls.append((B, K))
+    for k in (0.0, 1.5, 3.0):
+        pos, fb, th = P.select_decode_unit(calls, k=k)
+        for i, (B, K) in enumerate(calls):
+            e = orc.select_decode_unit(B, K, k)
+            assert (pos[i], fb[i], th[i]) == e
