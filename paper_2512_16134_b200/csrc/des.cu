@@ -30,8 +30,12 @@
 //    instance is at step s completes at step s + ceil(target/tps); it is
 //    pushed into a completion ring bucket and K grows by tps * B_at_begin
 //    minus the last-step excess of completers.
-//  * IQR quartiles read a sorted K multiset kept in shared memory, updated in
-//    O(U/32) per admission and re-sorted after a decode step.
+//  * A decode unit is one packed u64 (B << 48 | K) in shared memory, so the
+//    lexicographic (B, K) minimum is a u64 minimum.  IQR quartiles read a
+//    sorted K multiset, updated in O(U/32) per admission and re-sorted by a
+//    warp LSD radix sort after a decode step.  Step begin is O(1): resident
+//    count and max_u(per_req*B + per_kv*K) are maintained incrementally; the
+//    KV band uses exact per-instance sums of K and K^2.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -142,18 +146,70 @@ __device__ __forceinline__ uint64_t mt_temper(uint64_t y) {
 // ---------------------------------------------------------------------------
 // One replica, executed by one warp.
 // ---------------------------------------------------------------------------
+constexpr uint64_t kBOne = 1ull << 48;       // packed decode unit: B << 48 | K
+constexpr uint64_t kKMask = kBOne - 1;
+constexpr int kErrEnvelope = 6;               // B >= 2^15 or K >= 2^48 on a decode unit
+
+typedef unsigned __int128 u128;
+
+// Per-replica counters and FP sums (metrics.h:107-152 state), in shared memory
+// and written by lane 0 only: they are rarely read, so they should not occupy
+// 50 replicated registers per lane.  FP sums stay sequential in event order.
+struct Counters {
+  long long completed, throttled, cw, wr, passes, steps, outtok, wdf, drop, rej, def, flow,
+      mask, fb, alloc, dsel, events, ttft, sched, dev, kv_n;
+  double util, kv_mean, kv_sig;
+};
+
+__device__ __forceinline__ u128 shfl_xor_u128(u128 v, int o) {
+  uint64_t lo = (uint64_t)v, hi = (uint64_t)(v >> 64);
+  lo = __shfl_xor_sync(kFull, lo, o);
+  hi = __shfl_xor_sync(kFull, hi, o);
+  return ((u128)hi << 64) | lo;
+}
+__device__ __forceinline__ u128 bcast_u128(u128 v, int src) {
+  uint64_t lo = (uint64_t)v, hi = (uint64_t)(v >> 64);
+  lo = __shfl_sync(kFull, lo, src);
+  hi = __shfl_sync(kFull, hi, src);
+  return ((u128)hi << 64) | lo;
+}
+__device__ __forceinline__ double u128_to_f64(u128 v) {
+  return __dadd_rn(__dmul_rn((double)(uint64_t)(v >> 64), 18446744073709551616.0),
+                   (double)(uint64_t)v);
+}
+
 __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* sm) {
   const int lane = lane_id();
   const unsigned lt_mask = lanemask_lt();
 
-  // ---- constants
+  // ---- constants hoisted out of the (global) descriptor
   const int P = pt.P, Dn = pt.Dn, D = pt.D, Dd = pt.Dd, U = pt.U;
   const int PD = P * D;
   const bool sbs = pt.policy == kSbs;
+  const int policy = pt.policy, dec_policy = pt.decode_policy;
   const int64_t c_chunk = pt.c_chunk;
   const int64_t N = pt.N;
   const int64_t horizon = pt.horizon, warmup = pt.warmup;
   const int F = pt.F, Fm = pt.F - 1, R = pt.R, BC = pt.BC;
+  const int n_limit = pt.n_limit, cap_batch = pt.cap_batch, n_drops = pt.n_drops;
+  const int n_topo = pt.n_topo, w_size = pt.w_size, QD = pt.QD, QP = pt.QP, QW = pt.QW;
+  const bool per_req = pt.per_request != 0;
+  const int64_t tps = pt.tps, t_default = pt.t_default;
+  const double pf_base = pt.pf_base, pf_tok = pt.pf_tok, dc_base = pt.dc_base, dc_req = pt.dc_req,
+               dc_kv = pt.dc_kv, iqr_k = pt.iqr_k, wd_mult = pt.wd_mult;
+  const int64_t* __restrict__ g_arr = pt.arr;
+  const int32_t* __restrict__ g_prompt = pt.prompt;
+  const int32_t* __restrict__ g_output = pt.output;
+  int64_t* const o_dispatch = pt.o_dispatch;
+  int64_t* const o_pstart = pt.o_pstart;
+  int64_t* const o_ftok = pt.o_ftok;
+  int64_t* const o_comp = pt.o_comp;
+  int8_t* const o_status = pt.o_status;
+  int64_t* const g_ttft = pt.ttft;
+  int2* const g_fifo = pt.fifo;
+  int4* const g_buckets = pt.buckets;
+  uint64_t* const g_dwait = pt.dwait;
+  int64_t* const g_tpot_hist = pt.tpot_hist;
 
   // ---- shared-memory carve
   int64_t* s_out = (int64_t*)(sm + pt.sm_pf_out);
@@ -161,19 +217,26 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   int32_t* s_tail = (int32_t*)(sm + pt.sm_pf_tail);
   int32_t* s_rel = (int32_t*)(sm + pt.sm_pf_rel);
   uint8_t* s_part = (uint8_t*)(sm + pt.sm_pf_part);
-  int64_t* s_K = (int64_t*)(sm + pt.sm_dK);
-  int64_t* s_S = (int64_t*)(sm + pt.sm_dS);
-  int32_t* s_B = (int32_t*)(sm + pt.sm_dB);
-  int32_t* s_nst = (int32_t*)(sm + pt.sm_dnst);
+  uint64_t* s_PK = (uint64_t*)(sm + pt.sm_dPK);   // B << 48 | K per decode unit
+  uint64_t* s_R = (uint64_t*)(sm + pt.sm_dR);     // completers this step: n << 48 | kv release
+  uint64_t* s_S = (uint64_t*)(sm + pt.sm_dS);     // sorted K multiset over the unit list
+  uint64_t* s_T = (uint64_t*)(sm + pt.sm_dT);     // radix-sort scratch
+  int32_t* s_nst = (int32_t*)(sm + pt.sm_dnst);   // residents stamped at the next/current step
   int16_t* s_ul = (int16_t*)(sm + pt.sm_ulist);
   uint16_t* s_bcnt = (uint16_t*)(sm + pt.sm_bcnt);
+  uint32_t* s_hist = (uint32_t*)(sm + pt.sm_hist);
   int64_t* s_wr = (int64_t*)(sm + pt.sm_wring);
   uint64_t* s_wk = (uint64_t*)(sm + pt.sm_wkeys);
+  Counters* cn = (Counters*)(sm + pt.sm_cnt);
+  if (lane == 0) {
+    long long* z = (long long*)cn;
+    for (int i = 0; i < (int)(sizeof(Counters) / 8); ++i) z[i] = 0;
+  }
 
   for (int g = lane; g < PD; g += 32) {
     s_out[g] = 0; s_head[g] = 0; s_tail[g] = 0; s_rel[g] = 0; s_part[g] = 0;
   }
-  for (int u = lane; u < U; u += 32) { s_K[u] = 0; s_B[u] = 0; s_nst[u] = 0; }
+  for (int u = lane; u < U; u += 32) { s_PK[u] = 0; s_R[u] = 0; s_nst[u] = 0; }
   for (int b = lane; b < Dn * R; b += 32) s_bcnt[b] = 0;
   __syncwarp();
 
@@ -192,11 +255,15 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   int64_t ds_t = kInf64;
   uint32_t ds_s = 0xffffffffu;
   const int64_t d_death = (lane < Dn) ? pt.death[P + lane] : kInf64;
+  int64_t d_res = 0, d_s1 = 0;  // residents, sum K over the instance's units
+  u128 d_s2 = 0;                // sum K^2
+  double d_worst = 0.0;         // max_u decode_per_request*B + decode_per_kv*K
+  int64_t d_res_begin = 0;      // residents stamped at the running step
 
   // ---- scheduler state (SchedulerState, core.h:197-218; new_cluster core.cpp:162-168)
   int64_t now = 0;
   const int64_t l_net = pt.l_net;
-  int64_t t_bar = pt.t_default;
+  int64_t t_bar = t_default;
   int32_t n_active = P;
   int64_t i_opt = (t_bar + l_net) / n_active;  // no max(1) initially (core.cpp:167)
   bool has_ld = false;
@@ -214,7 +281,12 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   int32_t imm_next = 0;
   int64_t dec_rr = 0;
   int32_t mti = 312;
-  bool S_valid = false, ul_dirty = true;
+  bool S_valid = false, ul_dirty = true, ul_ident = false;
+  bool S_gathered = false;      // s_S holds the unit Ks (unsorted) after a step
+  uint64_t S_mx = 0;
+  // percentile ranks (decode_alloc.cpp:17-20) depend only on the unit count
+  int pc_n = -1, lo25 = 0, hi25 = 0, lo75 = 0, hi75 = 0;
+  double fr25 = 0.0, fr75 = 0.0;
   int32_t nul = 0;
   int error = 0;
 
@@ -224,15 +296,13 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   uint32_t o_s = 0;
   int o_k = 0, o_i = 0;
 
-  // ---- counters
-  int64_t c_completed = 0, c_throttled = 0, c_cw = 0, c_wr = 0, c_passes = 0, c_steps = 0,
-          c_outtok = 0, c_wdf = 0, c_drop = 0, c_rej = 0, c_def = 0, c_flow = 0, c_mask = 0,
-          c_fb = 0, c_alloc = 0, c_dsel = 0, c_events = 0, n_ttft = 0, s_ttft = 0, s_sched = 0,
-          s_dev = 0, kv_n = 0, tpot_n = 0;
-  double util_sum = 0.0, kv_mean_sum = 0.0, kv_sig_sum = 0.0, tpot_sum = 0.0;
+  // ---- counters (shared memory, lane 0) + lane-local TPOT partials
+  int64_t n_ttft = 0, tpot_n = 0;
+  double tpot_sum = 0.0;
+#define CNT(f, v) do { if (lane == 0) cn->f += (v); } while (0)
 
   // random decode policy: mt19937_64(seed ^ 0x9E3779B97F4A7C15) (simulation.cpp:42)
-  if (pt.decode_policy == kRandom) {
+  if (dec_policy == kRandom) {
     if (lane == 0) {
       uint64_t x = pt.rng_seed;
       pt.mt[0] = x;
@@ -246,8 +316,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
 
   // ---- arrival stream: lane l holds arrival[abase + l]
   int64_t abase = 0;
-  int64_t abuf = (lane < N) ? __ldg(pt.arr + lane) : kInf64;
-  int64_t anext = (32 + lane < N) ? __ldg(pt.arr + 32 + lane) : kInf64;
+  int64_t abuf = (lane < N) ? __ldg(g_arr + lane) : kInf64;
+  int64_t anext = (32 + lane < N) ? __ldg(g_arr + 32 + lane) : kInf64;
 
   // =======================================================================
   // helpers (all warp-uniform)
@@ -262,7 +332,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   auto maybe_die_d = [&](int j) {
     bool died = false;
     if (lane == j && !(dflags & G_DEAD) && now >= d_death) { dflags |= G_DEAD; died = true; }
-    if (__any_sync(kFull, died)) { ul_dirty = true; S_valid = false; }
+    if (__any_sync(kFull, died)) { ul_dirty = true; S_valid = false; S_gathered = false; }
   };
 
   auto arm_tick = [&](int64_t at) {  // simulation.cpp:234-238
@@ -270,13 +340,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     tick_s = seq++;
   };
 
-  auto n_active_count = [&]() -> int32_t {
-    return __popc(__ballot_sync(kFull, lane < P && (pflags & F_HEALTHY)));
-  };
-
   // recompute_interval (interval_control.cpp:18-24)
   auto recompute_interval = [&]() {
-    t_bar = (win_n == 0) ? pt.t_default : win_sum / (int64_t)win_n;
+    t_bar = (win_n == 0) ? t_default : win_sum / (int64_t)win_n;
     if (n_active <= 0) return;
     int64_t v = (t_bar + l_net) / (int64_t)n_active;
     i_opt = v > 1 ? v : 1;
@@ -306,23 +372,23 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     if (has) {
       l_done += 1;
       if (now >= warmup) l_cw += 1;
-      int64_t arr = __ldg(pt.arr + id);
-      if (pt.per_request) {
-        pt.o_comp[id] = now;
-        pt.o_status[id] = kStCompleted;
+      int64_t arr = __ldg(g_arr + id);
+      if (per_req) {
+        o_comp[id] = now;
+        o_status[id] = kStCompleted;
       }
       if (decode) {
-        int32_t out = __ldg(pt.output + id);
+        int32_t out = __ldg(g_output + id);
         int64_t dt = now - ftok;
         tpot_sum = __dadd_rn(tpot_sum, __ddiv_rn(__ddiv_rn((double)dt, 1e9), (double)(out - 1)));
         tpot_n += 1;
         int64_t per = dt / (int64_t)(out - 1);
-        atomicAdd((unsigned long long*)&pt.tpot_hist[hist_bin(per)], 1ull);
+        atomicAdd((unsigned long long*)&g_tpot_hist[hist_bin(per)], 1ull);
       }
       if (arr >= warmup) {
         inwin = true;
-        int64_t disp = pt.o_dispatch[id];
-        int64_t ps = pt.o_pstart[id];
+        int64_t disp = o_dispatch[id];
+        int64_t ps = o_pstart[id];
         ttft = ftok - arr;
         l_wr += 1;
         l_ttft += ttft;
@@ -331,16 +397,15 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       }
     }
     unsigned m = __ballot_sync(kFull, inwin);
-    if (inwin) pt.ttft[n_ttft + __popc(m & lt_mask)] = ttft;
+    if (inwin) g_ttft[n_ttft + __popc(m & lt_mask)] = ttft;
     n_ttft += __popc(m);
   };
   auto flush_lanes = [&]() {
-    c_completed += warp_sum_i64(l_done);
-    c_cw += warp_sum_i64(l_cw);
-    c_wr += warp_sum_i64(l_wr);
-    s_ttft += warp_sum_i64(l_ttft);
-    s_sched += warp_sum_i64(l_sched);
-    s_dev += warp_sum_i64(l_dev);
+    const int64_t a = warp_sum_i64(l_done), b = warp_sum_i64(l_cw), c = warp_sum_i64(l_wr),
+                  d = warp_sum_i64(l_ttft), e = warp_sum_i64(l_sched), f = warp_sum_i64(l_dev);
+    if (lane == 0) {
+      cn->completed += a; cn->cw += b; cn->wr += c; cn->ttft += d; cn->sched += e; cn->dev += f;
+    }
     l_done = l_cw = l_wr = l_ttft = l_sched = l_dev = 0;
   };
 
@@ -350,101 +415,118 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     int cnt = 0;
     for (int base = 0; base < U; base += 32) {
       int u = base + lane;
-      bool in = false;
-      if (u < U) {
-        int j = u / Dd;
-        int fl = __shfl_sync(kFull, dflags, j & 31);
-        in = (fl & G_HEALTHY) && !(fl & G_DEAD) &&
-             (pt.cap_batch <= 0 || s_B[u] < pt.cap_batch);
-      } else {
-        (void)__shfl_sync(kFull, dflags, 0);
-      }
+      int fl = __shfl_sync(kFull, dflags, (u < U ? u / Dd : 0) & 31);
+      bool in = u < U && (fl & G_HEALTHY) && !(fl & G_DEAD) &&
+                (cap_batch <= 0 || (int64_t)(s_PK[u] >> 48) < cap_batch);
       unsigned m = __ballot_sync(kFull, in);
       if (in) s_ul[cnt + __popc(m & lt_mask)] = (int16_t)u;
       cnt += __popc(m);
     }
     __syncwarp();
     nul = cnt;
+    ul_ident = cnt == U;
     ul_dirty = false;
     S_valid = false;
+    S_gathered = false;
   };
 
+  // sorted K multiset (for Q1/Q3) by warp radix sort
   auto rebuild_S = [&]() {
-    for (int i = lane; i < nul; i += 32) s_S[i] = s_K[s_ul[i]];
+    uint64_t mx = S_mx;
+    if (!S_gathered) {
+      mx = 0;
+      if (ul_ident) {
+        for (int i = lane; i < nul; i += 32) {
+          uint64_t k = s_PK[i] & kKMask;
+          s_S[i] = k;
+          mx = k > mx ? k : mx;
+        }
+      } else {
+        for (int i = lane; i < nul; i += 32) {
+          uint64_t k = s_PK[s_ul[i]] & kKMask;
+          s_S[i] = k;
+          mx = k > mx ? k : mx;
+        }
+      }
+      mx = (uint64_t)warp_max_i64((int64_t)mx);
+    }
+    S_gathered = false;
     __syncwarp();
-    warp_sort_buf((uint64_t*)s_S, nul);  // K >= 0: unsigned order == signed order
+    warp_radix_sort(s_S, s_T, s_hist, nul, mx ? 64 - __clzll((long long)mx) : 0);
     S_valid = true;
   };
 
-  // try_begin_decode_step (engine_model.cpp:153-179)
+  // try_begin_decode_step (engine_model.cpp:153-179).  Every resident is
+  // stamped (s_nst tracks them), the step time uses the maintained max.
   auto try_begin_step = [&](int j) {
     int fl = bcast(dflags, j);
     if ((fl & G_STEP) || (fl & G_DEAD)) return;
-    const int u0 = j * Dd;
-    bool any = false;
-    for (int d = lane; d < Dd; d += 32) any |= s_B[u0 + d] > 0;
-    if (!__any_sync(kFull, any)) return;
-    double worst = 0.0;
-    for (int d = lane; d < Dd; d += 32) {
-      int32_t b = s_B[u0 + d];
-      s_nst[u0 + d] = b;
-      double t = __dadd_rn(__dmul_rn(pt.dc_req, (double)b), __dmul_rn(pt.dc_kv, (double)s_K[u0 + d]));
-      worst = t > worst ? t : worst;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      double w = __shfl_xor_sync(kFull, worst, o);
-      worst = w > worst ? w : worst;
-    }
-    double dur = __dadd_rn(pt.dc_base, worst);
+    if (bcast(d_res, j) == 0) return;
+    double dur = __dadd_rn(dc_base, bcast(d_worst, j));
     int64_t t_end = now + llround_ns(dur);
     if (lane == j) {
       d_step += 1;
       dflags |= G_STEP;
       ds_t = t_end;
       ds_s = seq;
+      d_res_begin = d_res;
     }
     seq++;
     odirty = true;
-    __syncwarp();
   };
 
   // IQR select over the unit list (decode_alloc.cpp:38-81); returns position.
   auto iqr_select = [&]() -> int {
     if (!S_valid) rebuild_S();
-    double q1 = pct_sorted(s_S, nul, 25.0);
-    double q3 = pct_sorted(s_S, nul, 75.0);
-    double th = __dadd_rn(q3, __dmul_rn(pt.iqr_k, __dsub_rn(q3, q1)));
-    // pass 1: safe count
-    int nsafe = 0;
-    for (int i = lane; i < nul; i += 32) nsafe += ((double)s_K[s_ul[i]] <= th) ? 1 : 0;
-    nsafe = __reduce_add_sync(kFull, nsafe);
-    bool fallback = nsafe == 0;
-    if (fallback) c_fb += 1;
-    else if (nsafe < nul) c_mask += 1;
-    // lex-min (B, K), lowest position
-    int32_t bb = 0x7fffffff;
-    int64_t bk = kInf64;
-    int bp = 0x7fffffff;
-    for (int i = lane; i < nul; i += 32) {
-      int u = s_ul[i];
-      int64_t kv = s_K[u];
-      if (!fallback && !((double)kv <= th)) continue;
-      int32_t b = s_B[u];
-      if (b < bb || (b == bb && kv < bk)) { bb = b; bk = kv; bp = i; }
+    if (pc_n != nul) {
+      const double r25 = __ddiv_rn(__dmul_rn((double)nul - 1.0, 25.0), 100.0);
+      const double r75 = __ddiv_rn(__dmul_rn((double)nul - 1.0, 75.0), 100.0);
+      lo25 = (int)floor(r25); hi25 = (int)ceil(r25); fr25 = __dsub_rn(r25, (double)lo25);
+      lo75 = (int)floor(r75); hi75 = (int)ceil(r75); fr75 = __dsub_rn(r75, (double)lo75);
+      pc_n = nul;
     }
-    uint32_t mb = __reduce_min_sync(kFull, (uint32_t)bb);
-    int64_t ck = ((uint32_t)bb == mb) ? bk : kInf64;
-    int64_t mk = warp_min_i64(ck);
-    uint32_t cp = ((uint32_t)bb == mb && bk == mk) ? (uint32_t)bp : 0xffffffffu;
-    return (int)__reduce_min_sync(kFull, cp);
+    const double a1 = (double)s_S[lo25], b1 = (double)s_S[hi25];
+    const double a3 = (double)s_S[lo75], b3 = (double)s_S[hi75];
+    const double q1 = lo25 == hi25 ? a1 : __dadd_rn(a1, __dmul_rn(fr25, __dsub_rn(b1, a1)));
+    const double q3 = lo75 == hi75 ? a3 : __dadd_rn(a3, __dmul_rn(fr75, __dsub_rn(b3, a3)));
+    const double th = __dadd_rn(q3, __dmul_rn(iqr_k, __dsub_rn(q3, q1)));
+    // (double)K <= th  <=>  K <= floor(th) for integer K < 2^53
+    const double fth = floor(th);
+    const int64_t thi = fth >= 281474976710656.0 ? (int64_t)kKMask : (fth < 0.0 ? -1 : (int64_t)fth);
+    uint64_t bs = UINT64_MAX, ba = UINT64_MAX;
+    int ps = 0x7fffffff, pa = 0x7fffffff, ns = 0;
+    if (ul_ident) {
+      for (int i = lane; i < nul; i += 32) {
+        const uint64_t k = s_PK[i];
+        const bool safe = (int64_t)(k & kKMask) <= thi;
+        ns += safe;
+        if (safe && k < bs) { bs = k; ps = i; }
+        if (k < ba) { ba = k; pa = i; }
+      }
+    } else {
+      for (int i = lane; i < nul; i += 32) {
+        const uint64_t k = s_PK[s_ul[i]];
+        const bool safe = (int64_t)(k & kKMask) <= thi;
+        ns += safe;
+        if (safe && k < bs) { bs = k; ps = i; }
+        if (k < ba) { ba = k; pa = i; }
+      }
+    }
+    ns = __reduce_add_sync(kFull, ns);
+    const bool fallback = ns == 0;
+    if (fallback) CNT(fb, 1);
+    else if (ns < nul) CNT(mask, 1);
+    uint64_t key = fallback ? ba : bs;
+    int pos = fallback ? pa : ps;
+    uint64_t m = warp_min_u64(key);
+    return (int)__reduce_min_sync(kFull, key == m ? (uint32_t)pos : 0x7fffffffu);
   };
 
   // S multiset: replace one copy of `oldv` by `newv` (> oldv).
-  auto S_update = [&](int64_t oldv, int64_t newv) {
+  auto S_update = [&](uint64_t oldv, uint64_t newv) {
     int c_old = 0, c_new = 0;
     for (int i = lane; i < nul; i += 32) {
-      int64_t v = s_S[i];
+      uint64_t v = s_S[i];
       c_old += v < oldv;
       c_new += v < newv;
     }
@@ -453,7 +535,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     // shift S[c_old+1 .. c_new-1] left by one, then S[c_new-1] = newv
     for (int base = c_old; base < c_new - 1; base += 32) {
       int i = base + lane;
-      int64_t v = (i < c_new - 1) ? s_S[i + 1] : 0;
+      uint64_t v = (i < c_new - 1) ? s_S[i + 1] : 0;
       __syncwarp();
       if (i < c_new - 1) s_S[i] = v;
       __syncwarp();
@@ -466,23 +548,30 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   auto drain_decode = [&]() {
     if (ndw == 0) return;
     for (int j = 0; j < Dn; ++j) maybe_die_d(j);
-    warp_sort_buf(pt.dwait, ndw);
+    warp_sort_buf(g_dwait, ndw);
     uint32_t touched = 0;
     int32_t order_lane = -1;  // lane t holds the t-th touched instance
     int ntouched = 0;
     int wi = 0;
-    const int64_t tps = pt.tps;
+    uint64_t w_key = 0;
+    int32_t w_prompt = 0, w_out = 0;
     while (wi < ndw) {
       if (ul_dirty) rebuild_ulist();
       if (nul == 0) break;
-      uint64_t key = pt.dwait[wi];
-      int64_t id = key_id(key);
-      int32_t prompt = __ldg(pt.prompt + id);
-      int32_t out = __ldg(pt.output + id);
+      if ((wi & 31) == 0) {  // next 32 waiters: keys + lengths fetched in parallel
+        w_key = (wi + lane < ndw) ? g_dwait[wi + lane] : 0;
+        const int64_t wid = key_id(w_key);
+        w_prompt = (wi + lane < ndw) ? __ldg(g_prompt + wid) : 0;
+        w_out = (wi + lane < ndw) ? __ldg(g_output + wid) : 0;
+      }
+      const uint64_t key = bcast(w_key, wi & 31);
+      const int64_t id = key_id(key);
+      const int32_t prompt = bcast(w_prompt, wi & 31);
+      const int32_t out = bcast(w_out, wi & 31);
       int pos;
-      if (pt.decode_policy == kIqr) {
+      if (dec_policy == kIqr) {
         pos = iqr_select();
-      } else if (pt.decode_policy == kRandom) {
+      } else if (dec_policy == kRandom) {
         if (mti >= 312) { mt_twist(pt.mt); mti = 0; }
         uint64_t y = mt_temper(pt.mt[mti]);
         mti += 1;
@@ -493,27 +582,41 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         pos = (int)(dec_rr % nul);
         dec_rr += 1;
       }
-      c_dsel += 1;
-      int u = s_ul[pos];
-      int j = u / Dd;
-      int64_t oldK = s_K[u];
-      int64_t newK = oldK + prompt;
+      CNT(dsel, 1);
+      const int u = ul_ident ? pos : s_ul[pos];
+      const int j = u / Dd;
+      // admit_decode (engine_model.cpp:145-151): B += 1, K += prompt_len
+      const uint64_t k0 = s_PK[u];
+      const uint64_t K0 = k0 & kKMask, B0 = k0 >> 48;
+      const uint64_t K1 = K0 + (uint64_t)prompt;
+      if (B0 + 1 >= (1u << 15) || K1 >= kBOne) { error = kErrEnvelope; return; }
+      const bool stepping = d_flag(j, G_STEP);
       __syncwarp();
-      if (lane == 0) { s_B[u] += 1; s_K[u] = newK; }
-      if (pt.per_request && lane == 0) pt.o_status[id] = kStDecoding;
+      if (lane == 0) {
+        s_PK[u] = k0 + kBOne + (uint64_t)prompt;
+        if (!stepping) s_nst[u] += 1;  // stamped by the step that begins next
+        if (per_req) o_status[id] = kStDecoding;
+      }
+      if (lane == j) {
+        d_res += 1;
+        d_s1 += prompt;
+        d_s2 += (u128)(2 * K0 + (uint64_t)prompt) * (uint64_t)prompt;
+        double t = __dadd_rn(__dmul_rn(dc_req, (double)(B0 + 1)), __dmul_rn(dc_kv, (double)K1));
+        d_worst = t > d_worst ? t : d_worst;
+      }
       __syncwarp();
-      if (S_valid) S_update(oldK, newK);
-      if (pt.cap_batch > 0 && s_B[u] >= pt.cap_batch) ul_dirty = true;
+      if (S_valid) S_update(K0, K1);
+      if (cap_batch > 0 && (int64_t)B0 + 1 >= cap_batch) ul_dirty = true;
       // completion ring: finishes at step d_step + ceil(target/tps)
-      int64_t target = (int64_t)out - 1;
-      int64_t nsteps = (target + tps - 1) / tps;
-      int64_t excess = nsteps * tps - target;
-      int64_t c = bcast(d_step, j) + nsteps;
-      int b = j * R + (int)(c & (R - 1));
-      int cnt = s_bcnt[b];
+      const int64_t target = (int64_t)out - 1;
+      const int64_t nsteps = (target + tps - 1) / tps;
+      const int64_t excess = nsteps * tps - target;
+      const int64_t c = bcast(d_step, j) + nsteps;
+      const int b = j * R + (int)(c & (R - 1));
+      const int cnt = s_bcnt[b];
       if (cnt >= BC) { error = kErrOverflow; return; }
       if (lane == 0) {
-        pt.buckets[(int64_t)b * BC + cnt] =
+        g_buckets[(int64_t)b * BC + cnt] =
             make_int4((int)id, u, (int)(prompt + target + excess), (int)excess);
         s_bcnt[b] = (uint16_t)(cnt + 1);
       }
@@ -529,9 +632,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     if (wi > 0 && wi < ndw) {
       for (int base = 0; base < ndw - wi; base += 32) {
         int i = base + lane;
-        uint64_t v = (i < ndw - wi) ? pt.dwait[wi + i] : 0;
+        uint64_t v = (i < ndw - wi) ? g_dwait[wi + i] : 0;
         __syncwarp();
-        if (i < ndw - wi) pt.dwait[i] = v;
+        if (i < ndw - wi) g_dwait[i] = v;
         __syncwarp();
       }
     }
@@ -559,14 +662,14 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       bool part = s_part[g] != 0;
       int64_t outv = s_out[g];
       int64_t room = c_chunk;
-      int2* fq = pt.fifo + (int64_t)g * F;
+      int2* fq = g_fifo + (int64_t)g * F;
       while (room > 0 && h != t) {
         int2 e = fq[h & Fm];
         int64_t take = (int64_t)e.y < room ? (int64_t)e.y : room;
         room -= take;
         if (!part) {
-          pt.o_pstart[e.x] = now;
-          if (pt.per_request) pt.o_status[e.x] = kStPrefilling;
+          o_pstart[e.x] = now;
+          if (per_req) o_status[e.x] = kStPrefilling;
         }
         outv -= take;
         if (take == e.y) { h += 1; part = false; }
@@ -581,7 +684,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       terms[k] = __ddiv_rn((double)mn, (double)c_chunk);
     }
     amax = warp_max_i64(amax);
-    double dur = __dadd_rn(pt.pf_base, __dmul_rn(pt.pf_tok, (double)amax));
+    double dur = __dadd_rn(pf_base, __dmul_rn(pf_tok, (double)amax));
     int64_t t_end = now + llround_ns(dur);
     if (now >= warmup) {
       // chunk_utilization (metrics.cpp:193-202): sequential sum in DP order
@@ -592,8 +695,10 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         for (int l = 0; l < 32 && 32 * k + l < D; ++l)
           sum = __dadd_rn(sum, __shfl_sync(kFull, terms[k], l));
       }
-      util_sum = __dadd_rn(util_sum, __ddiv_rn(sum, (double)D));
-      c_passes += 1;
+      if (lane == 0) {
+        cn->util = __dadd_rn(cn->util, __ddiv_rn(sum, (double)D));
+        cn->passes += 1;
+      }
     }
     if (lane == p) {
       pflags |= F_BUSY;
@@ -624,21 +729,21 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       int64_t id = 0;
       int32_t out = 0;
       if (has) {
-        id = pt.fifo[(int64_t)(g0 + d) * F + (idx & Fm)].x;
+        id = g_fifo[(int64_t)(g0 + d) * F + (idx & Fm)].x;
         idx += 1;
-        out = __ldg(pt.output + id);
-        pt.o_ftok[id] = now;
+        out = __ldg(g_output + id);
+        o_ftok[id] = now;
       }
       bool done = has && out <= 1;   // decode_target() == 0
       bool wait = has && out > 1;
       complete_lanes(done, id, now, false);
       unsigned m = __ballot_sync(kFull, wait);
       if (wait) {
-        int32_t prompt = __ldg(pt.prompt + id);
-        pt.dwait[ndw + __popc(m & lt_mask)] = decode_key((int64_t)prompt + out, id);
+        int32_t prompt = __ldg(g_prompt + id);
+        g_dwait[ndw + __popc(m & lt_mask)] = decode_key((int64_t)prompt + out, id);
       }
       ndw += __popc(m);
-      if (ndw > pt.QD - 32) { error = kErrOverflow; }
+      if (ndw > QD - 32) { error = kErrOverflow; break; }
     }
     flush_lanes();
     if (lane == p) pflags &= ~F_BUSY;
@@ -649,14 +754,16 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   auto fifo_push = [&](int g, int64_t id, int32_t tokens) -> bool {
     int32_t t = s_tail[g];
     if (t - s_rel[g] >= F) return false;
-    pt.fifo[(int64_t)g * F + (t & Fm)] = make_int2((int)id, tokens);
+    g_fifo[(int64_t)g * F + (t & Fm)] = make_int2((int)id, tokens);
     s_tail[g] = t + 1;
     s_out[g] += tokens;
     return true;
   };
 
   // ---------------- perform_dispatch (simulation.cpp:265-342) ----------------
-  auto perform_dispatch = [&](int p) {
+  // Returns p when requests were dispatched (the caller then runs maybe_die,
+  // try_start_pass and the trailing tick, simulation.cpp:338-341), else -1.
+  auto perform_dispatch = [&](int p) -> int {
     const int g0 = p * D;
     int64_t cap[kMaxPrefillDp / 32];
 #pragma unroll
@@ -667,10 +774,10 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     // q_new keys, sorted
     const int nn = (int)(next_id - new_begin);
     uint64_t* nk = (nn <= kSmemWinKeys) ? s_wk : pt.wscr;
-    if (nn > pt.QW) { error = kErrOverflow; return; }
+    if (nn > QW) { error = kErrOverflow; return -1; }
     for (int i = lane; i < nn; i += 32) {
       int64_t id = new_begin + i;
-      nk[i] = pbaa_key(__ldg(pt.prompt + id), id);
+      nk[i] = pbaa_key(__ldg(g_prompt + id), id);
     }
     __syncwarp();
     warp_sort_buf(nk, nn);
@@ -706,8 +813,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
           for (int k = 0; k < kMaxPrefillDp / 32; ++k)
             if (k == (best >> 5)) cap[k] -= len;
           if (!fifo_push(g0 + best, id, tokens)) ovf = true;
-          pt.o_dispatch[id] = now;
-          if (pt.per_request) pt.o_status[id] = kStDispatched;
+          o_dispatch[id] = now;
+          if (per_req) o_status[id] = kStDispatched;
         }
         i += 1;
       }
@@ -717,8 +824,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     int k1 = greedy(pk, np, stopped);
     int k2 = 0;
     if (!stopped) k2 = greedy(nk, nn, stopped);
-    if (__any_sync(kFull, ovf)) { error = kErrOverflow; return; }
-    c_alloc += 1;
+    if (__any_sync(kFull, ovf)) { error = kErrOverflow; return -1; }
+    CNT(alloc, 1);
 
     // aging (prefill_alloc.cpp:70-87): pending suffix then new suffix
     int na = 0, thr = 0;
@@ -727,9 +834,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       bool valid = i < np;
       uint64_t key = valid ? pk[i] : 0;
       int32_t w = valid ? pw[i] + 1 : 0;
-      bool th = valid && w > pt.n_limit;
+      bool th = valid && w > n_limit;
       bool keep = valid && !th;
-      if (th && pt.per_request) pt.o_status[key_id(key)] = kStThrottled;
+      if (th && per_req) o_status[key_id(key)] = kStThrottled;
       unsigned m = __ballot_sync(kFull, keep);
       int pos = na + __popc(m & lt_mask);
       __syncwarp();
@@ -740,16 +847,16 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     }
     int nb = nn - k2;
     int nbk = nb;
-    if (nb > 0 && 1 > pt.n_limit) {
+    if (nb > 0 && 1 > n_limit) {
       for (int i = lane; i < nb; i += 32)
-        if (pt.per_request) pt.o_status[key_id(nk[k2 + i])] = kStThrottled;
+        if (per_req) o_status[key_id(nk[k2 + i])] = kStThrottled;
       thr += nb;
       nbk = 0;
     }
-    c_def += na + nbk;
-    c_throttled += thr;
-    if (thr > 0) c_flow += 1;
-    if (na + nbk > pt.QP) { error = kErrOverflow; return; }
+    CNT(def, na + nbk);
+    CNT(throttled, thr);
+    if (thr > 0) CNT(flow, 1);
+    if (na + nbk > QP) { error = kErrOverflow; return -1; }
     if (nbk > 0) {
       if (na == 0) {
         for (int i = lane; i < nbk; i += 32) { pk[i] = nk[k2 + i]; pw[i] = 1; }
@@ -776,13 +883,13 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
 
     if (k1 + k2 == 0) {
       if (np > 0) arm_tick(now + i_opt);
-      return;
+      return -1;
     }
     has_ld = true;
     last_disp = now;
     last_inst = p;
     // arm_watchdog (interval_control.cpp:76-86)
-    int64_t deadline = now + (int64_t)llround(__dmul_rn(pt.wd_mult, (double)t_bar));
+    int64_t deadline = now + (int64_t)llround(__dmul_rn(wd_mult, (double)t_bar));
     if (lane == p) {
       p_td += 1;
       pflags &= ~(F_EFSEEN | F_WDFIRED);
@@ -793,37 +900,30 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     }
     seq++;
     odirty = true;
-    maybe_die_p(p);
-    try_start_pass(p);
-    if (np > 0) arm_tick(now + i_opt);
+    return p;
   };
 
   // ---------------- try_dispatch (simulation.cpp:245-263) ----------------
-  auto try_dispatch = [&]() {
-    if (np + (next_id - new_begin) == 0) return;
-    if (n_active <= 0) return;
-    if (has_ld && now < last_disp + i_opt) { arm_tick(last_disp + i_opt); return; }
+  auto try_dispatch = [&]() -> int {
+    if (np + (next_id - new_begin) == 0) return -1;
+    if (n_active <= 0) return -1;
+    if (has_ld && now < last_disp + i_opt) { arm_tick(last_disp + i_opt); return -1; }
     // select_ready_instance (interval_control.cpp:50-74)
     unsigned hm = __ballot_sync(kFull, lane < P && (pflags & F_HEALTHY));
     unsigned gt = last_inst < 0 ? 0xffffffffu : (unsigned)(~((2ull << last_inst) - 1ull));
     unsigned cand = hm & gt;
     int target = cand ? __ffs(cand) - 1 : (hm ? __ffs(hm) - 1 : -1);
-    bool ready = false;
-    if (target >= 0) {
-      bool r = (p_td == 0 && !(pflags & F_BUSY)) || (pflags & F_EFSEEN) || (pflags & F_WDFIRED) ||
-               ((pflags & F_HASDL) && now >= p_deadline);
-      ready = bcast((int)r, target) != 0;
-    } else {
-      (void)bcast(0, 0);
-    }
-    if (!ready) { arm_tick(now + i_opt); return; }
-    perform_dispatch(target);
+    bool r = (p_td == 0 && !(pflags & F_BUSY)) || (pflags & F_EFSEEN) || (pflags & F_WDFIRED) ||
+             ((pflags & F_HASDL) && now >= p_deadline);
+    bool ready = __shfl_sync(kFull, (int)r, target < 0 ? 0 : target) != 0 && target >= 0;
+    if (!ready) { arm_tick(now + i_opt); return -1; }
+    return perform_dispatch(target);
   };
 
   // ---------------- baseline_dispatch (simulation.cpp:206-223) ----------------
-  auto baseline_dispatch = [&](int64_t id) {
+  auto baseline_dispatch = [&](int64_t id) -> int {
     int tp = -1, tdp = -1;
-    if (pt.policy == kLeastOutstanding) {
+    if (policy == kLeastOutstanding) {
       // least_outstanding (baselines.cpp:28-45)
       int64_t bv = kInf64;
       int bg = 0x7fffffff;
@@ -852,35 +952,28 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         break;
       }
     }
-    if (tp < 0) return;  // stays pending
-    int32_t prompt = __ldg(pt.prompt + id);
+    if (tp < 0) return -1;  // stays pending
+    int32_t prompt = __ldg(g_prompt + id);
     bool ok = true;
     if (lane == 0) {
-      pt.o_dispatch[id] = now;
-      if (pt.per_request) pt.o_status[id] = kStDispatched;
+      o_dispatch[id] = now;
+      if (per_req) o_status[id] = kStDispatched;
       ok = fifo_push(tp * D + tdp, id, prompt);
     }
-    if (!bcast((int)ok, 0)) { error = kErrOverflow; return; }
+    if (!bcast((int)ok, 0)) { error = kErrOverflow; return -1; }
     __syncwarp();
-    maybe_die_p(tp);
-    try_start_pass(tp);
+    return tp;
   };
 
-  // finish_decode_step (engine_model.cpp:181-217) + on_decode_step bookkeeping
+  // finish_decode_step (engine_model.cpp:181-217), record_step and
+  // record_kv_snapshot (simulation.cpp:486-512, metrics.cpp:50-72, 99-101)
   auto finish_step = [&](int j) {
     const int u0 = j * Dd;
-    const int64_t tps = pt.tps;
-    int64_t gen = 0;
-    for (int d = lane; d < Dd; d += 32) {
-      int64_t add = tps * (int64_t)s_nst[u0 + d];
-      s_K[u0 + d] += add;
-      gen += add;
-    }
-    __syncwarp();
     const int64_t s = bcast(d_step, j);
     const int b = j * R + (int)(s & (R - 1));
     const int n = s_bcnt[b];
-    const int4* ent = pt.buckets + (int64_t)b * BC;
+    const int4* ent = g_buckets + (int64_t)b * BC;
+    int64_t exc = 0, rel = 0;
     for (int base = 0; base < n; base += 32) {
       int e = base + lane;
       bool has = e < n;
@@ -888,56 +981,93 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       if (has) {
         int4 v = ent[e];
         id = v.x;
-        atomicAdd((unsigned long long*)&s_K[v.y], (unsigned long long)(-(int64_t)v.z));
-        atomicSub(&s_B[v.y], 1);
-        gen -= v.w;
-        ft = pt.o_ftok[id];
+        atomicAdd((unsigned long long*)&s_R[v.y], (unsigned long long)(kBOne | (uint64_t)(uint32_t)v.z));
+        exc += v.w;
+        rel += (uint32_t)v.z;
+        ft = o_ftok[id];
       }
       complete_lanes(has, id, ft, true);
     }
     __syncwarp();
-    flush_lanes();
+    if (n > 0) flush_lanes();
     if (lane == 0) s_bcnt[b] = 0;
-    gen = warp_sum_i64(gen);
-    if (lane == j) dflags &= ~G_STEP;
+    // every stamped resident produced tps tokens (minus the last-step excess
+    // of completers); completers release B and prompt + decode_done of K
+    const bool gather = ul_ident && Dn == 1;  // s_S order == unit order
+    u128 sumK2 = 0;
+    uint64_t mx = 0;
+    double worst = 0.0;
+    for (int d = lane; d < Dd; d += 32) {
+      const int u = u0 + d;
+      const uint64_t k = s_PK[u];
+      const uint64_t r = s_R[u];
+      const int32_t st = s_nst[u];
+      const uint64_t K = (k & kKMask) + (uint64_t)(tps * st) - (r & kKMask);
+      const uint64_t B = (k >> 48) - (r >> 48);
+      s_PK[u] = (B << 48) | K;
+      s_nst[u] = (int32_t)B;
+      if (r) s_R[u] = 0;
+      if (gather) s_S[u] = K;
+      mx = K > mx ? K : mx;
+      sumK2 += (u128)K * K;
+      double t = __dadd_rn(__dmul_rn(dc_req, (double)B), __dmul_rn(dc_kv, (double)K));
+      worst = t > worst ? t : worst;
+    }
+    exc = warp_sum_i64(exc);
+    rel = warp_sum_i64(rel);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sumK2 += shfl_xor_u128(sumK2, o);
+      double w = __shfl_xor_sync(kFull, worst, o);
+      worst = w > worst ? w : worst;
+    }
+    const int64_t stamped = bcast(d_res_begin, j);
+    const int64_t gen = tps * stamped - exc;
+    if (lane == j) {
+      d_res -= n;
+      d_s1 += tps * stamped - rel;
+      d_s2 = sumK2;
+      d_worst = worst;
+      dflags &= ~G_STEP;
+    }
     S_valid = false;
-    if (pt.cap_batch > 0 && n > 0) ul_dirty = true;
+    if (gather) {
+      S_gathered = true;
+      S_mx = (uint64_t)warp_max_i64((int64_t)mx);
+    }
+    if (cap_batch > 0 && n > 0) ul_dirty = true;
     __syncwarp();
-    // record_step (metrics.cpp:99-101)
-    if (now >= warmup) { c_steps += 1; c_outtok += gen; }
-    // record_kv_snapshot (simulation.cpp:486-495) -> kv_band (metrics.cpp:50-72)
     if (now >= warmup) {
-      int64_t sum = 0;
-      int cnt = 0;
-      for (int u = lane; u < U; u += 32) {
-        int fl = __shfl_sync(kFull, dflags, (u / Dd) & 31);
-        if ((fl & G_HEALTHY) && !(fl & G_DEAD)) { sum += s_K[u]; cnt += 1; }
+      CNT(steps, 1);
+      CNT(outtok, gen);
+      // kv_band over every healthy, live decode unit: mean from the exact
+      // integer sum (bit-identical), sigma from exact sum of squares
+      int64_t cnt = 0, s1 = 0;
+      u128 s2 = 0;
+      for (int q = 0; q < Dn; ++q) {
+        int fl = bcast(dflags, q);
+        int64_t a1 = bcast(d_s1, q);
+        u128 a2 = bcast_u128(d_s2, q);
+        if ((fl & G_HEALTHY) && !(fl & G_DEAD)) { cnt += Dd; s1 += a1; s2 += a2; }
       }
-      // (lanes beyond U still take part in the shuffles above via loop bound)
-      sum = warp_sum_i64(sum);
-      cnt = __reduce_add_sync(kFull, cnt);
       if (cnt > 0) {
-        double mean = __ddiv_rn((double)sum, (double)cnt);
-        double var = 0.0;
-        for (int u = lane; u < U; u += 32) {
-          int fl = __shfl_sync(kFull, dflags, (u / Dd) & 31);
-          if ((fl & G_HEALTHY) && !(fl & G_DEAD)) {
-            double dv = __dsub_rn((double)s_K[u], mean);
-            var = __dadd_rn(var, __dmul_rn(dv, dv));
-          }
+        const double n_d = (double)cnt;
+        const double mean = __ddiv_rn((double)s1, n_d);
+        const u128 xs = (u128)cnt * s2 - (u128)s1 * (u128)s1;  // n^2 * variance
+        const double var = __ddiv_rn(u128_to_f64(xs), n_d);    // == sum (v - mean)^2
+        const double sigma = sqrt(__ddiv_rn(var, n_d));
+        if (lane == 0) {
+          cn->kv_mean = __dadd_rn(cn->kv_mean, mean);
+          cn->kv_sig = __dadd_rn(cn->kv_sig, sigma);
+          cn->kv_n += 1;
         }
-        var = warp_sum_f64(var);
-        double sigma = sqrt(__ddiv_rn(var, (double)cnt));
-        kv_mean_sum = __dadd_rn(kv_mean_sum, mean);
-        kv_sig_sum = __dadd_rn(kv_sig_sum, sigma);
-        kv_n += 1;
       }
     }
   };
 
   // drop_matches (simulation.cpp:128-134)
   auto drop_matches = [&](int p) -> bool {
-    for (int i = 0; i < pt.n_drops; ++i) {
+    for (int i = 0; i < n_drops; ++i) {
       int inst = pt.drop_inst[i];
       if ((inst == -1 || inst == p) && now >= pt.drop_from[i] && now < pt.drop_until[i]) return true;
     }
@@ -945,8 +1075,14 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   };
 
   // =======================================================================
-  // event loop (SimClock::run_until, simclock.cpp:32-45)
+  // event loop (SimClock::run_until, simclock.cpp:32-45).  Each handler only
+  // decides *which* actions run; the actions themselves have one call site
+  // each (instruction-cache footprint) and run in the reference's order:
+  //   finish_pass/finish_step -> drain_decode_admissions -> begin decode step
+  //   -> try_start_pass -> [SBS EndForward ack] -> try_dispatch ->
+  //   try_start_pass(target) -> trailing tick.
   // =======================================================================
+  int64_t topo_t = (n_topo > 0) ? pt.topo_time[0] : kInf64;
   while (error == 0) {
     if (odirty) recompute_other();
     // live internal minimum: tick vs other
@@ -955,16 +1091,20 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     int ik = o_k;
     if (tick_t < it || (tick_t == it && tick_s < is)) { it = tick_t; is = tick_s; ik = 1; }
     const int64_t at = (next_id < N) ? bcast(abuf, (int)(next_id - abase)) : kInf64;
-    const int64_t tt = (topo_idx < pt.n_topo) ? pt.topo_time[topo_idx] : kInf64;
     int kind;
     int64_t et;
-    if (tt <= at && tt <= it) { kind = 4; et = tt; }      // topology (lowest seq)
-    else if (at <= it) { kind = 0; et = at; }             // arrival
+    if (topo_t <= at && topo_t <= it) { kind = 4; et = topo_t; }  // topology (lowest seq)
+    else if (at <= it) { kind = 0; et = at; }                      // arrival
     else { kind = ik; et = it; }
     if (et == kInf64 || et > horizon) break;
     now = et;
-    c_events += 1;
+    CNT(events, 1);
 
+    int start_p = -1;      // try_start_pass before the dispatch stage
+    int step_j = -1;       // decode instance whose step finished
+    int ef_p = -1;         // SBS EndForward acknowledgement
+    int64_t measured = 0;
+    bool dispatch = false;
     if (kind == 0) {
       // ---- on_arrival (simulation.cpp:196-204)
       const int64_t id = next_id;
@@ -972,14 +1112,18 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       if (next_id - abase == 32) {
         abase += 32;
         abuf = anext;
-        anext = (abase + 32 + lane < N) ? __ldg(pt.arr + abase + 32 + lane) : kInf64;
+        anext = (abase + 32 + lane < N) ? __ldg(g_arr + abase + 32 + lane) : kInf64;
       }
-      if (sbs) try_dispatch();
-      else baseline_dispatch(id);
+      if (sbs) {
+        dispatch = true;
+      } else {
+        start_p = baseline_dispatch(id);  // simulation.cpp:206-223
+        if (start_p >= 0) maybe_die_p(start_p);
+      }
     } else if (kind == 1) {
       // ---- on_tick (simulation.cpp:240-243): only the live tick reaches here
       tick_t = kInf64;
-      try_dispatch();
+      dispatch = true;
     } else if (kind == kEvEF) {
       // ---- on_end_forward (simulation.cpp:346-372)
       const int p = o_i;
@@ -987,36 +1131,10 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       odirty = true;
       maybe_die_p(p);
       if (p_flag(p, F_DEAD)) continue;
-      const int64_t measured = now - bcast(p_started, p);
+      measured = now - bcast(p_started, p);
       finish_pass(p);
-      drain_decode();
-      if (error) break;
-      try_start_pass(p);
-      if (!sbs) continue;
-      if (drop_matches(p)) { c_drop += 1; continue; }
-      // on_end_forward_sample (interval_control.cpp:26-36)
-      if (measured <= 0) {
-        c_rej += 1;
-      } else {
-        if (win_n < pt.w_size) {
-          s_wr[(win_head + win_n) % pt.w_size] = measured;
-          win_n += 1;
-          win_sum += measured;
-        } else {
-          win_sum += measured - s_wr[win_head];
-          s_wr[win_head] = measured;
-          win_head = (win_head + 1) % pt.w_size;
-        }
-        __syncwarp();
-        recompute_interval();
-      }
-      if (lane == p) {
-        p_td = p_td > 0 ? p_td - 1 : 0;
-        pflags |= F_EFSEEN;
-        pflags &= ~F_HASDL;  // disarm_watchdog
-        wd_t = kInf64;
-      }
-      try_dispatch();
+      start_p = p;
+      if (sbs) ef_p = p;
     } else if (kind == kEvWD) {
       // ---- on_watchdog (simulation.cpp:374-380) via watchdog_expired
       const int p = o_i;
@@ -1027,8 +1145,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         p_td = 0;
       }
       odirty = true;
-      c_wdf += 1;
-      if (sbs) try_dispatch();
+      CNT(wdf, 1);
+      dispatch = sbs;
     } else if (kind == kEvDS) {
       // ---- on_decode_step (simulation.cpp:497-512)
       const int j = o_i;
@@ -1037,60 +1155,115 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       maybe_die_d(j);
       if (d_flag(j, G_DEAD)) continue;
       finish_step(j);
-      drain_decode();
-      if (error) break;
-      try_begin_step(j);
+      step_j = j;
     } else {
       // ---- on_topology (simulation.cpp:382-393)
       const int inst = pt.topo_inst[topo_idx];
       const bool h = pt.topo_healthy[topo_idx] != 0;
       topo_idx += 1;
+      topo_t = (topo_idx < n_topo) ? pt.topo_time[topo_idx] : kInf64;
       if (inst < P) {
         if (lane == inst) pflags = h ? (pflags | F_HEALTHY) : (pflags & ~F_HEALTHY);
       } else {
         if (lane == inst - P) dflags = h ? (dflags | G_HEALTHY) : (dflags & ~G_HEALTHY);
         ul_dirty = true;
         S_valid = false;
+        S_gathered = false;
       }
-      int32_t na_ = n_active_count();
-      if (!sbs) continue;
-      n_active = na_;
-      recompute_interval();
-      try_dispatch();
+      int32_t na_ = __popc(__ballot_sync(kFull, lane < P && (pflags & F_HEALTHY)));
+      if (sbs) {
+        n_active = na_;
+        recompute_interval();
+        dispatch = true;
+      }
+    }
+
+    // ---- decode hand-off: hand_off_finished / on_decode_step tail
+    if (kind == kEvEF || kind == kEvDS) {
+      drain_decode();
+      if (error) break;
+      if (step_j >= 0) try_begin_step(step_j);
+    }
+    // ---- prefill passes and the SBS dispatch chain
+    for (int stage = 0; stage < 2; ++stage) {
+      if (start_p >= 0) try_start_pass(start_p);
+      if (stage == 1) {
+        if (start_p >= 0 && np > 0) arm_tick(now + i_opt);  // simulation.cpp:341
+        break;
+      }
+      if (ef_p >= 0) {
+        if (n_drops > 0 && drop_matches(ef_p)) {
+          CNT(drop, 1);  // scheduler view stays stale (simulation.cpp:359-362)
+        } else {
+          // on_end_forward_sample (interval_control.cpp:26-36)
+          if (measured <= 0) {
+            CNT(rej, 1);
+          } else {
+            if (win_n < w_size) {
+              s_wr[(win_head + win_n) % w_size] = measured;
+              win_n += 1;
+              win_sum += measured;
+            } else {
+              win_sum += measured - s_wr[win_head];
+              s_wr[win_head] = measured;
+              win_head = (win_head + 1) % w_size;
+            }
+            __syncwarp();
+            recompute_interval();
+          }
+          if (lane == ef_p) {
+            p_td = p_td > 0 ? p_td - 1 : 0;
+            pflags |= F_EFSEEN;
+            pflags &= ~F_HASDL;  // disarm_watchdog
+            wd_t = kInf64;
+          }
+          dispatch = true;
+        }
+      }
+      start_p = -1;
+      if (!dispatch) break;
+      start_p = try_dispatch();
+      if (error) break;
+      if (start_p < 0) break;
+      maybe_die_p(start_p);
     }
   }
 
   // ---- results
+  tpot_sum = warp_sum_f64(tpot_sum);
+  tpot_n = warp_sum_i64(tpot_n);
+  __syncwarp();
   if (lane == 0) {
-    res.completed = c_completed;
-    res.throttled = c_throttled;
-    res.cw = c_cw;
-    res.wr = c_wr;
-    res.passes = c_passes;
-    res.steps = c_steps;
-    res.out_tokens = c_outtok;
-    res.wd_fires = c_wdf;
-    res.dropped = c_drop;
-    res.rejected = c_rej;
-    res.deferrals = c_def;
-    res.flow = c_flow;
-    res.mask = c_mask;
-    res.fallback = c_fb;
-    res.alloc_calls = c_alloc;
-    res.dec_selects = c_dsel;
-    res.events = c_events;
+    res.completed = cn->completed;
+    res.throttled = cn->throttled;
+    res.cw = cn->cw;
+    res.wr = cn->wr;
+    res.passes = cn->passes;
+    res.steps = cn->steps;
+    res.out_tokens = cn->outtok;
+    res.wd_fires = cn->wdf;
+    res.dropped = cn->drop;
+    res.rejected = cn->rej;
+    res.deferrals = cn->def;
+    res.flow = cn->flow;
+    res.mask = cn->mask;
+    res.fallback = cn->fb;
+    res.alloc_calls = cn->alloc;
+    res.dec_selects = cn->dsel;
+    res.events = cn->events;
     res.n_ttft = n_ttft;
-    res.ttft_sum = s_ttft;
-    res.sched_sum = s_sched;
-    res.dev_sum = s_dev;
-    res.util_sum = util_sum;
-    res.kv_mean_sum = kv_mean_sum;
-    res.kv_sigma_sum = kv_sig_sum;
+    res.ttft_sum = cn->ttft;
+    res.sched_sum = cn->sched;
+    res.dev_sum = cn->dev;
+    res.util_sum = cn->util;
+    res.kv_mean_sum = cn->kv_mean;
+    res.kv_sigma_sum = cn->kv_sig;
     res.tpot_sum = tpot_sum;
-    res.kv_n = kv_n;
+    res.kv_n = cn->kv_n;
     res.tpot_n = tpot_n;
     res.error = error;
   }
+#undef CNT
   (void)kErrInvariant;
 }
 

@@ -73,7 +73,8 @@ struct DevPoint {
   int32_t QP, QW, F, R, BC, QD;
   // ---- shared-memory carve (bytes, relative to the warp's slice)
   int32_t sm_pf_out, sm_pf_head, sm_pf_tail, sm_pf_rel, sm_pf_part;
-  int32_t sm_dK, sm_dS, sm_dB, sm_dnst, sm_ulist, sm_bcnt, sm_wring, sm_wkeys;
+  int32_t sm_dPK, sm_dR, sm_dS, sm_dT, sm_dnst, sm_ulist, sm_bcnt, sm_hist, sm_wring, sm_wkeys, sm_cnt;
+  int32_t _pad2;
   int32_t sm_bytes;
   int32_t _pad1;
 };

@@ -330,14 +330,17 @@ void layout_smem(sbs::DevPoint& d) {
   d.sm_pf_tail = take(4 * PD);
   d.sm_pf_rel = take(4 * PD);
   d.sm_pf_part = take(PD);
-  d.sm_dK = take(8 * U);
-  d.sm_dS = take(8 * (size_t)next_pow2((int64_t)std::max<size_t>(U, 1)));
-  d.sm_dB = take(4 * U);
+  d.sm_dPK = take(8 * U);
+  d.sm_dR = take(8 * U);
+  d.sm_dS = take(8 * U);
+  d.sm_dT = take(8 * U);
   d.sm_dnst = take(4 * U);
   d.sm_ulist = take(2 * U);
   d.sm_bcnt = take(2 * (size_t)d.Dn * d.R);
+  d.sm_hist = take(4 * 256);
   d.sm_wring = take(8 * (size_t)d.w_size);
   d.sm_wkeys = take(8 * (size_t)sbs::kSmemWinKeys);
+  d.sm_cnt = take(256);
   d.sm_bytes = (int32_t)off;
 }
 

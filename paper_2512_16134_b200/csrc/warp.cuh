@@ -129,3 +129,63 @@ __device__ __forceinline__ int lower_bound_u64(const uint64_t* a, int n, uint64_
 }
 
 }  // namespace sbs
+
+namespace sbs {
+
+// Stable LSD radix sort (8-bit digits) of n uint64 keys with at most `nbits`
+// significant bits, by one warp, ascending.  a: keys (in/out), t: scratch of
+// n keys, hist: 256 x u32 (all shared memory).  Per pass: shared-memory
+// histogram, warp exclusive scan, then a stable scatter of 32-key chunks where
+// __match_any_sync groups equal digits and popc(peers & lanemask_lt) ranks
+// each key inside its group.
+__device__ __forceinline__ void warp_radix_sort(uint64_t* a, uint64_t* t, uint32_t* hist, int n,
+                                                int nbits) {
+  const int lane = lane_id();
+  const unsigned lt = lanemask_lt();
+  const int passes = (nbits + 7) >> 3;
+  uint64_t* src = a;
+  uint64_t* dst = t;
+  for (int p = 0; p < passes; ++p) {
+    const int sh = 8 * p;
+    for (int b = lane; b < 256; b += 32) hist[b] = 0;
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) atomicAdd(&hist[(unsigned)(src[i] >> sh) & 255u], 1u);
+    __syncwarp();
+    uint32_t v[8];
+    uint32_t s = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { v[k] = hist[8 * lane + k]; s += v[k]; }
+    uint32_t incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(kFull, incl, o);
+      if (lane >= o) incl += y;
+    }
+    uint32_t run = incl - s;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { hist[8 * lane + k] = run; run += v[k]; }
+    __syncwarp();
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + lane;
+      const bool valid = i < n;
+      const uint64_t x = valid ? src[i] : 0;
+      const unsigned dg = valid ? ((unsigned)(x >> sh) & 255u) : 256u + lane;
+      const unsigned peers = __match_any_sync(kFull, dg);
+      unsigned off = 0;
+      if (valid) {
+        off = hist[dg];
+        dst[off + __popc(peers & lt)] = x;
+      }
+      __syncwarp();
+      if (valid && (peers >> lane) == 1u) hist[dg] = off + __popc(peers);
+      __syncwarp();
+    }
+    uint64_t* tmp = src; src = dst; dst = tmp;
+  }
+  if (passes & 1) {
+    for (int i = lane; i < n; i += 32) a[i] = t[i];
+    __syncwarp();
+  }
+}
+
+}  // namespace sbs
