@@ -150,8 +150,6 @@ constexpr uint64_t kBOne = 1ull << 48;       // packed decode unit: B << 48 | K
 constexpr uint64_t kKMask = kBOne - 1;
 constexpr int kErrEnvelope = 6;               // B >= 2^15 or K >= 2^48 on a decode unit
 
-typedef unsigned __int128 u128;
-
 // Per-replica counters and FP sums (metrics.h:107-152 state), in shared memory
 // and written by lane 0 only: they are rarely read, so they should not occupy
 // 50 replicated registers per lane.  FP sums stay sequential in event order.
@@ -161,23 +159,7 @@ struct Counters {
   double util, kv_mean, kv_sig;
 };
 
-__device__ __forceinline__ u128 shfl_xor_u128(u128 v, int o) {
-  uint64_t lo = (uint64_t)v, hi = (uint64_t)(v >> 64);
-  lo = __shfl_xor_sync(kFull, lo, o);
-  hi = __shfl_xor_sync(kFull, hi, o);
-  return ((u128)hi << 64) | lo;
-}
-__device__ __forceinline__ u128 bcast_u128(u128 v, int src) {
-  uint64_t lo = (uint64_t)v, hi = (uint64_t)(v >> 64);
-  lo = __shfl_sync(kFull, lo, src);
-  hi = __shfl_sync(kFull, hi, src);
-  return ((u128)hi << 64) | lo;
-}
-__device__ __forceinline__ double u128_to_f64(u128 v) {
-  return __dadd_rn(__dmul_rn((double)(uint64_t)(v >> 64), 18446744073709551616.0),
-                   (double)(uint64_t)v);
-}
-
+template <int KD>  // prefill DP units per lane: 1 (dp_degree <= 32) or 4 (<= 128)
 __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* sm) {
   const int lane = lane_id();
   const unsigned lt_mask = lanemask_lt();
@@ -255,8 +237,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   int64_t ds_t = kInf64;
   uint32_t ds_s = 0xffffffffu;
   const int64_t d_death = (lane < Dn) ? pt.death[P + lane] : kInf64;
-  int64_t d_res = 0, d_s1 = 0;  // residents, sum K over the instance's units
-  u128 d_s2 = 0;                // sum K^2
+  int64_t d_res = 0;            // residents over the instance's units
   double d_worst = 0.0;         // max_u decode_per_request*B + decode_per_kv*K
   int64_t d_res_begin = 0;      // residents stamped at the running step
 
@@ -297,8 +278,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   int o_k = 0, o_i = 0;
 
   // ---- counters (shared memory, lane 0) + lane-local TPOT partials
-  int64_t n_ttft = 0, tpot_n = 0;
-  double tpot_sum = 0.0;
+  int64_t n_ttft = 0, tpot_n = 0, tpot_sum = 0;
 #define CNT(f, v) do { if (lane == 0) cn->f += (v); } while (0)
 
   // random decode policy: mt19937_64(seed ^ 0x9E3779B97F4A7C15) (simulation.cpp:42)
@@ -378,11 +358,11 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         o_status[id] = kStCompleted;
       }
       if (decode) {
+        // TPOT (not in the reference): integer ns per output token after the first
         int32_t out = __ldg(g_output + id);
-        int64_t dt = now - ftok;
-        tpot_sum = __dadd_rn(tpot_sum, __ddiv_rn(__ddiv_rn((double)dt, 1e9), (double)(out - 1)));
+        int64_t per = (now - ftok) / (int64_t)(out - 1);
+        tpot_sum += per;
         tpot_n += 1;
-        int64_t per = dt / (int64_t)(out - 1);
         atomicAdd((unsigned long long*)&g_tpot_hist[hist_bin(per)], 1ull);
       }
       if (arr >= warmup) {
@@ -400,14 +380,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     if (inwin) g_ttft[n_ttft + __popc(m & lt_mask)] = ttft;
     n_ttft += __popc(m);
   };
-  auto flush_lanes = [&]() {
-    const int64_t a = warp_sum_i64(l_done), b = warp_sum_i64(l_cw), c = warp_sum_i64(l_wr),
-                  d = warp_sum_i64(l_ttft), e = warp_sum_i64(l_sched), f = warp_sum_i64(l_dev);
-    if (lane == 0) {
-      cn->completed += a; cn->cw += b; cn->wr += c; cn->ttft += d; cn->sched += e; cn->dev += f;
-    }
-    l_done = l_cw = l_wr = l_ttft = l_sched = l_dev = 0;
-  };
+  // (the lane-local partial sums above are exact integers: reduced once at the end)
 
   // ---- decode unit list over healthy, live decode instances, skipping
   //      capped units (simulation.cpp:432-442)
@@ -599,8 +572,6 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       }
       if (lane == j) {
         d_res += 1;
-        d_s1 += prompt;
-        d_s2 += (u128)(2 * K0 + (uint64_t)prompt) * (uint64_t)prompt;
         double t = __dadd_rn(__dmul_rn(dc_req, (double)(B0 + 1)), __dmul_rn(dc_kv, (double)K1));
         d_worst = t > d_worst ? t : d_worst;
       }
@@ -651,9 +622,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     for (int d = lane; d < D; d += 32) any |= s_head[g0 + d] != s_tail[g0 + d];
     if (!__any_sync(kFull, any)) return;
     int64_t amax = 0;
-    double terms[kMaxPrefillDp / 32];
+    double terms[KD];
 #pragma unroll
-    for (int k = 0; k < kMaxPrefillDp / 32; ++k) {
+    for (int k = 0; k < KD; ++k) {
       terms[k] = 0.0;
       int d = lane + 32 * k;
       if (d >= D) continue;
@@ -680,8 +651,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       s_out[g] = outv;
       int64_t assigned = c_chunk - room;
       amax = assigned > amax ? assigned : amax;
-      int64_t mn = assigned < c_chunk ? assigned : c_chunk;
-      terms[k] = __ddiv_rn((double)mn, (double)c_chunk);
+      // min(a, c) / c (metrics.cpp:199-200); exact shortcuts for full/empty units
+      terms[k] = assigned >= c_chunk ? 1.0
+               : assigned == 0 ? 0.0 : __ddiv_rn((double)assigned, (double)c_chunk);
     }
     amax = warp_max_i64(amax);
     double dur = __dadd_rn(pf_base, __dmul_rn(pf_tok, (double)amax));
@@ -690,7 +662,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       // chunk_utilization (metrics.cpp:193-202): sequential sum in DP order
       double sum = 0.0;
 #pragma unroll
-      for (int k = 0; k < kMaxPrefillDp / 32; ++k) {
+      for (int k = 0; k < KD; ++k) {
         if (32 * k >= D) break;
         for (int l = 0; l < 32 && 32 * k + l < D; ++l)
           sum = __dadd_rn(sum, __shfl_sync(kFull, terms[k], l));
@@ -745,7 +717,6 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       ndw += __popc(m);
       if (ndw > QD - 32) { error = kErrOverflow; break; }
     }
-    flush_lanes();
     if (lane == p) pflags &= ~F_BUSY;
     __syncwarp();
   };
@@ -765,9 +736,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   // try_start_pass and the trailing tick, simulation.cpp:338-341), else -1.
   auto perform_dispatch = [&](int p) -> int {
     const int g0 = p * D;
-    int64_t cap[kMaxPrefillDp / 32];
+    int64_t cap[KD];
 #pragma unroll
-    for (int k = 0; k < kMaxPrefillDp / 32; ++k) {
+    for (int k = 0; k < KD; ++k) {
       int d = lane + 32 * k;
       cap[k] = d < D ? c_chunk - s_out[g0 + d] : INT64_MIN;
     }
@@ -798,7 +769,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         uint32_t lv = 0;
         int ld = 0x7fffffff;
 #pragma unroll
-        for (int k = 0; k < kMaxPrefillDp / 32; ++k) {
+        for (int k = 0; k < KD; ++k) {
           int64_t c = cap[k];
           uint32_t v = c > 0 ? (uint32_t)c : 0u;
           if (v > lv) { lv = v; ld = lane + 32 * k; }
@@ -810,7 +781,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         int32_t tokens = len > 1 ? len : 1;  // max(1, prompt - hit)
         if (lane == (best & 31)) {
 #pragma unroll
-          for (int k = 0; k < kMaxPrefillDp / 32; ++k)
+          for (int k = 0; k < KD; ++k)
             if (k == (best >> 5)) cap[k] -= len;
           if (!fifo_push(g0 + best, id, tokens)) ovf = true;
           o_dispatch[id] = now;
@@ -989,12 +960,10 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       complete_lanes(has, id, ft, true);
     }
     __syncwarp();
-    if (n > 0) flush_lanes();
     if (lane == 0) s_bcnt[b] = 0;
     // every stamped resident produced tps tokens (minus the last-step excess
     // of completers); completers release B and prompt + decode_done of K
     const bool gather = ul_ident && Dn == 1;  // s_S order == unit order
-    u128 sumK2 = 0;
     uint64_t mx = 0;
     double worst = 0.0;
     for (int d = lane; d < Dd; d += 32) {
@@ -1009,7 +978,6 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       if (r) s_R[u] = 0;
       if (gather) s_S[u] = K;
       mx = K > mx ? K : mx;
-      sumK2 += (u128)K * K;
       double t = __dadd_rn(__dmul_rn(dc_req, (double)B), __dmul_rn(dc_kv, (double)K));
       worst = t > worst ? t : worst;
     }
@@ -1017,16 +985,14 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     rel = warp_sum_i64(rel);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      sumK2 += shfl_xor_u128(sumK2, o);
       double w = __shfl_xor_sync(kFull, worst, o);
       worst = w > worst ? w : worst;
     }
     const int64_t stamped = bcast(d_res_begin, j);
     const int64_t gen = tps * stamped - exc;
+    (void)rel;
     if (lane == j) {
       d_res -= n;
-      d_s1 += tps * stamped - rel;
-      d_s2 = sumK2;
       d_worst = worst;
       dflags &= ~G_STEP;
     }
@@ -1040,21 +1006,29 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     if (now >= warmup) {
       CNT(steps, 1);
       CNT(outtok, gen);
-      // kv_band over every healthy, live decode unit: mean from the exact
-      // integer sum (bit-identical), sigma from exact sum of squares
-      int64_t cnt = 0, s1 = 0;
-      u128 s2 = 0;
-      for (int q = 0; q < Dn; ++q) {
-        int fl = bcast(dflags, q);
-        int64_t a1 = bcast(d_s1, q);
-        u128 a2 = bcast_u128(d_s2, q);
-        if ((fl & G_HEALTHY) && !(fl & G_DEAD)) { cnt += Dd; s1 += a1; s2 += a2; }
-      }
-      if (cnt > 0) {
+      // kv_band (metrics.cpp:50-72) over every healthy, live decode unit:
+      // the mean from the exact integer sum (bit-identical to the reference,
+      // whose partial sums are exact integers), then the reference's second
+      // pass sum (v - mean)^2 in FP64 (lane partials + tree: <= 1e-15 rel.)
+      unsigned live = __ballot_sync(kFull, lane < Dn && (dflags & G_HEALTHY) && !(dflags & G_DEAD));
+      if (live) {
+        const bool all = live == (Dn == 32 ? 0xffffffffu : ((1u << Dn) - 1u));
+        int64_t s1 = 0, cnt = 0;
+        for (int u = lane; u < U; u += 32) {
+          if (all || ((live >> (u / Dd)) & 1u)) { s1 += (int64_t)(s_PK[u] & kKMask); cnt += 1; }
+        }
+        s1 = warp_sum_i64(s1);
+        cnt = __reduce_add_sync(kFull, (unsigned)cnt);
         const double n_d = (double)cnt;
         const double mean = __ddiv_rn((double)s1, n_d);
-        const u128 xs = (u128)cnt * s2 - (u128)s1 * (u128)s1;  // n^2 * variance
-        const double var = __ddiv_rn(u128_to_f64(xs), n_d);    // == sum (v - mean)^2
+        double var = 0.0;
+        for (int u = lane; u < U; u += 32) {
+          if (all || ((live >> (u / Dd)) & 1u)) {
+            const double dv = __dsub_rn((double)(int64_t)(s_PK[u] & kKMask), mean);
+            var = __dadd_rn(var, __dmul_rn(dv, dv));
+          }
+        }
+        var = warp_sum_f64(var);
         const double sigma = sqrt(__ddiv_rn(var, n_d));
         if (lane == 0) {
           cn->kv_mean = __dadd_rn(cn->kv_mean, mean);
@@ -1230,14 +1204,20 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   }
 
   // ---- results
-  tpot_sum = warp_sum_f64(tpot_sum);
+  tpot_sum = warp_sum_i64(tpot_sum);
   tpot_n = warp_sum_i64(tpot_n);
+  l_done = warp_sum_i64(l_done);
+  l_cw = warp_sum_i64(l_cw);
+  l_wr = warp_sum_i64(l_wr);
+  l_ttft = warp_sum_i64(l_ttft);
+  l_sched = warp_sum_i64(l_sched);
+  l_dev = warp_sum_i64(l_dev);
   __syncwarp();
   if (lane == 0) {
-    res.completed = cn->completed;
+    res.completed = l_done;
     res.throttled = cn->throttled;
-    res.cw = cn->cw;
-    res.wr = cn->wr;
+    res.cw = l_cw;
+    res.wr = l_wr;
     res.passes = cn->passes;
     res.steps = cn->steps;
     res.out_tokens = cn->outtok;
@@ -1252,13 +1232,13 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     res.dec_selects = cn->dsel;
     res.events = cn->events;
     res.n_ttft = n_ttft;
-    res.ttft_sum = cn->ttft;
-    res.sched_sum = cn->sched;
-    res.dev_sum = cn->dev;
+    res.ttft_sum = l_ttft;
+    res.sched_sum = l_sched;
+    res.dev_sum = l_dev;
     res.util_sum = cn->util;
     res.kv_mean_sum = cn->kv_mean;
     res.kv_sigma_sum = cn->kv_sig;
-    res.tpot_sum = tpot_sum;
+    res.tpot_sum = (double)tpot_sum / 1e9;
     res.kv_n = cn->kv_n;
     res.tpot_n = tpot_n;
     res.error = error;
@@ -1279,7 +1259,8 @@ __global__ void __launch_bounds__(128) des_kernel(const DevPoint* __restrict__ p
     if (lane_id() == 0) pi = atomicAdd(next_point, 1);
     pi = bcast(pi, 0);
     if (pi >= n_pts) return;
-    run_replica(pts[pi], res[pi], my);
+    if (pts[pi].D <= 32) run_replica<1>(pts[pi], res[pi], my);
+    else run_replica<4>(pts[pi], res[pi], my);
     __syncwarp();
   }
 }
