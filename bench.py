@@ -290,13 +290,7 @@ def main():
     if errs:
         raise SystemExit(f"replica errors: {errs[:5]}")
 
-    def summary_buf(res, hist):
-        # fixed-size int64 buffer: exact sums + histograms (NCCL-reduced)
-        keys = ["generated", "completed", "alloc_calls", "decode_selects", "events",
-                "ttft_sum_ns", "window_requests", "output_tokens"]
-        v = [sum(int(r[k]) for r in res) for k in keys]
-        v += list(hist.ttft) + list(hist.tpot)
-        return torch.tensor(v, dtype=torch.int64, device=dev)
+    from paper_2512_16134_b200 import sweep
 
     # ---- timed: device-resident traces
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -314,18 +308,18 @@ def main():
             torch.cuda.synchronize()
             times.append(ev0.elapsed_time(ev1))
         res, hist = sim.results(stream=stream.cuda_stream, histograms=True)
-        buf = summary_buf(res, hist)
-        if dist:
-            dist.all_reduce(buf)
+        # final summary/histogram reduce (NCCL over NVLink at N > 1)
+        summary = sweep.unpack_summary(
+            sweep.all_reduce_summary(sweep.summary_vector(res, hist), device=dev))
     clocks = clk.summary()
     ms = statistics.mean(times)
     if dist:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    total_req = int(buf[0].item())
-    total_alloc = int(buf[2].item())
-    total_dsel = int(buf[3].item())
+    total_req = summary["generated"]
+    total_alloc = summary["alloc_calls"]
+    total_dsel = summary["decode_selects"]
     value = total_req / (ms / 1000.0)
 
     # ---- e2e: host traces -> H2D -> simulate -> D2H aggregates
@@ -394,6 +388,8 @@ def main():
                    "requests_per_gpu": n_req, "l2": "inputs (16 B/request traces) far larger than L2",
                    "parallelism": f"replicas sharded over {world} GPU(s), one warp per replica"},
         "allocations_per_s": total_alloc / (ms / 1000.0),
+        "summary": {"completed": summary["completed"], "window_requests": summary["window_requests"],
+                    "ttft_mean_s": summary.get("ttft_mean_s"), "events": summary["events"]},
         "decode_placements_per_s": total_dsel / (ms / 1000.0),
         "gpu_launches": args.steps * sim.launches_per_run,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

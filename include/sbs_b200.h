@@ -176,6 +176,7 @@ int sbs_generate_workload(const sbs_workload* spec, uint64_t seed,
 typedef struct sbs_sim sbs_sim;
 
 #define SBS_FLAG_PER_REQUEST 1u /* keep per-request timestamps (parity mode) */
+#define SBS_FLAG_LOGS 2u        /* keep run records (MetricsCollector, metrics.h:107-152) */
 
 /* traces: host arrays (uploaded here).  trace_of_point[i] selects the trace of
  * point i (NULL: point i uses trace i).  Points sharing a trace share HBM. */
@@ -195,6 +196,14 @@ int sbs_sim_results(sbs_sim* sim, sbs_aggregates* out, sbs_histograms* hist,
 int sbs_sim_requests(sbs_sim* sim, int32_t point, int64_t* dispatch_ns,
                      int64_t* prefill_start_ns, int64_t* first_token_ns,
                      int64_t* completion_ns, int8_t* status);
+/* SBS_FLAG_LOGS: the point's run records as int64 words: header
+ * kind | (payload words << 8) then payload; kinds 1 dispatch (time, instance),
+ * 2 control (time, i_opt, t_fwd_bar, n_active), 3 pass (time, instance,
+ * assigned[dp_degree]), 4 step (time, generated), 5 kv band (time, mean bits,
+ * sigma bits, min, max).  These are the records behind passes.csv,
+ * kvband.csv, control.csv and the dispatch log (metrics.cpp:194-273).
+ * With words NULL only *n_out is set. */
+int sbs_sim_log(sbs_sim* sim, int32_t point, int64_t* words, int64_t cap, int64_t* n_out);
 /* Number of kernel launches enqueued by one sbs_sim_launch. */
 int32_t sbs_sim_launches_per_run(const sbs_sim* sim);
 /* Device bytes allocated for this simulator. */

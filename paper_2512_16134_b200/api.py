@@ -171,6 +171,8 @@ def lib():
         L.sbs_sim_results.argtypes = [C.c_void_p, C.POINTER(Aggregates), C.POINTER(Histograms),
                                       C.c_void_p]
         L.sbs_sim_requests.argtypes = [C.c_void_p, C.c_int32] + [C.c_void_p] * 5
+        L.sbs_sim_log.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64,
+                                  C.POINTER(C.c_int64)]
         L.sbs_sim_launches_per_run.argtypes = [C.c_void_p]
         L.sbs_sim_device_bytes.argtypes = [C.c_void_p]
         L.sbs_sim_device_bytes.restype = C.c_int64
@@ -186,7 +188,8 @@ def lib():
 
 EXPORTED_SYMBOLS = [
     "sbs_generate_workload", "sbs_sim_create", "sbs_sim_upload_traces", "sbs_sim_launch",
-    "sbs_sim_results", "sbs_sim_requests", "sbs_sim_launches_per_run", "sbs_sim_device_bytes",
+    "sbs_sim_results", "sbs_sim_requests", "sbs_sim_log", "sbs_sim_launches_per_run",
+    "sbs_sim_device_bytes",
     "sbs_sim_destroy", "sbs_run_experiments", "sbs_prefill_allocate", "sbs_decode_select",
     "sbs_last_error", "sbs_version",
 ]
@@ -406,7 +409,8 @@ def generate_workload(point_or_cfg, pinned: bool = False) -> HostTrace:
 class Simulator:
     """Many replicas, one warp each, resident on one GPU (sbs_sim_*)."""
 
-    def __init__(self, points, traces, trace_of_point=None, per_request=False, device=0):
+    def __init__(self, points, traces, trace_of_point=None, per_request=False, logs=False,
+                 device=0):
         L = lib()
         self.points = list(points)
         self.traces = list(traces)
@@ -419,7 +423,8 @@ class Simulator:
         h = C.c_void_p()
         _check(L.sbs_sim_create(self._exp, n, self._tr, len(self.traces),
                                 C.cast(self._map, C.c_void_p) if self._map is not None else None,
-                                1 if per_request else 0, device, C.byref(h)))
+                                (1 if per_request else 0) | (2 if logs else 0), device,
+                                C.byref(h)))
         self.handle = h
         self.n = n
 
@@ -451,6 +456,14 @@ class Simulator:
         return {"dispatch": cols[0][:n], "prefill_start": cols[1][:n],
                 "first_token": cols[2][:n], "completion": cols[3][:n], "status": st[:n]}
 
+    def log(self, point: int) -> np.ndarray:
+        """Run records of one point (SBS_FLAG_LOGS), int64 words."""
+        n = C.c_int64(0)
+        _check(lib().sbs_sim_log(self.handle, point, None, 0, C.byref(n)))
+        buf = np.empty(max(n.value, 1), np.int64)
+        _check(lib().sbs_sim_log(self.handle, point, buf.ctypes.data, len(buf), C.byref(n)))
+        return buf[: n.value]
+
     @property
     def launches_per_run(self):
         return lib().sbs_sim_launches_per_run(self.handle)
@@ -471,19 +484,21 @@ class Simulator:
             pass
 
 
-def run_experiment(cfg: dict, per_request=False, device=0):
+def run_experiment(cfg: dict, per_request=False, logs=False, device=0):
     """≙ sbsim::run_experiment (simulation.h:33) on the GPU: returns a dict with
-    the Aggregates fields (and per-request arrays when per_request)."""
+    the Aggregates fields (and per-request arrays / run records on request)."""
     pt = experiment_from_config(cfg)
     tr = generate_workload(pt)
-    sim = Simulator([pt], [tr], per_request=per_request, device=device)
+    sim = Simulator([pt], [tr], per_request=per_request or logs, logs=logs, device=device)
     try:
         sim.launch()
         agg = sim.results()[0]
-        out = {"agg": agg, "digest": tr.digest, "n": tr.n}
-        if per_request:
+        out = {"agg": agg, "digest": tr.digest, "n": tr.n, "trace": tr}
+        if per_request or logs:
             out["requests"] = sim.requests(0)
-            out["trace"] = tr
+        if logs:
+            out["log"] = sim.log(0)
+            out["c_chunk"] = int(pt.exp.cluster.c_chunk)
         return out
     finally:
         sim.close()

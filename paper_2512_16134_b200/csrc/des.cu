@@ -159,7 +159,9 @@ struct Counters {
   double util, kv_mean, kv_sig;
 };
 
-template <int KD>  // prefill DP units per lane: 1 (dp_degree <= 32) or 4 (<= 128)
+// KD: prefill DP units per lane, 1 (dp_degree <= 32) or 4 (<= 128).
+// LOG: keep run records (compiled out of the sweep kernel).
+template <int KD, bool LOG>
 __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* sm) {
   const int lane = lane_id();
   const unsigned lt_mask = lanemask_lt();
@@ -192,6 +194,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   int4* const g_buckets = pt.buckets;
   uint64_t* const g_dwait = pt.dwait;
   int64_t* const g_tpot_hist = pt.tpot_hist;
+  int64_t* const g_log = LOG ? pt.log : nullptr;
+  const int64_t log_cap = LOG ? pt.log_cap : 0;
+  int64_t log_n = 0;
 
   // ---- shared-memory carve
   int64_t* s_out = (int64_t*)(sm + pt.sm_pf_out);
@@ -280,6 +285,20 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   // ---- counters (shared memory, lane 0) + lane-local TPOT partials
   int64_t n_ttft = 0, tpot_n = 0, tpot_sum = 0;
 #define CNT(f, v) do { if (lane == 0) cn->f += (v); } while (0)
+  // append one fixed-size record (lane 0); overflow is reported, never silent
+  auto log_rec = [&](int kind, int nw, int64_t a, int64_t b, int64_t c, int64_t d, int64_t e) {
+    if (log_n + 1 + nw > log_cap) { log_n = log_cap + 1; error = kErrOverflow; return; }
+    if (lane == 0) {
+      int64_t* w = g_log + log_n;
+      w[0] = kind | ((int64_t)nw << 8);
+      if (nw > 0) w[1] = a;
+      if (nw > 1) w[2] = b;
+      if (nw > 2) w[3] = c;
+      if (nw > 3) w[4] = d;
+      if (nw > 4) w[5] = e;
+    }
+    log_n += 1 + nw;
+  };
 
   // random decode policy: mt19937_64(seed ^ 0x9E3779B97F4A7C15) (simulation.cpp:42)
   if (dec_policy == kRandom) {
@@ -623,6 +642,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     if (!__any_sync(kFull, any)) return;
     int64_t amax = 0;
     double terms[KD];
+    int64_t asg[KD];
 #pragma unroll
     for (int k = 0; k < KD; ++k) {
       terms[k] = 0.0;
@@ -650,12 +670,29 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       s_part[g] = part ? 1 : 0;
       s_out[g] = outv;
       int64_t assigned = c_chunk - room;
+      asg[k] = assigned;
       amax = assigned > amax ? assigned : amax;
       // min(a, c) / c (metrics.cpp:199-200); exact shortcuts for full/empty units
       terms[k] = assigned >= c_chunk ? 1.0
                : assigned == 0 ? 0.0 : __ddiv_rn((double)assigned, (double)c_chunk);
     }
     amax = warp_max_i64(amax);
+    if (g_log) {  // record_pass (simulation.cpp:229, metrics.cpp:76-86)
+      if (log_n + 3 + D > log_cap) {
+        log_n = log_cap + 1;
+        error = kErrOverflow;
+      } else {
+        if (lane == 0) {
+          g_log[log_n] = LOG_PASS | ((int64_t)(2 + D) << 8);
+          g_log[log_n + 1] = now;
+          g_log[log_n + 2] = p;
+        }
+#pragma unroll
+        for (int k = 0; k < KD; ++k)
+          if (lane + 32 * k < D) g_log[log_n + 3 + lane + 32 * k] = asg[k];
+        log_n += 3 + D;
+      }
+    }
     double dur = __dadd_rn(pf_base, __dmul_rn(pf_tok, (double)amax));
     int64_t t_end = now + llround_ns(dur);
     if (now >= warmup) {
@@ -871,6 +908,10 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     }
     seq++;
     odirty = true;
+    if (g_log) {  // simulation.cpp:335-336
+      log_rec(LOG_DISPATCH, 2, now, p, 0, 0, 0);
+      log_rec(LOG_CONTROL, 4, now, i_opt, t_bar, n_active, 0);
+    }
     return p;
   };
 
@@ -933,6 +974,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     }
     if (!bcast((int)ok, 0)) { error = kErrOverflow; return -1; }
     __syncwarp();
+    if (g_log) log_rec(LOG_DISPATCH, 2, now, tp, 0, 0, 0);  // simulation.cpp:219
     return tp;
   };
 
@@ -1006,31 +1048,56 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     if (now >= warmup) {
       CNT(steps, 1);
       CNT(outtok, gen);
+    }
+    if (g_log) log_rec(LOG_STEP, 2, now, gen, 0, 0, 0);  // record_step (simulation.cpp:507)
+    if (now >= warmup || g_log) {
       // kv_band (metrics.cpp:50-72) over every healthy, live decode unit:
       // the mean from the exact integer sum (bit-identical to the reference,
       // whose partial sums are exact integers), then the reference's second
-      // pass sum (v - mean)^2 in FP64 (lane partials + tree: <= 1e-15 rel.)
+      // pass sum (v - mean)^2 in FP64: lane partials + tree (<= 1e-15 rel.),
+      // or, when run records are kept, sequentially in unit order (bit-exact).
       unsigned live = __ballot_sync(kFull, lane < Dn && (dflags & G_HEALTHY) && !(dflags & G_DEAD));
       if (live) {
         const bool all = live == (Dn == 32 ? 0xffffffffu : ((1u << Dn) - 1u));
-        int64_t s1 = 0, cnt = 0;
+        int64_t s1 = 0, cnt = 0, vmin = kInf64, vmax = -1;
         for (int u = lane; u < U; u += 32) {
-          if (all || ((live >> (u / Dd)) & 1u)) { s1 += (int64_t)(s_PK[u] & kKMask); cnt += 1; }
+          if (all || ((live >> (u / Dd)) & 1u)) {
+            const int64_t v = (int64_t)(s_PK[u] & kKMask);
+            s1 += v;
+            cnt += 1;
+            vmin = v < vmin ? v : vmin;
+            vmax = v > vmax ? v : vmax;
+          }
         }
         s1 = warp_sum_i64(s1);
         cnt = __reduce_add_sync(kFull, (unsigned)cnt);
         const double n_d = (double)cnt;
         const double mean = __ddiv_rn((double)s1, n_d);
         double var = 0.0;
-        for (int u = lane; u < U; u += 32) {
-          if (all || ((live >> (u / Dd)) & 1u)) {
-            const double dv = __dsub_rn((double)(int64_t)(s_PK[u] & kKMask), mean);
-            var = __dadd_rn(var, __dmul_rn(dv, dv));
+        if (g_log) {
+          if (lane == 0)
+            for (int u = 0; u < U; ++u)
+              if (all || ((live >> (u / Dd)) & 1u)) {
+                const double dv = __dsub_rn((double)(int64_t)(s_PK[u] & kKMask), mean);
+                var = __dadd_rn(var, __dmul_rn(dv, dv));
+              }
+          var = bcast(var, 0);
+        } else {
+          for (int u = lane; u < U; u += 32) {
+            if (all || ((live >> (u / Dd)) & 1u)) {
+              const double dv = __dsub_rn((double)(int64_t)(s_PK[u] & kKMask), mean);
+              var = __dadd_rn(var, __dmul_rn(dv, dv));
+            }
           }
+          var = warp_sum_f64(var);
         }
-        var = warp_sum_f64(var);
         const double sigma = sqrt(__ddiv_rn(var, n_d));
-        if (lane == 0) {
+        if (g_log) {
+          vmin = warp_min_i64(vmin);
+          vmax = warp_max_i64(vmax);
+          log_rec(LOG_KV, 5, now, __double_as_longlong(mean), __double_as_longlong(sigma), vmin, vmax);
+        }
+        if (now >= warmup && lane == 0) {
           cn->kv_mean = __dadd_rn(cn->kv_mean, mean);
           cn->kv_sig = __dadd_rn(cn->kv_sig, sigma);
           cn->kv_n += 1;
@@ -1057,6 +1124,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   //   try_start_pass(target) -> trailing tick.
   // =======================================================================
   int64_t topo_t = (n_topo > 0) ? pt.topo_time[0] : kInf64;
+  if (g_log && sbs) log_rec(LOG_CONTROL, 4, 0, i_opt, t_bar, n_active, 0);  // simulation.cpp:152
   while (error == 0) {
     if (odirty) recompute_other();
     // live internal minimum: tick vs other
@@ -1148,6 +1216,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       if (sbs) {
         n_active = na_;
         recompute_interval();
+        if (g_log) log_rec(LOG_CONTROL, 4, now, i_opt, t_bar, n_active, 0);  // simulation.cpp:391
         dispatch = true;
       }
     }
@@ -1191,6 +1260,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
             pflags &= ~F_HASDL;  // disarm_watchdog
             wd_t = kInf64;
           }
+          if (g_log) log_rec(LOG_CONTROL, 4, now, i_opt, t_bar, n_active, 0);  // simulation.cpp:370
           dispatch = true;
         }
       }
@@ -1241,6 +1311,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     res.tpot_sum = (double)tpot_sum / 1e9;
     res.kv_n = cn->kv_n;
     res.tpot_n = tpot_n;
+    res.log_n = log_n;
     res.error = error;
   }
 #undef CNT
@@ -1248,7 +1319,10 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
 }
 
 // Persistent kernel: each warp grabs replicas until none are left (the host
-// orders replicas by estimated cost, longest first).
+// orders replicas by estimated cost, longest first).  One instantiation per
+// (prefill DP units per lane, run records) so each keeps its own registers and
+// instruction footprint.
+template <int KD, bool LOG>
 __global__ void __launch_bounds__(128) des_kernel(const DevPoint* __restrict__ pts, int n_pts,
                                                   int* __restrict__ next_point,
                                                   DevResult* __restrict__ res, int smem_per_warp) {
@@ -1259,8 +1333,7 @@ __global__ void __launch_bounds__(128) des_kernel(const DevPoint* __restrict__ p
     if (lane_id() == 0) pi = atomicAdd(next_point, 1);
     pi = bcast(pi, 0);
     if (pi >= n_pts) return;
-    if (pts[pi].D <= 32) run_replica<1>(pts[pi], res[pi], my);
-    else run_replica<4>(pts[pi], res[pi], my);
+    run_replica<KD, LOG>(pts[pi], res[pi], my);
     __syncwarp();
   }
 }
@@ -1340,17 +1413,24 @@ __global__ void __launch_bounds__(256) finalize_kernel(const DevPoint* __restric
 // host-callable launchers (C++ linkage, used by sbs_host.cpp)
 // ---------------------------------------------------------------------------
 namespace sbs {
-cudaError_t launch_des(const DevPoint* d_pts, int n_pts, int* d_counter, DevResult* d_res,
-                       int smem_per_warp, int warps_per_block, int n_blocks, cudaStream_t st) {
+// variant: bit 0 = dp_degree > 32 (KD 4), bit 1 = run records
+cudaError_t launch_des(int variant, const DevPoint* d_pts, int n_pts, int* d_counter,
+                       DevResult* d_res, int smem_per_warp, int warps_per_block, int n_blocks,
+                       cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(d_counter, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
   size_t smem = (size_t)smem_per_warp * warps_per_block;
-  e = cudaFuncSetAttribute(des_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  void (*k)(const DevPoint*, int, int*, DevResult*, int) =
+      variant == 0 ? des_kernel<1, false> : variant == 1 ? des_kernel<4, false>
+    : variant == 2 ? des_kernel<1, true> : des_kernel<4, true>;
+  e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  des_kernel<<<n_blocks, 32 * warps_per_block, smem, st>>>(d_pts, n_pts, d_counter, d_res,
-                                                           smem_per_warp);
-  e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  k<<<n_blocks, 32 * warps_per_block, smem, st>>>(d_pts, n_pts, d_counter, d_res, smem_per_warp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const DevPoint* d_pts, int n_pts, DevResult* d_res, cudaStream_t st) {
+  if (n_pts == 0) return cudaSuccess;
   finalize_kernel<<<n_pts, 256, 0, st>>>(d_pts, d_res);
   return cudaGetLastError();
 }

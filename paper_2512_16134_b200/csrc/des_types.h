@@ -70,6 +70,8 @@ struct DevPoint {
   uint64_t* dwait;
   uint64_t* mt;
   int64_t* tpot_hist;  // kHistBins
+  int64_t* log;        // optional run records (parity / report files), LOG_* below
+  int64_t log_cap;     // words
   int32_t QP, QW, F, R, BC, QD;
   // ---- shared-memory carve (bytes, relative to the warp's slice)
   int32_t sm_pf_out, sm_pf_head, sm_pf_tail, sm_pf_rel, sm_pf_part;
@@ -77,6 +79,16 @@ struct DevPoint {
   int32_t _pad2;
   int32_t sm_bytes;
   int32_t _pad1;
+};
+
+// Run-record log (MetricsCollector records, metrics.h:107-152), one stream of
+// int64 words per replica: header = kind | (payload words << 8), then payload.
+enum LogKind : int32_t {
+  LOG_DISPATCH = 1,  // time, instance                      (record_dispatch)
+  LOG_CONTROL = 2,   // time, i_opt, t_fwd_bar, n_active      (record_control)
+  LOG_PASS = 3,      // time, instance, assigned[D]           (record_pass)
+  LOG_STEP = 4,      // time, generated                       (record_step)
+  LOG_KV = 5,        // time, mean bits, sigma bits, min, max (record_kv / kv_band)
 };
 
 struct DevResult {
@@ -88,6 +100,7 @@ struct DevResult {
   int64_t kv_n, tpot_n;
   int64_t ttft_sel[4];  // order statistics at ranks lo50, hi50, lo95, hi95
   int64_t ttft_hist[kHistBins];
+  int64_t log_n;        // words written (== log_cap + 1 on overflow)
   int32_t error;
   int32_t _pad;
 };

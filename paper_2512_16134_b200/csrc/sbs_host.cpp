@@ -30,8 +30,10 @@
 #include "des_types.h"
 
 namespace sbs {
-cudaError_t launch_des(const DevPoint* d_pts, int n_pts, int* d_counter, DevResult* d_res,
-                       int smem_per_warp, int warps_per_block, int n_blocks, cudaStream_t st);
+cudaError_t launch_des(int variant, const DevPoint* d_pts, int n_pts, int* d_counter,
+                       DevResult* d_res, int smem_per_warp, int warps_per_block, int n_blocks,
+                       cudaStream_t st);
+cudaError_t launch_finalize(const DevPoint* d_pts, int n_pts, DevResult* d_res, cudaStream_t st);
 struct PbaaArgs {
   int32_t n_windows;
   const int64_t* req_off;
@@ -279,6 +281,7 @@ struct PointHost {
   int trace = 0;
   // capacities (grown on overflow)
   int32_t F = 0, QP = 0, QW = 0, BC = 0, QD = 0;
+  int64_t LOG = 0;
   void* arena = nullptr;
   size_t arena_bytes = 0;
   void* fault_buf = nullptr;
@@ -295,7 +298,8 @@ struct sbs_sim {
   uint32_t flags = 0;
   std::vector<PointHost> pts;
   std::vector<TraceDev> traces;
-  std::vector<int> order;  // device slot -> point index (cost-descending)
+  std::vector<int> order;  // device slot -> point index (grouped by variant, cost-descending)
+  int group_begin[5] = {0, 0, 0, 0, 0};  // slots of kernel variant v: [group_begin[v], group_begin[v+1])
   sbs::DevPoint* d_pts = nullptr;
   sbs::DevResult* d_res = nullptr;
   int* d_counter = nullptr;
@@ -303,6 +307,7 @@ struct sbs_sim {
   int smem_per_warp = 0;
   int warps_per_block = 4;
   int n_blocks = 0;
+  int n_launches = 0;
   int64_t device_bytes = 0;
   int sm_count = 148;
 };
@@ -459,6 +464,8 @@ void build_point(sbs_sim& s, PointHost& p) {
   size_t o_dw = carve(8 * (size_t)p.QD);
   size_t o_mt = carve(8 * 312);
   size_t o_th = carve(8 * sbs::kHistBins);
+  const bool logs = (s.flags & SBS_FLAG_LOGS) != 0;
+  size_t o_log = logs ? carve(8 * (size_t)p.LOG) : 0;
   if (p.arena == nullptr || p.arena_bytes < sz) {
     if (p.arena) cudaFree(p.arena);
     p.arena = nullptr;
@@ -482,6 +489,8 @@ void build_point(sbs_sim& s, PointHost& p) {
   d.dwait = (uint64_t*)(b + o_dw);
   d.mt = (uint64_t*)(b + o_mt);
   d.tpot_hist = (int64_t*)(b + o_th);
+  d.log = logs ? (int64_t*)(b + o_log) : nullptr;
+  d.log_cap = logs ? p.LOG : 0;
   layout_smem(d);
   p.cost = (double)t.n * (1.0 + (double)d.U / 64.0) * (1.0 + (double)(d.P * d.D) / 256.0);
 }
@@ -512,6 +521,8 @@ void initial_caps(PointHost& p, const TraceDev& t) {
   p.QW = 4096;
   p.BC = 64;
   p.QD = 1024;
+  // run records: ~ a pass + a step + a control sample per few requests
+  p.LOG = std::max<int64_t>(1 << 16, t.n * (16 + 2 * (int64_t)c.dp_degree / 8));
 }
 
 void grow_caps(PointHost& p) {
@@ -520,6 +531,39 @@ void grow_caps(PointHost& p) {
   p.QW = std::min<int32_t>(p.QW * 2, 1 << 28);
   p.BC = std::min<int32_t>(p.BC * 2, 32768);
   p.QD = std::min<int32_t>(p.QD * 2, 1 << 28);
+  p.LOG = std::min<int64_t>(p.LOG * 2, (int64_t)1 << 34);
+}
+
+int variant_of(const PointHost& p) {
+  return (p.dp.D > 32 ? 1 : 0) | (p.dp.log != nullptr ? 2 : 0);
+}
+
+void order_points(sbs_sim& s) {
+  const int n = (int)s.pts.size();
+  s.order.resize(n);
+  for (int i = 0; i < n; ++i) s.order[i] = i;
+  std::stable_sort(s.order.begin(), s.order.end(), [&](int a, int b) {
+    int va = variant_of(s.pts[a]), vb = variant_of(s.pts[b]);
+    if (va != vb) return va < vb;
+    return s.pts[a].cost > s.pts[b].cost;
+  });
+  for (int v = 0; v <= 4; ++v) s.group_begin[v] = 0;
+  for (int i = 0; i < n; ++i) s.group_begin[variant_of(s.pts[s.order[i]]) + 1] += 1;
+  for (int v = 1; v <= 4; ++v) s.group_begin[v] += s.group_begin[v - 1];
+}
+
+void launch_all(sbs_sim& s, cudaStream_t st) {
+  s.n_launches = 0;
+  for (int v = 0; v < 4; ++v) {
+    const int b = s.group_begin[v], e = s.group_begin[v + 1];
+    if (e <= b) continue;
+    const int blocks = std::max(1, std::min(s.n_blocks, (e - b + s.warps_per_block - 1) / s.warps_per_block));
+    CUDA_OR_THROW(sbs::launch_des(v, s.d_pts + b, e - b, s.d_counter + v, s.d_res + b,
+                                  s.smem_per_warp, s.warps_per_block, blocks, st));
+    s.n_launches += 1;
+  }
+  CUDA_OR_THROW(sbs::launch_finalize(s.d_pts, (int)s.order.size(), s.d_res, st));
+  s.n_launches += 1;
 }
 
 void upload_points(sbs_sim& s) {
@@ -711,13 +755,10 @@ int sbs_sim_create(const sbs_experiment* points, int32_t n_points, const sbs_tra
       build_point(*s, p);
       s->device_bytes += (int64_t)p.arena_bytes;
     }
-    s->order.resize(n_points);
-    for (int i = 0; i < n_points; ++i) s->order[i] = i;
-    std::stable_sort(s->order.begin(), s->order.end(),
-                     [&](int a, int b) { return s->pts[a].cost > s->pts[b].cost; });
+    order_points(*s);
     CUDA_OR_THROW(cudaMalloc(&s->d_pts, sizeof(sbs::DevPoint) * n_points));
     CUDA_OR_THROW(cudaMalloc(&s->d_res, sizeof(sbs::DevResult) * n_points));
-    CUDA_OR_THROW(cudaMalloc(&s->d_counter, sizeof(int)));
+    CUDA_OR_THROW(cudaMalloc(&s->d_counter, 4 * sizeof(int)));
     s->h_res.resize(n_points);
     upload_points(*s);
     return SBS_OK;
@@ -743,15 +784,16 @@ int sbs_sim_launch(sbs_sim* s, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     CUDA_OR_THROW(cudaSetDevice(s->device));
     for (auto& p : s->pts) reset_point(p, st);
-    CUDA_OR_THROW(sbs::launch_des(s->d_pts, (int)s->order.size(), s->d_counter, s->d_res,
-                                  s->smem_per_warp, s->warps_per_block, s->n_blocks, st));
+    launch_all(*s, st);
     return SBS_OK;
   });
 }
 
 int32_t sbs_sim_launches_per_run(const sbs_sim* s) {
-  (void)s;
-  return 2;  // des_kernel + finalize_kernel (memsets are not kernels of ours)
+  // one des_kernel per variant group + finalize_kernel (memsets are not ours)
+  int n = 1;
+  for (int v = 0; v < 4; ++v) n += s->group_begin[v + 1] > s->group_begin[v] ? 1 : 0;
+  return n;
 }
 
 int64_t sbs_sim_device_bytes(const sbs_sim* s) { return s->device_bytes; }
@@ -779,8 +821,7 @@ int sbs_sim_results(sbs_sim* s, sbs_aggregates* out, sbs_histograms* hist, void*
       if (attempt >= 12) throw Error{SBS_ERR_OVERFLOW, "device arena overflow persists"};
       upload_points(*s);
       for (auto& p : s->pts) reset_point(p, st);
-      CUDA_OR_THROW(sbs::launch_des(s->d_pts, n, s->d_counter, s->d_res, s->smem_per_warp,
-                                    s->warps_per_block, s->n_blocks, st));
+      launch_all(*s, st);
     }
     int rc = SBS_OK;
     if (hist) std::memset(hist, 0, sizeof(*hist));
@@ -819,6 +860,24 @@ int sbs_sim_requests(sbs_sim* s, int32_t point, int64_t* dispatch_ns, int64_t* p
     if (first_token_ns) CUDA_OR_THROW(cudaMemcpy(first_token_ns, d.o_ftok, 8 * n, cudaMemcpyDeviceToHost));
     if (completion_ns) CUDA_OR_THROW(cudaMemcpy(completion_ns, d.o_comp, 8 * n, cudaMemcpyDeviceToHost));
     if (status) CUDA_OR_THROW(cudaMemcpy(status, d.o_status, n, cudaMemcpyDeviceToHost));
+    return SBS_OK;
+  });
+}
+
+int sbs_sim_log(sbs_sim* s, int32_t point, int64_t* words, int64_t cap, int64_t* n_out) {
+  return guarded([&] {
+    if (!(s->flags & SBS_FLAG_LOGS))
+      throw Error{SBS_ERR_CONFIG, "simulator was created without SBS_FLAG_LOGS"};
+    if (point < 0 || point >= (int)s->pts.size()) throw Error{SBS_ERR_CONFIG, "point out of range"};
+    CUDA_OR_THROW(cudaSetDevice(s->device));
+    int slot = -1;
+    for (size_t i = 0; i < s->order.size(); ++i)
+      if (s->order[i] == point) slot = (int)i;
+    const int64_t n = s->h_res[slot].log_n;
+    if (n_out) *n_out = n;
+    if (words == nullptr) return SBS_OK;
+    if (n > cap) return fail(SBS_ERR_OVERFLOW, "log buffer too small");
+    CUDA_OR_THROW(cudaMemcpy(words, s->pts[point].dp.log, 8 * (size_t)n, cudaMemcpyDeviceToHost));
     return SBS_OK;
   });
 }

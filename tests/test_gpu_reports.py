@@ -1,0 +1,96 @@
+"""GPU: report files and the reference's acceptance checks, from GPU runs.
+
+* requests.csv / passes.csv / kvband.csv / control.csv rebuilt from the DES
+  kernel's run records are byte-identical to the reference's writers
+  (metrics.cpp:194-273), checked against the sha256 of the reference's files
+  (tests/golden/csv_sha256.json) — acceptance check 9's artefacts.
+* Acceptance checks 1, 5, 6, 8 (acceptance.cpp:69-87, 193-223, 482-530)
+  evaluated on GPU results with the reference's thresholds.
+"""
+import copy
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+import paper_2512_16134_b200 as P
+from paper_2512_16134_b200 import reports
+from oracle import ref
+from tests.common import CASES, GOLD
+
+pytestmark = pytest.mark.gpu
+SHA = json.load(open(GOLD / "csv_sha256.json"))
+HAVE_REF = ref.available()
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_report_files_byte_identical(name):
+    run = P.run_experiment(CASES[name], logs=True)
+    csvs = reports.all_csvs(run)
+    for kind, text in csvs.items():
+        got = hashlib.sha256(text.encode()).hexdigest()
+        if got != SHA[name][kind] and HAVE_REF:
+            want = ref.run(CASES[name], csv=True)["csv"][kind].splitlines()
+            mine = text.splitlines()
+            bad = next(i for i, (a, b) in enumerate(zip(mine + [""], want + [""])) if a != b)
+            pytest.fail(f"{name}/{kind} line {bad}: gpu={mine[bad:bad+1]} ref={want[bad:bad+1]}")
+        assert got == SHA[name][kind], f"{name}/{kind}.csv differs from the reference"
+
+
+def _load(name):
+    return json.load(open(GOLD / "configs" / f"{name}.json"))
+
+
+def test_acceptance_1_wait_shift_oracle():
+    cfg = _load("oracle_n8")
+    cfg["scheduler"]["policy"] = "immediate"
+    wait_imm = P.run_experiment(cfg)["agg"]["total_wait_mean_s"]
+    cfg["scheduler"]["policy"] = "sbs"
+    wait_sbs = P.run_experiment(cfg)["agg"]["total_wait_mean_s"]
+    assert 0.45 <= wait_imm <= 0.55
+    assert 0.05625 <= wait_sbs <= 0.06875
+
+
+def test_acceptance_5_6_decode_balance_and_throughput():
+    cfg = _load("decode_dp32")
+    iqr = P.run_experiment(cfg)["agg"]
+    cfg["scheduler"]["decode_policy"] = "random"
+    rnd = P.run_experiment(cfg)["agg"]
+    assert iqr["kv_sigma_time_avg"] / rnd["kv_sigma_time_avg"] <= 0.70
+    assert iqr["output_tokens_per_s"] / rnd["output_tokens_per_s"] >= 1.05
+
+
+def test_acceptance_8_watchdog_liveness():
+    cfg = _load("liveness")
+    run = P.run_experiment(cfg, logs=True)
+    log = reports.parse_log(run["log"])
+    t_bar = round(cfg["cluster"]["t_default_s"] * 1e9)
+    i_opt = (t_bar + round(cfg["cluster"]["l_net_s"] * 1e9)) // cfg["cluster"]["n_instances_prefill"]
+    bound = round(5.0 * t_bar) + i_opt
+    per = {}
+    for t, inst in log["dispatch"]:
+        per.setdefault(inst, []).append(t)
+    worst = 0
+    for inst in range(cfg["cluster"]["n_instances_prefill"]):
+        ts = per.get(inst, [])
+        assert len(ts) >= 2
+        gaps = [ts[0]] + [b - a for a, b in zip(ts, ts[1:])]
+        worst = max(worst, max(gaps))
+    assert worst <= bound and run["agg"]["completed"] > 0
+    assert run["agg"]["watchdog_fires"] == 36  # reference value
+
+
+@pytest.mark.skipif(not HAVE_REF, reason="compiled reference unavailable on this box")
+def test_report_files_random_configs_vs_reference():
+    rng = np.random.default_rng(77)
+    for t in range(12):
+        c = copy.deepcopy(CASES[["short_3k", "decode_dp32", "cfg2_20s"][t % 3]])
+        c["workload"]["duration_s"] = float(rng.uniform(2, 8))
+        c["cluster"]["dp_degree"] = int(rng.choice([1, 3, 8, 40]))
+        c["scheduler"]["policy"] = str(rng.choice(["sbs", "immediate", "least_outstanding"]))
+        c["sim"]["seed"] = int(rng.integers(0, 10**6))
+        mine = reports.all_csvs(P.run_experiment(c, logs=True))
+        want = ref.run(c, csv=True)["csv"]
+        for kind in mine:
+            assert mine[kind] == want[kind], f"random#{t} {kind}"
