@@ -242,6 +242,10 @@ typedef struct sbs_window_batch {
   uint8_t* flow;
 } sbs_window_batch;
 int sbs_prefill_allocate(const sbs_window_batch* batch, void* stream);
+/* Asynchronous form: enqueue only.  `error_out` is a DEVICE int32 the caller
+ * zeroes beforehand; the kernel sets it to SBS_ERR_OVERFLOW when a window
+ * exceeds the kernel envelope (1024 requests, 1024 DP units). */
+int sbs_prefill_allocate_async(const sbs_window_batch* batch, int32_t* error_out, void* stream);
 
 /* Batched IQR-masked lexicographic decode selection (select_decode_unit,    */
 /* decode_alloc.cpp:38-81).  Call c considers units [unit_off[c],           */
@@ -259,6 +263,9 @@ typedef struct sbs_decode_batch {
   double* threshold_out;
 } sbs_decode_batch;
 int sbs_decode_select(const sbs_decode_batch* batch, void* stream);
+/* Asynchronous form (see sbs_prefill_allocate_async); error 3 = empty call,
+ * 4 = more than 2048 units. */
+int sbs_decode_select_async(const sbs_decode_batch* batch, int32_t* error_out, void* stream);
 
 const char* sbs_last_error(void);
 const char* sbs_version(void);

@@ -190,7 +190,8 @@ EXPORTED_SYMBOLS = [
     "sbs_generate_workload", "sbs_sim_create", "sbs_sim_upload_traces", "sbs_sim_launch",
     "sbs_sim_results", "sbs_sim_requests", "sbs_sim_log", "sbs_sim_launches_per_run",
     "sbs_sim_device_bytes",
-    "sbs_sim_destroy", "sbs_run_experiments", "sbs_prefill_allocate", "sbs_decode_select",
+    "sbs_sim_destroy", "sbs_run_experiments", "sbs_prefill_allocate",
+    "sbs_prefill_allocate_async", "sbs_decode_select", "sbs_decode_select_async",
     "sbs_last_error", "sbs_version",
 ]
 

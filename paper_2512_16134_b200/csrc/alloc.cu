@@ -222,8 +222,14 @@ __global__ void __launch_bounds__(32 * kAllocWarps) iqr_kernel(IqrArgs A) {
 
 cudaError_t launch_pbaa(const PbaaArgs& a, cudaStream_t st) {
   const int smem = kAllocWarps * (kAllocMaxReq * 20 + kAllocMaxDp * 8);
-  cudaError_t e = cudaFuncSetAttribute(pbaa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
+  static thread_local int configured = -1;  // attribute set once per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured != dev) {
+    cudaError_t e = cudaFuncSetAttribute(pbaa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = dev;
+  }
   int blocks = (a.n_windows + kAllocWarps - 1) / kAllocWarps;
   if (blocks == 0) return cudaSuccess;
   pbaa_kernel<<<blocks, 32 * kAllocWarps, smem, st>>>(a);
@@ -232,8 +238,14 @@ cudaError_t launch_pbaa(const PbaaArgs& a, cudaStream_t st) {
 
 cudaError_t launch_iqr(const IqrArgs& a, cudaStream_t st) {
   const int smem = kAllocWarps * kIqrMaxUnits * 8;
-  cudaError_t e = cudaFuncSetAttribute(iqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
+  static thread_local int configured = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (configured != dev) {
+    cudaError_t e = cudaFuncSetAttribute(iqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = dev;
+  }
   int blocks = (a.n_calls + kAllocWarps - 1) / kAllocWarps;
   if (blocks == 0) return cudaSuccess;
   iqr_kernel<<<blocks, 32 * kAllocWarps, smem, st>>>(a);

@@ -681,6 +681,26 @@ int parallel_threads() {
   return (int)std::max(1u, hc);
 }
 
+// Per-thread, per-device error flag for the allocation kernels (allocated
+// once: a per-call cudaMallocAsync costs milliseconds once the pool trims).
+struct Scratch {
+  int device = -1;
+  int32_t* d_err = nullptr;
+  int32_t* h_err = nullptr;
+};
+Scratch& scratch() {
+  thread_local Scratch sc[16];
+  int dev = 0;
+  CUDA_OR_THROW(cudaGetDevice(&dev));
+  Scratch& s = sc[dev & 15];
+  if (s.d_err == nullptr) {
+    CUDA_OR_THROW(cudaMalloc(&s.d_err, sizeof(int32_t)));
+    CUDA_OR_THROW(cudaMallocHost(&s.h_err, sizeof(int32_t)));
+    s.device = dev;
+  }
+  return s;
+}
+
 }  // namespace
 
 extern "C" {
@@ -956,38 +976,51 @@ int sbs_run_experiments(const sbs_experiment* points, int32_t n_points, sbs_aggr
 
 int sbs_prefill_allocate(const sbs_window_batch* b, void* stream) {
   return guarded([&] {
-    int32_t* d_err = nullptr;
     cudaStream_t st = (cudaStream_t)stream;
-    CUDA_OR_THROW(cudaMallocAsync(&d_err, sizeof(int32_t), st));
-    CUDA_OR_THROW(cudaMemsetAsync(d_err, 0, sizeof(int32_t), st));
+    Scratch& sc = scratch();
+    CUDA_OR_THROW(cudaMemsetAsync(sc.d_err, 0, sizeof(int32_t), st));
     sbs::PbaaArgs a{b->n_windows, b->req_off, b->n_pending, b->dp_off, b->n_limit, b->req_id,
                     b->prompt_len, b->wait_in, b->caps, b->out_dp, b->out_rank, b->wait_out,
-                    b->flow, d_err};
+                    b->flow, sc.d_err};
     CUDA_OR_THROW(sbs::launch_pbaa(a, st));
-    int32_t h_err = 0;
-    CUDA_OR_THROW(cudaMemcpyAsync(&h_err, d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CUDA_OR_THROW(cudaFreeAsync(d_err, st));
+    CUDA_OR_THROW(cudaMemcpyAsync(sc.h_err, sc.d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CUDA_OR_THROW(cudaStreamSynchronize(st));
-    if (h_err) throw Error{h_err, "window exceeds the kernel's shared-memory envelope"};
+    if (*sc.h_err) throw Error{*sc.h_err, "window exceeds the kernel's shared-memory envelope"};
     return SBS_OK;
   });
 }
 
 int sbs_decode_select(const sbs_decode_batch* b, void* stream) {
   return guarded([&] {
-    int32_t* d_err = nullptr;
     cudaStream_t st = (cudaStream_t)stream;
-    CUDA_OR_THROW(cudaMallocAsync(&d_err, sizeof(int32_t), st));
-    CUDA_OR_THROW(cudaMemsetAsync(d_err, 0, sizeof(int32_t), st));
+    Scratch& sc = scratch();
+    CUDA_OR_THROW(cudaMemsetAsync(sc.d_err, 0, sizeof(int32_t), st));
     sbs::IqrArgs a{b->n_calls, b->unit_off, b->batch, b->kv, b->k, b->pos_out,
-                   b->fallback_out, b->threshold_out, d_err};
+                   b->fallback_out, b->threshold_out, sc.d_err};
     CUDA_OR_THROW(sbs::launch_iqr(a, st));
-    int32_t h_err = 0;
-    CUDA_OR_THROW(cudaMemcpyAsync(&h_err, d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-    CUDA_OR_THROW(cudaFreeAsync(d_err, st));
+    CUDA_OR_THROW(cudaMemcpyAsync(sc.h_err, sc.d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CUDA_OR_THROW(cudaStreamSynchronize(st));
-    if (h_err == 3) throw Error{SBS_ERR_INVARIANT, "select_decode_unit: no units"};
-    if (h_err) throw Error{h_err, "decode call exceeds the kernel's shared-memory envelope"};
+    if (*sc.h_err == 3) throw Error{SBS_ERR_INVARIANT, "select_decode_unit: no units"};
+    if (*sc.h_err) throw Error{*sc.h_err, "decode call exceeds the kernel's shared-memory envelope"};
+    return SBS_OK;
+  });
+}
+
+int sbs_prefill_allocate_async(const sbs_window_batch* b, int32_t* error_out, void* stream) {
+  return guarded([&] {
+    sbs::PbaaArgs a{b->n_windows, b->req_off, b->n_pending, b->dp_off, b->n_limit, b->req_id,
+                    b->prompt_len, b->wait_in, b->caps, b->out_dp, b->out_rank, b->wait_out,
+                    b->flow, error_out};
+    CUDA_OR_THROW(sbs::launch_pbaa(a, (cudaStream_t)stream));
+    return SBS_OK;
+  });
+}
+
+int sbs_decode_select_async(const sbs_decode_batch* b, int32_t* error_out, void* stream) {
+  return guarded([&] {
+    sbs::IqrArgs a{b->n_calls, b->unit_off, b->batch, b->kv, b->k, b->pos_out,
+                   b->fallback_out, b->threshold_out, error_out};
+    CUDA_OR_THROW(sbs::launch_iqr(a, (cudaStream_t)stream));
     return SBS_OK;
   });
 }

@@ -1,0 +1,283 @@
+// Drop-in replacement for the reference's prefill_alloc.cpp and decode_alloc.cpp
+// (proj/src), built against the reference's own headers (proj/include/sbsim).
+// Link this translation unit *instead of* those two files and every caller —
+// Runner::perform_dispatch (simulation.cpp:287-289), Runner::
+// drain_decode_admissions (:459-460), the acceptance audits — runs the
+// allocation on the B200 through the C-ABI (include/sbs_b200.h):
+//   allocate_batch / greedy_dispatch -> sbs_prefill_allocate (PBAA kernel)
+//   select_decode_unit / schedule_decode_batch -> sbs_decode_select (IQR kernel)
+// percentile / outlier_threshold / lex_less are the scalar helpers the
+// reference's metrics also use (metrics.cpp:151-152); they stay host math.
+//
+// Cache-aware PBAA (AllocMode::kCacheAware) is outside the GPU path's scope
+// and raises ConfigError, as any unsupported configuration does.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "sbs_b200.h"
+#include "sbsim/decode_alloc.h"
+#include "sbsim/prefill_alloc.h"
+
+namespace {
+
+// Per-thread device staging: one pinned host block and one device block,
+// grown on demand, one stream.  Each call is a single H2D copy, one kernel and
+// a single D2H copy.
+struct Staging {
+  cudaStream_t stream = nullptr;
+  unsigned char* host = nullptr;
+  unsigned char* dev = nullptr;
+  size_t cap = 0;
+
+  void ensure(size_t bytes) {
+    if (stream == nullptr) check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    if (bytes <= cap) return;
+    size_t n = std::max(bytes, cap * 2);
+    if (host) cudaFreeHost(host);
+    if (dev) cudaFree(dev);
+    check(cudaMallocHost(&host, n));
+    check(cudaMalloc(&dev, n));
+    cap = n;
+  }
+  static void check(cudaError_t e) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string("sbs_b200 shim: ") + cudaGetErrorString(e));
+  }
+  ~Staging() {
+    if (host) cudaFreeHost(host);
+    if (dev) cudaFree(dev);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+thread_local Staging g_st;
+
+size_t align8(size_t v) { return (v + 7) & ~size_t(7); }
+
+void throw_rc(int rc) {
+  if (rc == SBS_OK) return;
+  if (rc == SBS_ERR_CONFIG) throw sbsim::ConfigError(sbs_last_error());
+  if (rc == SBS_ERR_INVARIANT) throw std::logic_error(sbs_last_error());
+  throw std::runtime_error(std::string("sbs_b200: ") + sbs_last_error());
+}
+
+struct WindowOut {
+  std::vector<int32_t> dp, rank, wait;
+  std::vector<int64_t> caps;
+  bool flow = false;
+};
+
+// One cluster-window through the batched PBAA kernel.
+WindowOut run_window(std::span<sbsim::Request* const> pending,
+                     std::span<sbsim::Request* const> fresh,
+                     const std::vector<sbsim::DpPlan>& dps, int n_limit) {
+  const size_t n = pending.size() + fresh.size(), D = dps.size();
+  // layout in the staging block
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = align8(off + bytes); return o; };
+  const size_t o_roff = take(16), o_np = take(4), o_doff = take(16), o_nl = take(4),
+               o_id = take(8 * n), o_len = take(8 * n), o_win = take(4 * n), o_caps = take(8 * D),
+               o_dp = take(4 * n), o_rank = take(4 * n), o_wout = take(4 * n),
+               o_flow = take(8), o_err = take(8);
+  g_st.ensure(off + 64);
+  unsigned char* h = g_st.host;
+  int64_t roff[2] = {0, (int64_t)n}, doff[2] = {0, (int64_t)D};
+  int32_t np = (int32_t)pending.size(), nl = n_limit;
+  std::memcpy(h + o_roff, roff, 16);
+  std::memcpy(h + o_np, &np, 4);
+  std::memcpy(h + o_doff, doff, 16);
+  std::memcpy(h + o_nl, &nl, 4);
+  size_t i = 0;
+  for (auto* q : {&pending, &fresh})
+    for (sbsim::Request* r : *q) {
+      ((int64_t*)(h + o_id))[i] = (int64_t)r->id;
+      ((int64_t*)(h + o_len))[i] = r->prompt_len;
+      ((int32_t*)(h + o_win))[i] = r->wait_cycles;
+      ++i;
+    }
+  for (size_t d = 0; d < D; ++d) ((int64_t*)(h + o_caps))[d] = dps[d].c_avail;
+  *(int32_t*)(h + o_err) = 0;
+  unsigned char* g = g_st.dev;
+  // one H2D of the whole block (inputs + zeroed error word), one kernel, one D2H
+  Staging::check(cudaMemcpyAsync(g, h, off, cudaMemcpyHostToDevice, g_st.stream));
+  sbs_window_batch b{};
+  b.n_windows = 1;
+  b.req_off = (const int64_t*)(g + o_roff);
+  b.n_pending = (const int32_t*)(g + o_np);
+  b.dp_off = (const int64_t*)(g + o_doff);
+  b.n_limit = (const int32_t*)(g + o_nl);
+  b.req_id = (const int64_t*)(g + o_id);
+  b.prompt_len = (const int64_t*)(g + o_len);
+  b.wait_in = (const int32_t*)(g + o_win);
+  b.caps = (int64_t*)(g + o_caps);
+  b.out_dp = (int32_t*)(g + o_dp);
+  b.out_rank = (int32_t*)(g + o_rank);
+  b.wait_out = (int32_t*)(g + o_wout);
+  b.flow = (uint8_t*)(g + o_flow);
+  throw_rc(sbs_prefill_allocate_async(&b, (int32_t*)(g + o_err), g_st.stream));
+  Staging::check(cudaMemcpyAsync(h + o_caps, g + o_caps, off - o_caps, cudaMemcpyDeviceToHost,
+                                 g_st.stream));
+  Staging::check(cudaStreamSynchronize(g_st.stream));
+  if (*(int32_t*)(h + o_err)) throw_rc(SBS_ERR_OVERFLOW);
+  WindowOut w;
+  w.dp.assign((int32_t*)(h + o_dp), (int32_t*)(h + o_dp) + n);
+  w.rank.assign((int32_t*)(h + o_rank), (int32_t*)(h + o_rank) + n);
+  w.wait.assign((int32_t*)(h + o_wout), (int32_t*)(h + o_wout) + n);
+  w.caps.assign((int64_t*)(h + o_caps), (int64_t*)(h + o_caps) + D);
+  w.flow = h[o_flow] != 0;
+  return w;
+}
+
+}  // namespace
+
+namespace sbsim {
+
+Tokens cache_hit_len(const Request& req, const DpPlan& dp) {
+  if (dp.cache == nullptr) return 0;
+  return dp.cache->longest_hit(req.prefix_tokens, req.prompt_len);
+}
+
+Tokens capacity_after(const Request& req, const DpPlan& dp, AllocMode mode) {
+  Tokens charge = req.prompt_len;
+  if (mode == AllocMode::kCacheAware) charge -= cache_hit_len(req, dp);
+  return dp.c_avail - charge;
+}
+
+void greedy_dispatch(std::span<Request* const> queue, std::vector<DpPlan>& dps, AllocMode mode,
+                     std::vector<Placement>& mapping, std::vector<Request*>& deferred) {
+  if (mode == AllocMode::kCacheAware)
+    throw ConfigError("cache-aware allocation is out of scope of the B200 path");
+  // one phase == a window whose whole queue is "pending", never throttled
+  WindowOut w = run_window(queue, {}, dps, std::numeric_limits<int>::max());
+  std::vector<std::pair<int32_t, size_t>> placed;
+  for (size_t i = 0; i < queue.size(); ++i) {
+    if (w.dp[i] >= 0) placed.emplace_back(w.rank[i], i);
+    else deferred.push_back(queue[i]);
+  }
+  std::sort(placed.begin(), placed.end());
+  for (auto& [rk, i] : placed) mapping.emplace_back(queue[i], dps[(size_t)w.dp[i]].dp_index);
+  for (size_t d = 0; d < dps.size(); ++d) dps[d].c_avail = w.caps[d];
+}
+
+AllocationResult allocate_batch(std::span<Request* const> q_pending,
+                                std::span<Request* const> q_new, std::vector<DpPlan>& dps,
+                                int n_limit, AllocMode mode) {
+  if (mode == AllocMode::kCacheAware)
+    throw ConfigError("cache-aware allocation is out of scope of the B200 path");
+  AllocationResult res;
+  WindowOut w = run_window(q_pending, q_new, dps, n_limit);
+  const size_t n = q_pending.size() + q_new.size();
+  auto req = [&](size_t i) { return i < q_pending.size() ? q_pending[i] : q_new[i - q_pending.size()]; };
+  std::vector<std::pair<int32_t, size_t>> placed;
+  for (size_t i = 0; i < n; ++i) {
+    Request* r = req(i);
+    if (w.dp[i] >= 0) {
+      placed.emplace_back(w.rank[i], i);
+    } else {
+      r->wait_cycles = w.wait[i];
+      (w.dp[i] == -2 ? res.throttled : res.deferred).push_back(r);
+    }
+  }
+  std::sort(placed.begin(), placed.end());
+  for (auto& [rk, i] : placed) res.mapping.emplace_back(req(i), dps[(size_t)w.dp[i]].dp_index);
+  for (size_t d = 0; d < dps.size(); ++d) dps[d].c_avail = w.caps[d];
+  res.flow_control = w.flow;
+  return res;
+}
+
+double percentile(std::vector<double> values, double p) {
+  if (values.empty()) throw std::logic_error("percentile: empty input");
+  p = std::clamp(p, 0.0, 100.0);
+  std::sort(values.begin(), values.end());
+  double rank = (static_cast<double>(values.size()) - 1.0) * p / 100.0;
+  auto lo = static_cast<std::size_t>(std::floor(rank));
+  auto hi = static_cast<std::size_t>(std::ceil(rank));
+  if (lo == hi) return values[lo];
+  return values[lo] + (rank - static_cast<double>(lo)) * (values[hi] - values[lo]);
+}
+
+double outlier_threshold(std::span<const Tokens> kv_loads, double k) {
+  std::vector<double> v(kv_loads.begin(), kv_loads.end());
+  double q1 = percentile(v, 25.0);
+  double q3 = percentile(std::move(v), 75.0);
+  return q3 + k * (q3 - q1);
+}
+
+bool lex_less(const std::pair<int, Tokens>& a, const std::pair<int, Tokens>& b) {
+  return a.first != b.first ? a.first < b.first : a.second < b.second;
+}
+
+int select_decode_unit(const std::vector<DecodeUnitPlan>& units, double k,
+                       std::uint64_t request_id, const DecodeObserver& observe) {
+  if (units.empty()) throw std::logic_error("select_decode_unit: no units");
+  const size_t U = units.size();
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = align8(off + bytes); return o; };
+  const size_t o_off = take(16), o_b = take(4 * U), o_k = take(8 * U), o_err = take(8),
+               o_pos = take(4), o_fb = take(8), o_th = take(8);
+  g_st.ensure(off + 64);
+  unsigned char* h = g_st.host;
+  int64_t uo[2] = {0, (int64_t)U};
+  std::memcpy(h + o_off, uo, 16);
+  for (size_t i = 0; i < U; ++i) {
+    ((int32_t*)(h + o_b))[i] = units[i].batch;
+    ((int64_t*)(h + o_k))[i] = units[i].kv;
+  }
+  *(int32_t*)(h + o_err) = 0;
+  unsigned char* g = g_st.dev;
+  Staging::check(cudaMemcpyAsync(g, h, o_pos, cudaMemcpyHostToDevice, g_st.stream));
+  sbs_decode_batch b{};
+  b.n_calls = 1;
+  b.unit_off = (const int64_t*)(g + o_off);
+  b.batch = (const int32_t*)(g + o_b);
+  b.kv = (const int64_t*)(g + o_k);
+  b.k = k;
+  b.pos_out = (int32_t*)(g + o_pos);
+  b.fallback_out = (uint8_t*)(g + o_fb);
+  b.threshold_out = (double*)(g + o_th);
+  throw_rc(sbs_decode_select_async(&b, (int32_t*)(g + o_err), g_st.stream));
+  Staging::check(cudaMemcpyAsync(h + o_err, g + o_err, off - o_err, cudaMemcpyDeviceToHost,
+                                 g_st.stream));
+  Staging::check(cudaStreamSynchronize(g_st.stream));
+  if (int e = *(int32_t*)(h + o_err)) throw_rc(e == 3 ? SBS_ERR_INVARIANT : SBS_ERR_OVERFLOW);
+  int pos = *(int32_t*)(h + o_pos);
+  if (observe) {
+    DecodePlacementInfo info;
+    info.request_id = request_id;
+    info.threshold = *(double*)(h + o_th);
+    info.fallback = h[o_fb] != 0;
+    for (size_t i = 0; i < U; ++i) {
+      info.kv_snapshot.push_back(units[i].kv);
+      if (info.fallback || static_cast<double>(units[i].kv) <= info.threshold)
+        info.safe.push_back((int)i);
+    }
+    info.selected = pos;
+    observe(info);
+  }
+  return pos;
+}
+
+std::vector<std::pair<std::uint64_t, int>> schedule_decode_batch(
+    std::vector<DecodeCandidate> candidates, std::vector<DecodeUnitPlan>& units, double k,
+    const DecodeObserver& observe) {
+  std::stable_sort(candidates.begin(), candidates.end(),
+                   [](const DecodeCandidate& a, const DecodeCandidate& b) {
+                     return a.sort_len != b.sort_len ? a.sort_len > b.sort_len
+                                                     : a.request_id < b.request_id;
+                   });
+  std::vector<std::pair<std::uint64_t, int>> out;
+  for (const auto& c : candidates) {
+    int pos = select_decode_unit(units, k, c.request_id, observe);
+    units[(size_t)pos].batch += 1;
+    units[(size_t)pos].kv += c.kv_len;
+    out.emplace_back(c.request_id, units[(size_t)pos].unit_index);
+  }
+  return out;
+}
+
+}  // namespace sbsim
