@@ -148,7 +148,7 @@ __device__ __forceinline__ uint64_t mt_temper(uint64_t y) {
 // ---------------------------------------------------------------------------
 constexpr uint64_t kBOne = 1ull << 48;       // packed decode unit: B << 48 | K
 constexpr uint64_t kKMask = kBOne - 1;
-constexpr int kErrEnvelope = 6;               // B >= 2^15 or K >= 2^48 on a decode unit
+constexpr int kErrEnvelope = 6;               // B >= 2^15 or K >= 2^32 on a decode unit
 
 // Per-replica counters and FP sums (metrics.h:107-152 state), in shared memory
 // and written by lane 0 only: they are rarely read, so they should not occupy
@@ -581,7 +581,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       const uint64_t k0 = s_PK[u];
       const uint64_t K0 = k0 & kKMask, B0 = k0 >> 48;
       const uint64_t K1 = K0 + (uint64_t)prompt;
-      if (B0 + 1 >= (1u << 15) || K1 >= kBOne) { error = kErrEnvelope; return; }
+      if (B0 + 1 >= (1u << 15) || K1 >= (1ull << 32)) { error = kErrEnvelope; return; }
       const bool stepping = d_flag(j, G_STEP);
       __syncwarp();
       if (lane == 0) {
@@ -1006,7 +1006,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     // every stamped resident produced tps tokens (minus the last-step excess
     // of completers); completers release B and prompt + decode_done of K
     const bool gather = ul_ident && Dn == 1;  // s_S order == unit order
-    uint64_t mx = 0;
+    uint64_t mx = 0, s1 = 0, s2lo = 0, s2hi = 0;  // sum K, sum K^2 (128-bit)
     double worst = 0.0;
     for (int d = lane; d < Dd; d += 32) {
       const int u = u0 + d;
@@ -1020,11 +1020,26 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       if (r) s_R[u] = 0;
       if (gather) s_S[u] = K;
       mx = K > mx ? K : mx;
+      s1 += K;
+      const uint64_t k2 = K * K;  // K < 2^32 (decode-unit envelope)
+      s2lo += k2;
+      s2hi += s2lo < k2;
       double t = __dadd_rn(__dmul_rn(dc_req, (double)B), __dmul_rn(dc_kv, (double)K));
       worst = t > worst ? t : worst;
     }
     exc = warp_sum_i64(exc);
     rel = warp_sum_i64(rel);
+    const bool band_fast = !LOG && Dn == 1 && now >= warmup;
+    if (band_fast) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        s1 += __shfl_xor_sync(kFull, s1, o);
+        const uint64_t lo = __shfl_xor_sync(kFull, s2lo, o);
+        const uint64_t hi = __shfl_xor_sync(kFull, s2hi, o);
+        s2lo += lo;
+        s2hi += hi + (s2lo < lo);
+      }
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       double w = __shfl_xor_sync(kFull, worst, o);
@@ -1050,7 +1065,23 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       CNT(outtok, gen);
     }
     if (g_log) log_rec(LOG_STEP, 2, now, gen, 0, 0, 0);  // record_step (simulation.cpp:507)
-    if (now >= warmup || g_log) {
+    if (band_fast) {
+      // single decode instance: the band comes from the step loop's exact sums
+      // mean = sum/n (bit-identical); sum (v-mean)^2 = (n*sum v^2 - (sum v)^2)/n
+      if (d_flag(0, G_HEALTHY) && !d_flag(0, G_DEAD) && lane == 0) {
+        typedef unsigned __int128 u128;
+        const double n_d = (double)Dd;
+        const u128 sq = ((u128)s2hi << 64) | s2lo;
+        const u128 x = (u128)(uint64_t)Dd * sq - (u128)s1 * (u128)s1;
+        const double xd = __dadd_rn(__dmul_rn((double)(uint64_t)(x >> 64), 18446744073709551616.0),
+                                    (double)(uint64_t)x);
+        const double mean = __ddiv_rn((double)s1, n_d);
+        const double sigma = sqrt(__ddiv_rn(__ddiv_rn(xd, n_d), n_d));
+        cn->kv_mean = __dadd_rn(cn->kv_mean, mean);
+        cn->kv_sig = __dadd_rn(cn->kv_sig, sigma);
+        cn->kv_n += 1;
+      }
+    } else if (now >= warmup || g_log) {
       // kv_band (metrics.cpp:50-72) over every healthy, live decode unit:
       // the mean from the exact integer sum (bit-identical to the reference,
       // whose partial sums are exact integers), then the reference's second
