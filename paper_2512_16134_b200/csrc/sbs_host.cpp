@@ -18,6 +18,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -578,7 +579,11 @@ void upload_points(sbs_sim& s) {
                            cudaMemcpyHostToDevice));
   // occupancy: warps per block 4 unless shared memory forces fewer
   const int max_smem_block = 227 * 1024;
-  int wpb = 4;
+  // spread replicas over every SM first: warps of one SM share its issue
+  // slots, L1.5 instruction cache and shared-memory pipe (4 per SM at most)
+  const int n_rep = (int)s.order.size();
+  int wpb = std::max(1, std::min(4, (n_rep + s.sm_count - 1) / std::max(1, s.sm_count)));
+  if (const char* e = std::getenv("SBS_WARPS_PER_BLOCK")) wpb = std::max(1, std::min(4, std::atoi(e)));
   while (wpb > 1 && wpb * s.smem_per_warp > max_smem_block) wpb >>= 1;
   if (s.smem_per_warp > max_smem_block)
     throw Error{SBS_ERR_CONFIG, "replica state exceeds shared memory"};
