@@ -19,7 +19,7 @@ from pathlib import Path
 import numpy as np
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "lib" / "libsbs_b200.so"
+LIB_PATH = Path(os.environ["SBS_LIB"]) if os.environ.get("SBS_LIB") else PKG / "lib" / "libsbs_b200.so"
 
 OK, ERR_CONFIG, ERR_INVARIANT, ERR_OVERFLOW, ERR_CUDA = 0, 1, 3, 4, 5
 
@@ -174,6 +174,7 @@ def lib():
         L.sbs_sim_log.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64,
                                   C.POINTER(C.c_int64)]
         L.sbs_sim_launches_per_run.argtypes = [C.c_void_p]
+        L.sbs_sim_profile_counters.argtypes = [C.c_void_p, C.c_void_p]
         L.sbs_sim_device_bytes.argtypes = [C.c_void_p]
         L.sbs_sim_device_bytes.restype = C.c_int64
         L.sbs_sim_destroy.argtypes = [C.c_void_p]
@@ -192,7 +193,7 @@ EXPORTED_SYMBOLS = [
     "sbs_sim_device_bytes",
     "sbs_sim_destroy", "sbs_run_experiments", "sbs_prefill_allocate",
     "sbs_prefill_allocate_async", "sbs_decode_select", "sbs_decode_select_async",
-    "sbs_last_error", "sbs_version",
+    "sbs_last_error", "sbs_version", "sbs_sim_profile_counters",
 ]
 
 
@@ -464,6 +465,11 @@ class Simulator:
         buf = np.empty(max(n.value, 1), np.int64)
         _check(lib().sbs_sim_log(self.handle, point, buf.ctypes.data, len(buf), C.byref(n)))
         return buf[: n.value]
+
+    def profile_counters(self):
+        out = (C.c_int64 * 16)()
+        lib().sbs_sim_profile_counters(self.handle, out)
+        return list(out)
 
     @property
     def launches_per_run(self):

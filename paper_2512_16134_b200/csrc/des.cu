@@ -161,6 +161,16 @@ struct Counters {
 
 // KD: prefill DP units per lane, 1 (dp_degree <= 32) or 4 (<= 128).
 // LOG: keep run records (compiled out of the sweep kernel).
+// Development instrumentation: -DSBS_PROF accumulates clock64() cycles per
+// region (inclusive) into DevResult::prof.  Compiled out by default.
+#ifdef SBS_PROF
+#define PROF_BEGIN(r) const long long _pt##r = clock64()
+#define PROF_END(r) prof_acc[r] += clock64() - _pt##r
+#else
+#define PROF_BEGIN(r)
+#define PROF_END(r)
+#endif
+
 template <int KD, bool LOG>
 __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* sm) {
   const int lane = lane_id();
@@ -179,6 +189,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   const int n_topo = pt.n_topo, w_size = pt.w_size, QD = pt.QD, QP = pt.QP, QW = pt.QW;
   const bool per_req = pt.per_request != 0;
   const int64_t tps = pt.tps, t_default = pt.t_default;
+  const double inv_dd = 1.0 / (double)(pt.Dd > 0 ? pt.Dd : 1);
   const double pf_base = pt.pf_base, pf_tok = pt.pf_tok, dc_base = pt.dc_base, dc_req = pt.dc_req,
                dc_kv = pt.dc_kv, iqr_k = pt.iqr_k, wd_mult = pt.wd_mult;
   const int64_t* __restrict__ g_arr = pt.arr;
@@ -283,7 +294,11 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   int o_k = 0, o_i = 0;
 
   // ---- counters (shared memory, lane 0) + lane-local TPOT partials
-  int64_t n_ttft = 0, tpot_n = 0, tpot_sum = 0;
+  int64_t n_ttft = 0, tpot_n = 0;
+  double tpot_sum = 0.0;
+#ifdef SBS_PROF
+  long long prof_acc[16] = {0};
+#endif
 #define CNT(f, v) do { if (lane == 0) cn->f += (v); } while (0)
   // append one fixed-size record (lane 0); overflow is reported, never silent
   auto log_rec = [&](int kind, int nw, int64_t a, int64_t b, int64_t c, int64_t d, int64_t e) {
@@ -365,29 +380,28 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   // ---- completion accounting (metrics.cpp:117-153), called by the lanes
   //      holding a completed request; all lanes must call (ballots inside).
   int64_t l_cw = 0, l_wr = 0, l_ttft = 0, l_sched = 0, l_dev = 0, l_done = 0;
-  auto complete_lanes = [&](bool has, int64_t id, int64_t ftok, bool decode) {
+  // All per-request inputs are passed in: the callers issue every global
+  // load of a completer at once (one memory round trip, not a chain).
+  auto complete_lanes = [&](bool has, int64_t id, int64_t ftok, bool decode, int64_t arr,
+                            int32_t out, int64_t disp, int64_t ps) {
     int64_t ttft = 0;
     bool inwin = false;
     if (has) {
       l_done += 1;
       if (now >= warmup) l_cw += 1;
-      int64_t arr = __ldg(g_arr + id);
       if (per_req) {
         o_comp[id] = now;
         o_status[id] = kStCompleted;
       }
       if (decode) {
-        // TPOT (not in the reference): integer ns per output token after the first
-        int32_t out = __ldg(g_output + id);
-        int64_t per = (now - ftok) / (int64_t)(out - 1);
-        tpot_sum += per;
+        // TPOT (not in the reference): ns per output token after the first
+        const double per = __dmul_rn((double)(now - ftok), __drcp_rn((double)(out - 1)));
+        tpot_sum = __dadd_rn(tpot_sum, per);
         tpot_n += 1;
-        atomicAdd((unsigned long long*)&g_tpot_hist[hist_bin(per)], 1ull);
+        atomicAdd((unsigned long long*)&g_tpot_hist[hist_bin((int64_t)per)], 1ull);
       }
       if (arr >= warmup) {
         inwin = true;
-        int64_t disp = o_dispatch[id];
-        int64_t ps = o_pstart[id];
         ttft = ftok - arr;
         l_wr += 1;
         l_ttft += ttft;
@@ -469,7 +483,10 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
 
   // IQR select over the unit list (decode_alloc.cpp:38-81); returns position.
   auto iqr_select = [&]() -> int {
+    PROF_BEGIN(7);
     if (!S_valid) rebuild_S();
+    PROF_END(7);
+    PROF_BEGIN(5);
     if (pc_n != nul) {
       const double r25 = __ddiv_rn(__dmul_rn((double)nul - 1.0, 25.0), 100.0);
       const double r75 = __ddiv_rn(__dmul_rn((double)nul - 1.0, 75.0), 100.0);
@@ -511,7 +528,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     uint64_t key = fallback ? ba : bs;
     int pos = fallback ? pa : ps;
     uint64_t m = warp_min_u64(key);
-    return (int)__reduce_min_sync(kFull, key == m ? (uint32_t)pos : 0x7fffffffu);
+    const int sel = (int)__reduce_min_sync(kFull, key == m ? (uint32_t)pos : 0x7fffffffu);
+    PROF_END(5);
+    return sel;
   };
 
   // S multiset: replace one copy of `oldv` by `newv` (> oldv).
@@ -595,7 +614,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         d_worst = t > d_worst ? t : d_worst;
       }
       __syncwarp();
+      PROF_BEGIN(6);
       if (S_valid) S_update(K0, K1);
+      PROF_END(6);
       if (cap_batch > 0 && (int64_t)B0 + 1 >= cap_batch) ul_dirty = true;
       // completion ring: finishes at step d_step + ceil(target/tps)
       const int64_t target = (int64_t)out - 1;
@@ -735,17 +756,20 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       }
       bool has = d < D;
       if (!__any_sync(kFull, has)) break;
-      int64_t id = 0;
+      int64_t id = 0, arr = 0, disp = 0, ps = 0;
       int32_t out = 0;
       if (has) {
         id = g_fifo[(int64_t)(g0 + d) * F + (idx & Fm)].x;
         idx += 1;
         out = __ldg(g_output + id);
+        arr = __ldg(g_arr + id);
+        disp = o_dispatch[id];
+        ps = o_pstart[id];
         o_ftok[id] = now;
       }
       bool done = has && out <= 1;   // decode_target() == 0
       bool wait = has && out > 1;
-      complete_lanes(done, id, now, false);
+      complete_lanes(done, id, now, false, arr, out, disp, ps);
       unsigned m = __ballot_sync(kFull, wait);
       if (wait) {
         int32_t prompt = __ldg(g_prompt + id);
@@ -987,22 +1011,30 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     const int n = s_bcnt[b];
     const int4* ent = g_buckets + (int64_t)b * BC;
     int64_t exc = 0, rel = 0;
+    PROF_BEGIN(11);
     for (int base = 0; base < n; base += 32) {
       int e = base + lane;
       bool has = e < n;
-      int64_t id = 0, ft = 0;
+      int64_t id = 0, ft = 0, arr = 0, disp = 0, ps = 0;
+      int32_t out = 0;
       if (has) {
-        int4 v = ent[e];
+        const int4 v = ent[e];
         id = v.x;
+        ft = o_ftok[id];  // every load of the completer issued before any use
+        arr = __ldg(g_arr + id);
+        out = __ldg(g_output + id);
+        disp = o_dispatch[id];
+        ps = o_pstart[id];
         atomicAdd((unsigned long long*)&s_R[v.y], (unsigned long long)(kBOne | (uint64_t)(uint32_t)v.z));
         exc += v.w;
         rel += (uint32_t)v.z;
-        ft = o_ftok[id];
       }
-      complete_lanes(has, id, ft, true);
+      complete_lanes(has, id, ft, true, arr, out, disp, ps);
     }
     __syncwarp();
     if (lane == 0) s_bcnt[b] = 0;
+    PROF_END(11);
+    PROF_BEGIN(12);
     // every stamped resident produced tps tokens (minus the last-step excess
     // of completers); completers release B and prompt + decode_done of K
     const bool gather = ul_ident && Dn == 1;  // s_S order == unit order
@@ -1027,23 +1059,24 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       double t = __dadd_rn(__dmul_rn(dc_req, (double)B), __dmul_rn(dc_kv, (double)K));
       worst = t > worst ? t : worst;
     }
-    exc = warp_sum_i64(exc);
-    rel = warp_sum_i64(rel);
+    PROF_END(12);
+    PROF_BEGIN(13);
+    (void)rel;
     const bool band_fast = !LOG && Dn == 1 && now >= warmup;
-    if (band_fast) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        s1 += __shfl_xor_sync(kFull, s1, o);
-        const uint64_t lo = __shfl_xor_sync(kFull, s2lo, o);
-        const uint64_t hi = __shfl_xor_sync(kFull, s2hi, o);
-        s2lo += lo;
-        s2hi += hi + (s2lo < lo);
-      }
-    }
+    // one interleaved butterfly for every per-step reduction (their shuffle
+    // latencies overlap instead of chaining)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      double w = __shfl_xor_sync(kFull, worst, o);
+      const double w = __shfl_xor_sync(kFull, worst, o);
+      const int64_t ex = __shfl_xor_sync(kFull, exc, o);
+      const uint64_t a1 = __shfl_xor_sync(kFull, s1, o);
+      const uint64_t lo = __shfl_xor_sync(kFull, s2lo, o);
+      const uint64_t hi = __shfl_xor_sync(kFull, s2hi, o);
       worst = w > worst ? w : worst;
+      exc += ex;
+      s1 += a1;
+      s2lo += lo;
+      s2hi += hi + (s2lo < lo);
     }
     const int64_t stamped = bcast(d_res_begin, j);
     const int64_t gen = tps * stamped - exc;
@@ -1065,6 +1098,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       CNT(outtok, gen);
     }
     if (g_log) log_rec(LOG_STEP, 2, now, gen, 0, 0, 0);  // record_step (simulation.cpp:507)
+    PROF_END(13);
+    PROF_BEGIN(14);
     if (band_fast) {
       // single decode instance: the band comes from the step loop's exact sums
       // mean = sum/n (bit-identical); sum (v-mean)^2 = (n*sum v^2 - (sum v)^2)/n
@@ -1075,8 +1110,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         const u128 x = (u128)(uint64_t)Dd * sq - (u128)s1 * (u128)s1;
         const double xd = __dadd_rn(__dmul_rn((double)(uint64_t)(x >> 64), 18446744073709551616.0),
                                     (double)(uint64_t)x);
-        const double mean = __ddiv_rn((double)s1, n_d);
-        const double sigma = sqrt(__ddiv_rn(__ddiv_rn(xd, n_d), n_d));
+        const double mean = __ddiv_rn((double)s1, n_d);  // == reference mean (exact sum)
+        const double sigma = __dmul_rn(sqrt(xd), inv_dd);  // sqrt(sum (v-mean)^2 / n), ~1e-16
         cn->kv_mean = __dadd_rn(cn->kv_mean, mean);
         cn->kv_sig = __dadd_rn(cn->kv_sig, sigma);
         cn->kv_n += 1;
@@ -1135,6 +1170,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         }
       }
     }
+    PROF_END(14);
   };
 
   // drop_matches (simulation.cpp:128-134)
@@ -1157,6 +1193,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   int64_t topo_t = (n_topo > 0) ? pt.topo_time[0] : kInf64;
   if (g_log && sbs) log_rec(LOG_CONTROL, 4, 0, i_opt, t_bar, n_active, 0);  // simulation.cpp:152
   while (error == 0) {
+    PROF_BEGIN(0);
     if (odirty) recompute_other();
     // live internal minimum: tick vs other
     int64_t it = o_t;
@@ -1171,6 +1208,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     else { kind = ik; et = it; }
     if (et == kInf64 || et > horizon) break;
     now = et;
+    PROF_END(0);
     CNT(events, 1);
 
     int start_p = -1;      // try_start_pass before the dispatch stage
@@ -1205,7 +1243,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       maybe_die_p(p);
       if (p_flag(p, F_DEAD)) continue;
       measured = now - bcast(p_started, p);
+      PROF_BEGIN(2);
       finish_pass(p);
+      PROF_END(2);
       start_p = p;
       if (sbs) ef_p = p;
     } else if (kind == kEvWD) {
@@ -1227,7 +1267,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       odirty = true;
       maybe_die_d(j);
       if (d_flag(j, G_DEAD)) continue;
+      PROF_BEGIN(3);
       finish_step(j);
+      PROF_END(3);
       step_j = j;
     } else {
       // ---- on_topology (simulation.cpp:382-393)
@@ -1254,13 +1296,20 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
 
     // ---- decode hand-off: hand_off_finished / on_decode_step tail
     if (kind == kEvEF || kind == kEvDS) {
+      PROF_BEGIN(4);
       drain_decode();
+      PROF_END(4);
       if (error) break;
+      PROF_BEGIN(10);
       if (step_j >= 0) try_begin_step(step_j);
+      PROF_END(10);
     }
+    PROF_BEGIN(9);
     // ---- prefill passes and the SBS dispatch chain
     for (int stage = 0; stage < 2; ++stage) {
+      PROF_BEGIN(8);
       if (start_p >= 0) try_start_pass(start_p);
+      PROF_END(8);
       if (stage == 1) {
         if (start_p >= 0 && np > 0) arm_tick(now + i_opt);  // simulation.cpp:341
         break;
@@ -1302,10 +1351,11 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       if (start_p < 0) break;
       maybe_die_p(start_p);
     }
+    PROF_END(9);
   }
 
   // ---- results
-  tpot_sum = warp_sum_i64(tpot_sum);
+  tpot_sum = warp_sum_f64(tpot_sum);
   tpot_n = warp_sum_i64(tpot_n);
   l_done = warp_sum_i64(l_done);
   l_cw = warp_sum_i64(l_cw);
@@ -1339,11 +1389,14 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     res.util_sum = cn->util;
     res.kv_mean_sum = cn->kv_mean;
     res.kv_sigma_sum = cn->kv_sig;
-    res.tpot_sum = (double)tpot_sum / 1e9;
+    res.tpot_sum = tpot_sum / 1e9;
     res.kv_n = cn->kv_n;
     res.tpot_n = tpot_n;
     res.log_n = log_n;
     res.error = error;
+#ifdef SBS_PROF
+    for (int i = 0; i < 16; ++i) res.prof[i] = prof_acc[i];
+#endif
   }
 #undef CNT
   (void)kErrInvariant;

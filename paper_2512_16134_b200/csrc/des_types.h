@@ -101,6 +101,7 @@ struct DevResult {
   int64_t ttft_sel[4];  // order statistics at ranks lo50, hi50, lo95, hi95
   int64_t ttft_hist[kHistBins];
   int64_t log_n;        // words written (== log_cap + 1 on overflow)
+  int64_t prof[16];     // SBS_PROF builds only: clock64 cycles per region
   int32_t error;
   int32_t _pad;
 };

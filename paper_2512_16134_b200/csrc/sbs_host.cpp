@@ -907,6 +907,13 @@ int sbs_sim_log(sbs_sim* s, int32_t point, int64_t* words, int64_t cap, int64_t*
   });
 }
 
+int sbs_sim_profile_counters(const sbs_sim* s, int64_t* out16) {
+  for (int i = 0; i < 16; ++i) out16[i] = 0;
+  for (const auto& r : s->h_res)
+    for (int i = 0; i < 16; ++i) out16[i] += r.prof[i];
+  return SBS_OK;
+}
+
 void sbs_sim_destroy(sbs_sim* s) {
   if (s == nullptr) return;
   cudaSetDevice(s->device);
