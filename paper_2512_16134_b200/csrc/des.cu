@@ -217,8 +217,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   uint8_t* s_part = (uint8_t*)(sm + pt.sm_pf_part);
   uint64_t* s_PK = (uint64_t*)(sm + pt.sm_dPK);   // B << 48 | K per decode unit
   uint64_t* s_R = (uint64_t*)(sm + pt.sm_dR);     // completers this step: n << 48 | kv release
-  uint64_t* s_S = (uint64_t*)(sm + pt.sm_dS);     // sorted K multiset over the unit list
-  uint64_t* s_T = (uint64_t*)(sm + pt.sm_dT);     // radix-sort scratch
+  uint32_t* s_S = (uint32_t*)(sm + pt.sm_dS);     // sorted K multiset over the unit list (K < 2^32)
+  uint32_t* s_T = (uint32_t*)(sm + pt.sm_dT);     // radix-sort scratch
   int32_t* s_nst = (int32_t*)(sm + pt.sm_dnst);   // residents stamped at the next/current step
   int16_t* s_ul = (int16_t*)(sm + pt.sm_ulist);
   uint16_t* s_bcnt = (uint16_t*)(sm + pt.sm_bcnt);
@@ -444,13 +444,13 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       if (ul_ident) {
         for (int i = lane; i < nul; i += 32) {
           uint64_t k = s_PK[i] & kKMask;
-          s_S[i] = k;
+          s_S[i] = (uint32_t)k;
           mx = k > mx ? k : mx;
         }
       } else {
         for (int i = lane; i < nul; i += 32) {
           uint64_t k = s_PK[s_ul[i]] & kKMask;
-          s_S[i] = k;
+          s_S[i] = (uint32_t)k;
           mx = k > mx ? k : mx;
         }
       }
@@ -458,7 +458,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     }
     S_gathered = false;
     __syncwarp();
-    warp_radix_sort(s_S, s_T, s_hist, nul, mx ? 64 - __clzll((long long)mx) : 0);
+    warp_radix_sort<uint32_t>(s_S, s_T, s_hist, nul, mx ? 64 - __clzll((long long)mx) : 0);
     S_valid = true;
   };
 
@@ -535,23 +535,18 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
 
   // S multiset: replace one copy of `oldv` by `newv` (> oldv).
   auto S_update = [&](uint64_t oldv, uint64_t newv) {
-    int c_old = 0, c_new = 0;
-    for (int i = lane; i < nul; i += 32) {
-      uint64_t v = s_S[i];
-      c_old += v < oldv;
-      c_new += v < newv;
-    }
-    c_old = __reduce_add_sync(kFull, c_old);
-    c_new = __reduce_add_sync(kFull, c_new);
+    const uint32_t o = (uint32_t)oldv, nv = (uint32_t)newv;
+    const int c_old = warp_lower_bound<uint32_t>(s_S, nul, o);
+    const int c_new = warp_lower_bound<uint32_t>(s_S, nul, nv);
     // shift S[c_old+1 .. c_new-1] left by one, then S[c_new-1] = newv
     for (int base = c_old; base < c_new - 1; base += 32) {
       int i = base + lane;
-      uint64_t v = (i < c_new - 1) ? s_S[i + 1] : 0;
+      uint32_t v = (i < c_new - 1) ? s_S[i + 1] : 0;
       __syncwarp();
       if (i < c_new - 1) s_S[i] = v;
       __syncwarp();
     }
-    if (lane == 0) s_S[c_new - 1] = newv;
+    if (lane == 0) s_S[c_new - 1] = nv;
     __syncwarp();
   };
 
@@ -1050,7 +1045,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       s_PK[u] = (B << 48) | K;
       s_nst[u] = (int32_t)B;
       if (r) s_R[u] = 0;
-      if (gather) s_S[u] = K;
+      if (gather) s_S[u] = (uint32_t)K;
       mx = K > mx ? K : mx;
       s1 += K;
       const uint64_t k2 = K * K;  // K < 2^32 (decode-unit envelope)

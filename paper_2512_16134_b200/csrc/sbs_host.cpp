@@ -338,8 +338,8 @@ void layout_smem(sbs::DevPoint& d) {
   d.sm_pf_part = take(PD);
   d.sm_dPK = take(8 * U);
   d.sm_dR = take(8 * U);
-  d.sm_dS = take(8 * U);
-  d.sm_dT = take(8 * U);
+  d.sm_dS = take(4 * U);
+  d.sm_dT = take(4 * U);
   d.sm_dnst = take(4 * U);
   d.sm_ulist = take(2 * U);
   d.sm_bcnt = take(2 * (size_t)d.Dn * d.R);

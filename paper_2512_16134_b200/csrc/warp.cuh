@@ -138,13 +138,13 @@ namespace sbs {
 // histogram, warp exclusive scan, then a stable scatter of 32-key chunks where
 // __match_any_sync groups equal digits and popc(peers & lanemask_lt) ranks
 // each key inside its group.
-__device__ __forceinline__ void warp_radix_sort(uint64_t* a, uint64_t* t, uint32_t* hist, int n,
-                                                int nbits) {
+template <typename Key>
+__device__ __forceinline__ void warp_radix_sort(Key* a, Key* t, uint32_t* hist, int n, int nbits) {
   const int lane = lane_id();
   const unsigned lt = lanemask_lt();
   const int passes = (nbits + 7) >> 3;
-  uint64_t* src = a;
-  uint64_t* dst = t;
+  Key* src = a;
+  Key* dst = t;
   for (int p = 0; p < passes; ++p) {
     const int sh = 8 * p;
     for (int b = lane; b < 256; b += 32) hist[b] = 0;
@@ -168,7 +168,7 @@ __device__ __forceinline__ void warp_radix_sort(uint64_t* a, uint64_t* t, uint32
     for (int base = 0; base < n; base += 32) {
       const int i = base + lane;
       const bool valid = i < n;
-      const uint64_t x = valid ? src[i] : 0;
+      const Key x = valid ? src[i] : 0;
       const unsigned dg = valid ? ((unsigned)(x >> sh) & 255u) : 256u + lane;
       const unsigned peers = __match_any_sync(kFull, dg);
       unsigned off = 0;
@@ -180,12 +180,37 @@ __device__ __forceinline__ void warp_radix_sort(uint64_t* a, uint64_t* t, uint32
       if (valid && (peers >> lane) == 1u) hist[dg] = off + __popc(peers);
       __syncwarp();
     }
-    uint64_t* tmp = src; src = dst; dst = tmp;
+    Key* tmp = src; src = dst; dst = tmp;
   }
   if (passes & 1) {
     for (int i = lane; i < n; i += 32) a[i] = t[i];
     __syncwarp();
   }
+}
+
+}  // namespace sbs
+
+namespace sbs {
+
+// Number of elements < x in a sorted array (a lower bound), by a warp: one
+// 32-ary partition round per 32x narrowing, then a ballot over the last <= 32.
+template <typename Key>
+__device__ __forceinline__ int warp_lower_bound(const Key* a, int n, Key x) {
+  const int lane = lane_id();
+  int lo = 0, hi = n;  // answer in [lo, hi]
+  while (hi - lo > 32) {
+    const int step = (hi - lo + 31) >> 5;
+    const int idx = lo + lane * step;
+    const bool lt = idx < hi && a[idx] < x;
+    const int k = __popc(__ballot_sync(kFull, lt));  // pivots < x (ascending)
+    if (k == 0) return lo;
+    const int nlo = lo + (k - 1) * step + 1;
+    const int nhi = lo + k * step;
+    lo = nlo;
+    hi = nhi < hi ? nhi : hi;
+  }
+  const int idx = lo + lane;
+  return lo + __popc(__ballot_sync(kFull, idx < hi && a[idx] < x));
 }
 
 }  // namespace sbs
