@@ -525,10 +525,13 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     const bool fallback = ns == 0;
     if (fallback) CNT(fb, 1);
     else if (ns < nul) CNT(mask, 1);
-    uint64_t key = fallback ? ba : bs;
-    int pos = fallback ? pa : ps;
-    uint64_t m = warp_min_u64(key);
-    const int sel = (int)__reduce_min_sync(kFull, key == m ? (uint32_t)pos : 0x7fffffffu);
+    const uint64_t key = fallback ? ba : bs;
+    const int pos = fallback ? pa : ps;
+    // key = B << 48 | K with K < 2^32: minimise (B, K, position) with 32-bit REDUX
+    const uint32_t kb = (uint32_t)(key >> 48), kk = (uint32_t)key;
+    const uint32_t mb = __reduce_min_sync(kFull, kb);
+    const uint32_t mk = __reduce_min_sync(kFull, kb == mb ? kk : 0xffffffffu);
+    const int sel = (int)__reduce_min_sync(kFull, (kb == mb && kk == mk) ? (uint32_t)pos : 0x7fffffffu);
     PROF_END(5);
     return sel;
   };
@@ -590,7 +593,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       }
       CNT(dsel, 1);
       const int u = ul_ident ? pos : s_ul[pos];
-      const int j = u / Dd;
+      const int j = Dn == 1 ? 0 : u / Dd;
       // admit_decode (engine_model.cpp:145-151): B += 1, K += prompt_len
       const uint64_t k0 = s_PK[u];
       const uint64_t K0 = k0 & kKMask, B0 = k0 >> 48;
@@ -615,7 +618,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       if (cap_batch > 0 && (int64_t)B0 + 1 >= cap_batch) ul_dirty = true;
       // completion ring: finishes at step d_step + ceil(target/tps)
       const int64_t target = (int64_t)out - 1;
-      const int64_t nsteps = (target + tps - 1) / tps;
+      const int64_t nsteps = tps == 1 ? target : (target + tps - 1) / tps;
       const int64_t excess = nsteps * tps - target;
       const int64_t c = bcast(d_step, j) + nsteps;
       const int b = j * R + (int)(c & (R - 1));
