@@ -18,7 +18,7 @@ _i64p = C.POINTER(C.c_int64)
 def lib():
     global _lib
     if _lib is None:
-        srcs = [HERE / "sbs_oracle.c", HERE / "sbs_oracle.h"]
+        srcs = [HERE / "sbs_oracle.c", HERE / "sbs_oracle_des.c", HERE / "sbs_oracle.h"]
         if not LIB_PATH.exists() or any(s.stat().st_mtime > LIB_PATH.stat().st_mtime for s in srcs):
             subprocess.run(["make", "-s", "oracle"], cwd=HERE, check=True)
         L = C.CDLL(str(LIB_PATH))
@@ -96,3 +96,114 @@ def allocate_many(req_off, n_pending, dp_off, n_limit, req_id, prompt_len, wait_
                             (req_off, n_pending, dp_off, n_limit, req_id, prompt_len, wait_in,
                              caps, od, orank, ow, flow)])
     return od[:n], orank[:n], ow[:n], caps, flow[:len(n_pending)]
+
+
+# ---------------- full simulator restatement (sbs_oracle_des.c) ----------------
+class _Drop(C.Structure):
+    _fields_ = [("instance", C.c_int), ("from_s", C.c_double), ("until_s", C.c_double)]
+
+
+class _Dead(C.Structure):
+    _fields_ = [("instance", C.c_int), ("time_s", C.c_double)]
+
+
+class _Topo(C.Structure):
+    _fields_ = [("instance", C.c_int), ("healthy", C.c_int), ("time_s", C.c_double)]
+
+
+class OrcConfig(C.Structure):
+    _fields_ = [("n_instances_prefill", C.c_int), ("n_instances_decode", C.c_int),
+                ("dp_degree", C.c_int), ("dp_degree_decode", C.c_int), ("c_chunk", C.c_int64),
+                ("w_size", C.c_int64), ("decode_tokens_per_step", C.c_int64),
+                ("t_default_s", C.c_double), ("l_net_s", C.c_double), ("iqr_k", C.c_double),
+                ("watchdog_multiplier", C.c_double), ("n_limit", C.c_int),
+                ("decode_max_batch_per_dp", C.c_int), ("prefill_base_s", C.c_double),
+                ("prefill_per_token_s", C.c_double), ("decode_base_s", C.c_double),
+                ("decode_per_request_s", C.c_double), ("decode_per_kv_token_s", C.c_double),
+                ("policy", C.c_int), ("decode_policy", C.c_int), ("seed", C.c_uint64),
+                ("duration_s", C.c_double), ("warmup_fraction", C.c_double),
+                ("drops", C.POINTER(_Drop)), ("n_drops", C.c_int), ("deads", C.POINTER(_Dead)),
+                ("n_deads", C.c_int), ("topology", C.POINTER(_Topo)), ("n_topology", C.c_int)]
+
+
+class OrcResult(C.Structure):
+    _fields_ = ([(k, C.c_uint64) for k in ("generated", "completed", "throttled", "in_flight",
+                                           "window_requests")]
+                + [(k, C.c_double) for k in ("ttft_mean_s", "ttft_p50_s", "ttft_p95_s",
+                                             "scheduler_wait_mean_s", "device_wait_mean_s",
+                                             "total_wait_mean_s")]
+                + [("passes", C.c_uint64), ("chunk_util_mean", C.c_double),
+                   ("decode_steps", C.c_uint64), ("output_tokens", C.c_uint64)]
+                + [(k, C.c_double) for k in ("output_tokens_per_s", "kv_mean_time_avg",
+                                             "kv_sigma_time_avg", "completed_per_s")]
+                + [(k, C.c_uint64) for k in ("watchdog_fires", "dropped_end_forwards",
+                                             "rejected_samples", "deferrals",
+                                             "flow_control_events", "mask_events",
+                                             "fallback_events")]
+                + [("warmup_cutoff_s", C.c_double), ("duration_s", C.c_double),
+                   ("alloc_calls", C.c_uint64), ("decode_selects", C.c_uint64),
+                   ("error", C.c_int)])
+
+
+def _config(cfg):
+    """Reference JSON schema (defaults: config.h / core.h) -> OrcConfig."""
+    c = cfg.get("cluster", {})
+    e = c.get("engine", {})
+    w = cfg.get("workload", {})
+    s = cfg.get("scheduler", {})
+    sim = cfg.get("sim", {})
+    f = cfg.get("faults", {})
+    oc = OrcConfig(
+        n_instances_prefill=c.get("n_instances_prefill", 1),
+        n_instances_decode=c.get("n_instances_decode", 1), dp_degree=c.get("dp_degree", 1),
+        dp_degree_decode=c.get("dp_degree_decode", 0), c_chunk=c.get("c_chunk", 1),
+        w_size=c.get("w_size", 64), decode_tokens_per_step=c.get("decode_tokens_per_step", 1),
+        t_default_s=c.get("t_default_s", 0.1), l_net_s=c.get("l_net_s", 0.0),
+        iqr_k=c.get("iqr_k", 1.5), watchdog_multiplier=c.get("watchdog_multiplier", 5.0),
+        n_limit=c.get("n_limit", 8), decode_max_batch_per_dp=c.get("decode_max_batch_per_dp", 0),
+        prefill_base_s=e.get("prefill_base_s", 0.0),
+        prefill_per_token_s=e.get("prefill_per_token_s", 0.0),
+        decode_base_s=e.get("decode_base_s", 0.0),
+        decode_per_request_s=e.get("decode_per_request_s", 0.0),
+        decode_per_kv_token_s=e.get("decode_per_kv_token_s", 0.0),
+        policy={"sbs": 0, "immediate": 1, "round_robin": 1, "least_outstanding": 3}[s.get("policy", "sbs")],
+        decode_policy={"iqr": 0, "random": 1, "round_robin": 2}[s.get("decode_policy", "iqr")],
+        seed=sim.get("seed", 1), duration_s=w.get("duration_s", 1.0),
+        warmup_fraction=sim.get("warmup_fraction", 0.1))
+    keep = []
+    d = [_Drop(x.get("instance", -1), x.get("from_s", 0.0), x.get("until_s", float("inf")))
+         for x in f.get("drop_end_forward", [])]
+    dd = [_Dead(x.get("instance", 0), x.get("time_s", 0.0)) for x in f.get("dead", [])]
+    t = [_Topo(x.get("instance", 0), 1 if x.get("healthy") else 0, x.get("time_s", 0.0))
+         for x in f.get("topology", [])]
+    if d:
+        arr = (_Drop * len(d))(*d); keep.append(arr)
+        oc.drops, oc.n_drops = C.cast(arr, C.POINTER(_Drop)), len(d)
+    if dd:
+        arr = (_Dead * len(dd))(*dd); keep.append(arr)
+        oc.deads, oc.n_deads = C.cast(arr, C.POINTER(_Dead)), len(dd)
+    if t:
+        arr = (_Topo * len(t))(*t); keep.append(arr)
+        oc.topology, oc.n_topology = C.cast(arr, C.POINTER(_Topo)), len(t)
+    return oc, keep
+
+
+def run(cfg, arrival, prompt, output, per_request=True):
+    """Run the C restatement on a given trace (e.g. the reference's own)."""
+    L = lib()
+    if not hasattr(L, "_orc_run_bound"):
+        L.orc_run.argtypes = [C.POINTER(OrcConfig), C.c_void_p, C.c_void_p, C.c_void_p,
+                              C.c_int64, C.POINTER(OrcResult), C.c_void_p]
+        L._orc_run_bound = True
+    oc, keep = _config(cfg)
+    a = np.ascontiguousarray(arrival, np.int64)
+    p = np.ascontiguousarray(prompt, np.int32)
+    o = np.ascontiguousarray(output, np.int32)
+    res = OrcResult()
+    pr = np.zeros((max(len(a), 1), 5), np.int64) if per_request else None
+    L.orc_run(C.byref(oc), a.ctypes.data, p.ctypes.data, o.ctypes.data, len(a), C.byref(res),
+              pr.ctypes.data if per_request else None)
+    out = {"agg": {k: getattr(res, k) for k, _ in OrcResult._fields_}}
+    if per_request:
+        out["requests"] = pr[: len(a)]
+    return out

@@ -37,4 +37,51 @@ void orc_allocate_many(int64_t n_windows, const int64_t* req_off, const int32_t*
                        const int64_t* prompt_len, const int32_t* wait_in, int64_t* caps,
                        int32_t* out_dp, int32_t* out_rank, int32_t* wait_out, uint8_t* flow);
 
+/* ---- full simulator restatement (sbs_oracle_des.c) ---- */
+typedef struct { int instance; double from_s, until_s; } orc_drop;
+typedef struct { int instance; double time_s; } orc_dead;
+typedef struct { int instance; int healthy; double time_s; } orc_topo;
+
+/* ExperimentConfig fields on the path (config.h:66-75, core.h:236-260) */
+typedef struct {
+  int n_instances_prefill, n_instances_decode, dp_degree, dp_degree_decode;
+  int64_t c_chunk, w_size, decode_tokens_per_step;
+  double t_default_s, l_net_s, iqr_k, watchdog_multiplier;
+  int n_limit, decode_max_batch_per_dp;
+  double prefill_base_s, prefill_per_token_s, decode_base_s, decode_per_request_s,
+      decode_per_kv_token_s;
+  int policy;        /* 0 sbs, 1 immediate/round_robin, 3 least_outstanding */
+  int decode_policy; /* 0 iqr, 1 random, 2 round_robin */
+  uint64_t seed;
+  double duration_s, warmup_fraction;
+  const orc_drop* drops;
+  int n_drops;
+  const orc_dead* deads;
+  int n_deads;
+  const orc_topo* topology;
+  int n_topology;
+} orc_config;
+
+/* Aggregates (metrics.h:67-102) + counters */
+typedef struct {
+  uint64_t generated, completed, throttled, in_flight, window_requests;
+  double ttft_mean_s, ttft_p50_s, ttft_p95_s, scheduler_wait_mean_s, device_wait_mean_s,
+      total_wait_mean_s;
+  uint64_t passes;
+  double chunk_util_mean;
+  uint64_t decode_steps, output_tokens;
+  double output_tokens_per_s, kv_mean_time_avg, kv_sigma_time_avg, completed_per_s;
+  uint64_t watchdog_fires, dropped_end_forwards, rejected_samples, deferrals,
+      flow_control_events, mask_events, fallback_events;
+  double warmup_cutoff_s, duration_s;
+  uint64_t alloc_calls, decode_selects;
+  int error;
+} orc_result;
+
+/* run_experiment (simulation.cpp:136-169) on a given trace.  per_req
+ * (nullable): n rows of (status, dispatch, prefill_start, first_token,
+ * completion), -1 when unset.  Returns 0 or 3 (invariant). */
+int orc_run(const orc_config* cfg, const int64_t* arr, const int32_t* prompt,
+            const int32_t* output, int64_t n, orc_result* res, int64_t* per_req);
+
 #endif
