@@ -204,9 +204,10 @@ int sbs_sim_requests(sbs_sim* sim, int32_t point, int64_t* dispatch_ns,
  * kvband.csv, control.csv and the dispatch log (metrics.cpp:194-273).
  * With words NULL only *n_out is set. */
 int sbs_sim_log(sbs_sim* sim, int32_t point, int64_t* words, int64_t cap, int64_t* n_out);
-/* Development hook: per-region clock64 cycles summed over replicas (non-zero
- * only in an SBS_PROF=1 build of the library). */
-int sbs_sim_profile_counters(const sbs_sim* sim, int64_t* out16);
+/* Development hook: SBS_PROF_COUNTERS per-region clock64 cycle / spin
+ * counters summed over replicas (non-zero only in an SBS_PROF=1 build). */
+#define SBS_PROF_COUNTERS 24
+int sbs_sim_profile_counters(const sbs_sim* sim, int64_t* out);
 /* Number of kernel launches enqueued by one sbs_sim_launch. */
 int32_t sbs_sim_launches_per_run(const sbs_sim* sim);
 /* Device bytes allocated for this simulator. */

@@ -467,7 +467,7 @@ class Simulator:
         return buf[: n.value]
 
     def profile_counters(self):
-        out = (C.c_int64 * 16)()
+        out = (C.c_int64 * 24)()
         lib().sbs_sim_profile_counters(self.handle, out)
         return list(out)
 

@@ -155,12 +155,10 @@ constexpr int kErrEnvelope = 6;               // B >= 2^15 or K >= 2^32 on a dec
 // 50 replicated registers per lane.  FP sums stay sequential in event order.
 struct Counters {
   long long completed, throttled, cw, wr, passes, steps, outtok, wdf, drop, rej, def, flow,
-      mask, fb, alloc, dsel, events, ttft, sched, dev, kv_n;
-  double util, kv_mean, kv_sig;
+      mask, fb, alloc, dsel, events, ttft, sched, dev, kv_n, n_ttft, tpot_n, err;
+  double util, kv_mean, kv_sig, tpot;
 };
 
-// KD: prefill DP units per lane, 1 (dp_degree <= 32) or 4 (<= 128).
-// LOG: keep run records (compiled out of the sweep kernel).
 // Development instrumentation: -DSBS_PROF accumulates clock64() cycles per
 // region (inclusive) into DevResult::prof.  Compiled out by default.
 #ifdef SBS_PROF
@@ -171,8 +169,49 @@ struct Counters {
 #define PROF_END(r)
 #endif
 
-template <int KD, bool LOG>
-__device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* sm) {
+// Ordering of the two-warp channel: CTA scope within one CTA, cluster scope
+// when the two warps of a replica sit in the two CTAs of a cluster.
+template <bool CL>
+__device__ __forceinline__ void chan_fence() {
+  if constexpr (CL) asm volatile("fence.acq_rel.cluster;" ::: "memory");
+  else __threadfence_block();
+}
+// acquire load of a channel word from this warp's own copy
+template <bool CL>
+__device__ __forceinline__ long long chan_ld(const volatile long long* p) {
+  long long v;
+  if constexpr (CL) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared((const void*)p);
+    asm volatile("ld.acquire.cluster.shared::cta.b64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+  } else {
+    v = *p;
+    __threadfence_block();
+  }
+  return v;
+}
+template <bool CL>
+__device__ __forceinline__ int chan_ld(const volatile int* p) {
+  int v;
+  if constexpr (CL) {
+    const unsigned a = (unsigned)__cvta_generic_to_shared((const void*)p);
+    asm volatile("ld.acquire.cluster.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  } else {
+    v = *p;
+    __threadfence_block();
+  }
+  return v;
+}
+
+// KD: prefill DP units per lane, 1 (dp_degree <= 32) or 4 (<= 128).
+// LOG: keep run records (compiled out of the sweep kernel).
+// ROLE: 0 = the whole replica on one warp; 1 = the prefill warp and 2 = the
+// decode warp of a two-warp replica (see the channel notes at the event loop).
+template <int KD, bool LOG, int ROLE, bool CL>
+__device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* sm,
+                            unsigned char* sm_peer) {
+  static_assert(!(LOG && ROLE != 0), "run records are kept by the one-warp replica only");
+  constexpr bool kPre = ROLE != 2;  // this warp runs the prefill side
+  constexpr bool kDec = ROLE != 1;  // this warp runs the decode side
   const int lane = lane_id();
   const unsigned lt_mask = lanemask_lt();
 
@@ -225,17 +264,25 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   uint32_t* s_hist = (uint32_t*)(sm + pt.sm_hist);
   int64_t* s_wr = (int64_t*)(sm + pt.sm_wring);
   uint64_t* s_wk = (uint64_t*)(sm + pt.sm_wkeys);
-  Counters* cn = (Counters*)(sm + pt.sm_cnt);
+  Counters* cn = (Counters*)(sm + (ROLE == 2 ? pt.sm_cnt2 : pt.sm_cnt));
+  // two-warp replicas: every channel word is read from this warp's own copy
+  // (chL) and written into the peer's (chR); one CTA (CL false): the same
+  // struct; a CTA pair of a cluster (CL true): the peer CTA's shared memory
+  Chan* const chL = (Chan*)(sm + pt.sm_chan);
+  Chan* const chR = (Chan*)((CL ? sm_peer : sm) + pt.sm_chan);
   if (lane == 0) {
     long long* z = (long long*)cn;
     for (int i = 0; i < (int)(sizeof(Counters) / 8); ++i) z[i] = 0;
   }
 
-  for (int g = lane; g < PD; g += 32) {
-    s_out[g] = 0; s_head[g] = 0; s_tail[g] = 0; s_rel[g] = 0; s_part[g] = 0;
+  if (kPre)
+    for (int g = lane; g < PD; g += 32) {
+      s_out[g] = 0; s_head[g] = 0; s_tail[g] = 0; s_rel[g] = 0; s_part[g] = 0;
+    }
+  if (kDec) {
+    for (int u = lane; u < U; u += 32) { s_PK[u] = 0; s_R[u] = 0; s_nst[u] = 0; }
+    for (int b = lane; b < Dn * R; b += 32) s_bcnt[b] = 0;
   }
-  for (int u = lane; u < U; u += 32) { s_PK[u] = 0; s_R[u] = 0; s_nst[u] = 0; }
-  for (int b = lane; b < Dn * R; b += 32) s_bcnt[b] = 0;
   __syncwarp();
 
   // ---- lane-resident instance state (lane p <-> prefill instance p,
@@ -247,6 +294,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   uint32_t ef_s = 0xffffffffu, wd_s = 0xffffffffu;
   const int64_t p_death = (lane < P) ? pt.death[lane] : kInf64;
   int32_t imm_dp = 0;  // RotationCursor::next_dp (baselines.h:17-20)
+  int32_t ef_hidx = 0, ef_hext = 0;  // ROLE 1: handler that scheduled the live EndForward
 
   int dflags = (lane < Dn) ? G_HEALTHY : 0;
   int64_t d_step = 0;
@@ -256,6 +304,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   int64_t d_res = 0;            // residents over the instance's units
   double d_worst = 0.0;         // max_u decode_per_request*B + decode_per_kv*K
   int64_t d_res_begin = 0;      // residents stamped at the running step
+  int64_t ds_ts = 0;            // ROLE 2: scheduling time of the live decode step,
+  int32_t ds_hk = 1, ds_hi = 0;  // its handler: 0 = EndForward #ds_hi, 1 = a decode step
 
   // ---- scheduler state (SchedulerState, core.h:197-218; new_cluster core.cpp:162-168)
   int64_t now = 0;
@@ -286,6 +336,10 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   double fr25 = 0.0, fr75 = 0.0;
   int32_t nul = 0;
   int error = 0;
+  int32_t pidx = 0, cur_ext = 0;   // ROLE 1: prefill-warp event index, handler is arrival/topology
+  int32_t d_hk = 1, d_hi = 0;      // ROLE 2: handler of the decode event being processed
+  int32_t ktail = 0;               // ROLE 1: hand-off keys written
+  int32_t ctail = 0, chead = 0;    // ROLE 2 / ROLE 1: completion ring positions
 
   // other-event cache (EF/WD/DS min)
   bool odirty = true;
@@ -297,7 +351,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   int64_t n_ttft = 0, tpot_n = 0;
   double tpot_sum = 0.0;
 #ifdef SBS_PROF
-  long long prof_acc[16] = {0};
+  long long prof_acc[24] = {0};
+  const long long prof_t0 = clock64();
 #endif
 #define CNT(f, v) do { if (lane == 0) cn->f += (v); } while (0)
   // append one fixed-size record (lane 0); overflow is reported, never silent
@@ -383,19 +438,19 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   // All per-request inputs are passed in: the callers issue every global
   // load of a completer at once (one memory round trip, not a chain).
   auto complete_lanes = [&](bool has, int64_t id, int64_t ftok, bool decode, int64_t arr,
-                            int32_t out, int64_t disp, int64_t ps) {
+                            int32_t out, int64_t disp, int64_t ps, int64_t t_done) {
     int64_t ttft = 0;
     bool inwin = false;
     if (has) {
       l_done += 1;
-      if (now >= warmup) l_cw += 1;
+      if (t_done >= warmup) l_cw += 1;
       if (per_req) {
-        o_comp[id] = now;
+        o_comp[id] = t_done;
         o_status[id] = kStCompleted;
       }
       if (decode) {
         // TPOT (not in the reference): ns per output token after the first
-        const double per = __dmul_rn((double)(now - ftok), __drcp_rn((double)(out - 1)));
+        const double per = __dmul_rn((double)(t_done - ftok), __drcp_rn((double)(out - 1)));
         tpot_sum = __dadd_rn(tpot_sum, per);
         tpot_n += 1;
         atomicAdd((unsigned long long*)&g_tpot_hist[hist_bin((int64_t)per)], 1ull);
@@ -410,8 +465,50 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       }
     }
     unsigned m = __ballot_sync(kFull, inwin);
-    if (inwin) g_ttft[n_ttft + __popc(m & lt_mask)] = ttft;
+    if (inwin) {
+      const int64_t k = n_ttft + __popc(m & lt_mask);
+      g_ttft[ROLE == 2 ? N - 1 - k : k] = ttft;  // decode warp fills from the top
+    }
     n_ttft += __popc(m);
+  };
+
+  // ROLE 1: account the decode warp's completions (metrics.cpp:117-153 inputs)
+  auto consume_completions = [&]() {
+#ifdef SBS_PROF
+    const long long pc0 = clock64();
+#endif
+    for (;;) {
+      // one decode-warp chunk at a time, each record on the lane that held it
+      // there: the lane-local TPOT sums accumulate exactly as in a serial run.
+      // Entries carry the ring lap of their position: a chunk is taken once
+      // every word of it is visible (no release fence on the decode side).
+      const int i = chead + lane;
+      const uint64_t lap = (uint64_t)((i / kChanComp) & 0xFFFF);
+      const uint64_t w0 = (uint64_t)*(volatile long long*)&chL->comp_id[i % kChanComp];
+      const uint64_t w1 = (uint64_t)*(volatile long long*)&chL->comp_t[i % kChanComp];
+      const int cnt = __shfl_sync(kFull, (w0 >> 48) == lap ? (int)((w0 >> 32) & 63) : 0, 0);
+      if (cnt == 0) break;
+      const bool has = lane < cnt;
+      if (!__all_sync(kFull, !has || ((w0 >> 48) == lap && (w1 >> 48) == lap))) break;
+      int64_t id = 0, t = 0, ft = 0, arr = 0, disp = 0, ps = 0;
+      int32_t out = 0;
+      if (has) {
+        id = (int64_t)(w0 & 0xFFFFFFFFull);
+        t = (int64_t)(w1 & ((1ull << 48) - 1));
+        ft = o_ftok[id];
+        arr = __ldg(g_arr + id);
+        out = __ldg(g_output + id);
+        disp = o_dispatch[id];
+        ps = o_pstart[id];
+      }
+      complete_lanes(has, id, ft, true, arr, out, disp, ps, t);
+      chead += cnt;
+      __syncwarp();  // every lane's entry reads precede the release of the slots
+      if (lane == 0) chR->chead = chead;
+    }
+#ifdef SBS_PROF
+    prof_acc[19] += clock64() - pc0;
+#endif
   };
   // (the lane-local partial sums above are exact integers: reduced once at the end)
 
@@ -476,6 +573,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       ds_t = t_end;
       ds_s = seq;
       d_res_begin = d_res;
+      ds_ts = now;
+      ds_hk = d_hk;
+      ds_hi = d_hi;
     }
     seq++;
     odirty = true;
@@ -733,6 +833,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       p_started = now;
       ef_t = t_end;
       ef_s = seq;
+      ef_hidx = pidx;
+      ef_hext = cur_ext;
     }
     seq++;
     odirty = true;
@@ -767,14 +869,33 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       }
       bool done = has && out <= 1;   // decode_target() == 0
       bool wait = has && out > 1;
-      complete_lanes(done, id, now, false, arr, out, disp, ps);
+      complete_lanes(done, id, now, false, arr, out, disp, ps, now);
       unsigned m = __ballot_sync(kFull, wait);
-      if (wait) {
-        int32_t prompt = __ldg(g_prompt + id);
-        g_dwait[ndw + __popc(m & lt_mask)] = decode_key((int64_t)prompt + out, id);
+      if (ROLE == 1) {
+        // hand-off ring: wait for room (the decode warp consumes independently)
+        if (m) {
+          for (;;) {
+            const int kh = chL->khead;
+            if (ktail + 32 - kh <= kChanKeys) break;
+            consume_completions();  // the decode warp may be waiting on us
+            __nanosleep(100);
+          }
+          chan_fence<CL>();
+          if (wait) {
+            int32_t prompt = __ldg(g_prompt + id);
+            chR->keys[(ktail + __popc(m & lt_mask)) % kChanKeys] = decode_key((int64_t)prompt + out, id);
+          }
+          ktail += __popc(m);
+          ndw += __popc(m);  // keys of this EndForward
+        }
+      } else {
+        if (wait) {
+          int32_t prompt = __ldg(g_prompt + id);
+          g_dwait[ndw + __popc(m & lt_mask)] = decode_key((int64_t)prompt + out, id);
+        }
+        ndw += __popc(m);
+        if (ndw > QD - 32) { error = kErrOverflow; break; }
       }
-      ndw += __popc(m);
-      if (ndw > QD - 32) { error = kErrOverflow; break; }
     }
     if (lane == p) pflags &= ~F_BUSY;
     __syncwarp();
@@ -1015,6 +1136,31 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       bool has = e < n;
       int64_t id = 0, ft = 0, arr = 0, disp = 0, ps = 0;
       int32_t out = 0;
+      if (ROLE == 2) {
+        // completion accounting goes back to the prefill warp: (id, time)
+        const int cnt = n - base < 32 ? n - base : 32;
+        for (;;) {
+          const int chd = chan_ld<CL>(&chL->chead);
+          if (ctail + cnt - chd <= kChanComp) break;
+#ifdef SBS_PROF
+          prof_acc[18] += 1;
+#endif
+          __nanosleep(64);
+        }
+        if (has) {
+          const int4 v = ent[e];
+          const int pos = ctail + lane, slot = pos % kChanComp;
+          const uint64_t lap = (uint64_t)((pos / kChanComp) & 0xFFFF) << 48;
+          chR->comp_t[slot] = (int64_t)((uint64_t)now | lap);
+          chR->comp_id[slot] =
+              (int64_t)((uint64_t)(uint32_t)v.x | (lane == 0 ? (uint64_t)cnt << 32 : 0) | lap);
+          atomicAdd((unsigned long long*)&s_R[v.y], (unsigned long long)(kBOne | (uint64_t)(uint32_t)v.z));
+          exc += v.w;
+          rel += (uint32_t)v.z;
+        }
+        ctail += cnt;
+        continue;
+      }
       if (has) {
         const int4 v = ent[e];
         id = v.x;
@@ -1027,7 +1173,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         exc += v.w;
         rel += (uint32_t)v.z;
       }
-      complete_lanes(has, id, ft, true, arr, out, disp, ps);
+      complete_lanes(has, id, ft, true, arr, out, disp, ps, now);
     }
     __syncwarp();
     if (lane == 0) s_bcnt[b] = 0;
@@ -1188,7 +1334,146 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   //   -> try_start_pass -> [SBS EndForward ack] -> try_dispatch ->
   //   try_start_pass(target) -> trailing tick.
   // =======================================================================
+  if constexpr (ROLE == 2) {
+    // ===================================================================
+    // Decode warp of a two-warp replica.  The decode side never feeds back
+    // into the prefill side; it sees (a) its own decode steps, (b) topology
+    // events of decode instances, (c) one record per EndForward from the
+    // prefill warp (simulation.cpp:397-411 hand-off).  They are merged in the
+    // reference's (time, seq) order: topology < EndForward/step by seq; an
+    // EndForward/step tie at the same ns is ordered by their scheduling
+    // times, then by the prefill-warp index of the scheduling handlers (an
+    // EndForward's drain schedules steps before its own restart/dispatch),
+    // then arrival/topology handlers before internal ones; anything deeper is
+    // reported (kErrSplitTie) and the host reruns the replica on one warp.
+    // The prefill warp publishes p_done = time of the next event it will
+    // process, so a decode event at time c is safe once p_done > c.
+    // ===================================================================
+    int rhead = 0, khead = 0, dtopo = 0, pub_head = 0;
+    bool aborted = false;
+    auto next_dtopo = [&]() -> int64_t {
+      while (dtopo < n_topo && pt.topo_inst[dtopo] < P) ++dtopo;
+      return dtopo < n_topo ? pt.topo_time[dtopo] : kInf64;
+    };
+    int64_t dt_t = next_dtopo();
+    for (;;) {
+      if (odirty) recompute_other();
+      const int64_t td = o_t <= horizon ? o_t : kInf64;
+      const int64_t tt = dt_t <= horizon ? dt_t : kInf64;
+      // progress first, then the queue (one shared load per word: warp-uniform)
+      const long long pdone = chan_ld<CL>(&chL->p_done);
+      const int tail = chan_ld<CL>(&chL->tail);
+      const bool have = rhead < tail;
+      const ChanRec* rc = &chL->rec[rhead % kChanRecs];
+      const int64_t th = have ? rc->t : kInf64;
+      if (aborted) {  // keep the prefill warp unblocked until it finishes
+        if (have) {
+          rhead += 1;
+          khead += rc->nk;
+          chan_fence<CL>();
+          __syncwarp();
+          if (lane == 0) { chR->head = rhead; chR->khead = khead; }
+          continue;
+        }
+        if (pdone == kInf64) break;
+        __nanosleep(128);
+        continue;
+      }
+      const int64_t c = td < tt ? td : tt;
+      if (!have) {
+        if (c == kInf64 && pdone == kInf64) break;  // all done
+        if (pdone <= c) {  // an EndForward <= c may still come
+#ifdef SBS_PROF
+          prof_acc[16] += 1;
+#endif
+          if (pub_head != rhead) {  // exact release before waiting on the prefill warp
+            chan_fence<CL>();
+            __syncwarp();
+            if (lane == 0) { chR->head = rhead; chR->khead = khead; }
+            pub_head = rhead;
+          }
+          __nanosleep(64);
+          continue;
+        }
+      }
+      int kind;  // 0 record, 1 step, 2 topology
+      if (tt <= th && tt <= td) {
+        kind = 2;
+      } else if (th < td) {
+        kind = 0;
+      } else if (th == td) {
+        const int j = o_i;
+        const int64_t tsd = bcast(ds_ts, j);
+        const int hk = bcast(ds_hk, j), hi = bcast(ds_hi, j);
+        int ef_first;
+        if (rc->ts != tsd) ef_first = rc->ts < tsd;
+        else if (hk == 0) ef_first = rc->h_idx < hi;
+        else if (rc->h_ext) ef_first = 1;
+        else { error = kErrSplitTie; aborted = true; continue; }
+        kind = ef_first ? 0 : 1;
+      } else {
+        kind = 1;
+      }
+      if (kind == 0) {
+        // ---- hand_off_finished (simulation.cpp:397-411) of one EndForward
+        now = th;
+        const int nk = rc->nk, k0 = rc->k0;
+        d_hk = 0;
+        d_hi = rc->ef_idx;
+        if (ndw + nk + 32 > QD) { error = kErrOverflow; aborted = true; continue; }
+        // release the previous record's slots (its reads are long complete; this
+        // record's are released at the next one, or exactly before a wait)
+        if (lane == 0) { chR->head = rhead; chR->khead = khead; }
+        pub_head = rhead;
+        for (int i = lane; i < nk; i += 32) g_dwait[ndw + i] = chL->keys[(k0 + i) % kChanKeys];
+        ndw += nk;
+        rhead += 1;
+        khead += nk;
+        PROF_BEGIN(4);
+        drain_decode();
+        PROF_END(4);
+      } else if (kind == 1) {
+        // ---- on_decode_step (simulation.cpp:497-512)
+        now = td;
+        CNT(events, 1);
+        const int j = o_i;
+        if (lane == j) ds_t = kInf64;
+        odirty = true;
+        maybe_die_d(j);
+        if (d_flag(j, G_DEAD)) continue;
+        PROF_BEGIN(3);
+        finish_step(j);
+        PROF_END(3);
+        d_hk = 1;
+        PROF_BEGIN(15);
+        drain_decode();
+        PROF_END(15);
+        PROF_BEGIN(10);
+        if (!error) try_begin_step(j);
+        PROF_END(10);
+      } else {
+        // ---- on_topology for a decode instance (simulation.cpp:382-388)
+        now = tt;
+        const int inst = pt.topo_inst[dtopo];
+        const bool h = pt.topo_healthy[dtopo] != 0;
+        dtopo += 1;
+        dt_t = next_dtopo();
+        if (lane == inst - P) dflags = h ? (dflags | G_HEALTHY) : (dflags & ~G_HEALTHY);
+        ul_dirty = true;
+        S_valid = false;
+        S_gathered = false;
+      }
+      if (error) aborted = true;
+    }
+    chan_fence<CL>();
+    __syncwarp();
+    if (lane == 0) chR->d_done = 1;
+#ifdef SBS_PROF
+    prof_acc[20] += clock64() - prof_t0;
+#endif
+  } else {
   int64_t topo_t = (n_topo > 0) ? pt.topo_time[0] : kInf64;
+  int ch_tail = 0;
   if (g_log && sbs) log_rec(LOG_CONTROL, 4, 0, i_opt, t_bar, n_active, 0);  // simulation.cpp:152
   while (error == 0) {
     PROF_BEGIN(0);
@@ -1208,6 +1493,15 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     now = et;
     PROF_END(0);
     CNT(events, 1);
+    if (ROLE == 1) {
+      consume_completions();
+      // progress for the decode warp: every event before `et` is processed.
+      // (Ordered after every earlier record by the fence that follows each
+      // record publish; a stale value only makes the decode warp wait.)
+      if (lane == 0) chR->p_done = et;
+      pidx += 1;
+      cur_ext = (kind == 0 || kind == 4) ? 1 : 0;
+    }
 
     int start_p = -1;      // try_start_pass before the dispatch stage
     int step_j = -1;       // decode instance whose step finished
@@ -1244,6 +1538,36 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       PROF_BEGIN(2);
       finish_pass(p);
       PROF_END(2);
+      if (ROLE == 1) {
+        // hand-off record for the decode warp (one per EndForward)
+        const int32_t hidx = bcast(ef_hidx, p), hext = bcast(ef_hext, p);
+        for (;;) {
+          const int hd = chL->head;
+          if (ch_tail - hd < kChanRecs) break;
+#ifdef SBS_PROF
+          prof_acc[17] += 1;
+#endif
+          consume_completions();  // the decode warp may be waiting on us
+          __nanosleep(100);
+        }
+        chan_fence<CL>();
+        if (lane == 0) {
+          ChanRec& r = chR->rec[ch_tail % kChanRecs];
+          r.t = now;
+          r.ts = now - measured;  // pass start == when this EndForward was scheduled
+          r.ef_idx = pidx;
+          r.h_idx = hidx;
+          r.h_ext = hext;
+          r.nk = ndw;
+          r.k0 = ktail - ndw;
+        }
+        chan_fence<CL>();  // every lane's key / record writes precede the publish
+        __syncwarp();
+        if (lane == 0) chR->tail = ch_tail + 1;
+        chan_fence<CL>();  // the record precedes any later progress word
+        ch_tail += 1;
+        ndw = 0;
+      }
       start_p = p;
       if (sbs) ef_p = p;
     } else if (kind == kEvWD) {
@@ -1293,7 +1617,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     }
 
     // ---- decode hand-off: hand_off_finished / on_decode_step tail
-    if (kind == kEvEF || kind == kEvDS) {
+    if (ROLE == 0 && (kind == kEvEF || kind == kEvDS)) {
       PROF_BEGIN(4);
       drain_decode();
       PROF_END(4);
@@ -1351,6 +1675,24 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     }
     PROF_END(9);
   }
+  if (ROLE == 1) {
+    chan_fence<CL>();
+    __syncwarp();
+    if (lane == 0) chR->p_done = kInf64;
+#ifdef SBS_PROF
+    prof_acc[21] += clock64() - prof_t0;
+#endif
+    // the decode warp finishes later: keep accounting its completions
+    for (;;) {
+      const int dd = chL->d_done;
+      chan_fence<CL>();
+      consume_completions();
+      if (dd) break;
+      __nanosleep(128);
+    }
+    consume_completions();
+  }
+  }  // ROLE != 2
 
   // ---- results
   tpot_sum = warp_sum_f64(tpot_sum);
@@ -1361,7 +1703,22 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   l_ttft = warp_sum_i64(l_ttft);
   l_sched = warp_sum_i64(l_sched);
   l_dev = warp_sum_i64(l_dev);
+#ifdef SBS_PROF
+  if (ROLE == 0) prof_acc[21] += clock64() - prof_t0;
+#endif
   __syncwarp();
+  if (ROLE != 0) {
+    if (lane == 0) {
+      cn->completed = l_done; cn->cw = l_cw; cn->wr = l_wr;
+      cn->ttft = l_ttft; cn->sched = l_sched; cn->dev = l_dev;
+      cn->n_ttft = n_ttft; cn->tpot_n = tpot_n; cn->tpot = tpot_sum; cn->err = error;
+#ifdef SBS_PROF
+      for (int i = 0; i < 24; ++i) atomicAdd((unsigned long long*)&res.prof[i], (unsigned long long)prof_acc[i]);
+#endif
+    }
+    __syncwarp();
+    return;
+  }
   if (lane == 0) {
     res.completed = l_done;
     res.throttled = cn->throttled;
@@ -1393,7 +1750,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     res.log_n = log_n;
     res.error = error;
 #ifdef SBS_PROF
-    for (int i = 0; i < 16; ++i) res.prof[i] = prof_acc[i];
+    for (int i = 0; i < 24; ++i) res.prof[i] = prof_acc[i];
 #endif
   }
 #undef CNT
@@ -1415,8 +1772,153 @@ __global__ void __launch_bounds__(128) des_kernel(const DevPoint* __restrict__ p
     if (lane_id() == 0) pi = atomicAdd(next_point, 1);
     pi = bcast(pi, 0);
     if (pi >= n_pts) return;
-    run_replica<KD, LOG>(pts[pi], res[pi], my);
+    run_replica<KD, LOG, 0, false>(pts[pi], res[pi], my, my);
     __syncwarp();
+  }
+}
+
+// Channel reset before a replica (one warp).  Completion-ring entries get a
+// lap tag no live position carries, so nothing left from an earlier replica
+// reads as a published entry.
+__device__ void chan_init(Chan* ch, int lane) {
+  for (int i = lane; i < kChanComp; i += 32) ch->comp_id[i] = (long long)(0xFFFFull << 48);
+  if (lane == 0) {
+    ch->p_done = 0;
+    ch->tail = 0; ch->head = 0; ch->ktail = 0; ch->khead = 0; ch->abort = 0;
+    ch->ctail = 0; ch->chead = 0; ch->d_done = 0;
+  }
+  __syncwarp();
+}
+
+// Two-warp replicas: the prefill warp folds both warps' counters into the
+// replica's DevResult (a: prefill warp, b: decode warp).
+__device__ void combine_pair(const DevPoint& pt, DevResult& res, const Counters* a,
+                             const Counters* b) {
+  const int lane = lane_id();
+  // decode-warp TTFTs were written from the top of the buffer: move them
+  // down behind the prefill warp's (the finalize select reads [0, n))
+  const int64_t na = a->n_ttft, nb = b->n_ttft, N = pt.N;
+  for (int64_t base = 0; base < nb; base += 32) {
+    const int64_t i = base + lane;
+    const int64_t v = i < nb ? pt.ttft[N - nb + i] : 0;
+    __syncwarp();
+    if (i < nb) pt.ttft[na + i] = v;
+    __syncwarp();
+  }
+  if (lane == 0) {
+    DevResult& r = res;
+    r.completed = a->completed + b->completed;
+    r.throttled = a->throttled;
+    r.cw = a->cw + b->cw;
+    r.wr = a->wr + b->wr;
+    r.passes = a->passes;
+    r.steps = b->steps;
+    r.out_tokens = b->outtok;
+    r.wd_fires = a->wdf;
+    r.dropped = a->drop;
+    r.rejected = a->rej;
+    r.deferrals = a->def;
+    r.flow = a->flow;
+    r.mask = b->mask;
+    r.fallback = b->fb;
+    r.alloc_calls = a->alloc;
+    r.dec_selects = b->dsel;
+    r.events = a->events + b->events;
+    r.n_ttft = na + nb;
+    r.ttft_sum = a->ttft + b->ttft;
+    r.sched_sum = a->sched + b->sched;
+    r.dev_sum = a->dev + b->dev;
+    r.util_sum = a->util;
+    r.kv_mean_sum = b->kv_mean;
+    r.kv_sigma_sum = b->kv_sig;
+    r.tpot_sum = (a->tpot + b->tpot) / 1e9;
+    r.kv_n = b->kv_n;
+    r.tpot_n = a->tpot_n + b->tpot_n;
+    r.log_n = 0;
+    const long long e = b->err ? b->err : a->err;
+    r.error = (int)e;
+  }
+}
+
+// Two-warp replicas: warp 2k runs the prefill side, warp 2k+1 the decode side
+// of the same replica (shared-memory slice + hand-off channel), synchronised
+// by a named barrier per pair.
+__device__ __forceinline__ void pair_sync(int pair) {
+  asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory");
+}
+
+template <int KD>
+__global__ void __launch_bounds__(128) des_split_kernel(const DevPoint* __restrict__ pts, int n_pts,
+                                                        int* __restrict__ next_point,
+                                                        DevResult* __restrict__ res,
+                                                        int smem_per_pair) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ int s_pi[2];
+  const int warp = threadIdx.x >> 5, pair = warp >> 1, role = warp & 1, lane = lane_id();
+  unsigned char* my = smem + pair * smem_per_pair;
+  for (;;) {
+    if (role == 0 && lane == 0) s_pi[pair] = atomicAdd(next_point, 1);
+    pair_sync(pair);
+    const int pi = s_pi[pair];
+    if (pi >= n_pts) return;
+    const DevPoint& pt = pts[pi];
+    Chan* ch = (Chan*)(my + pt.sm_chan);
+    if (role == 0) chan_init(ch, lane);
+    if (role == 0 && lane == 0)
+      for (int i = 0; i < 24; ++i) res[pi].prof[i] = 0;
+    pair_sync(pair);
+    if (role == 0) run_replica<KD, false, 1, false>(pt, res[pi], my, my);
+    else run_replica<KD, false, 2, false>(pt, res[pi], my, my);
+    pair_sync(pair);
+    if (role == 0)
+      combine_pair(pt, res[pi], (const Counters*)(my + pt.sm_cnt), (const Counters*)(my + pt.sm_cnt2));
+    pair_sync(pair);
+  }
+}
+
+// Cluster pairs: the two warps of a replica sit in the two CTAs of a 2-CTA
+// cluster, CTA rank 0 holding W prefill warps and rank 1 their W decode
+// warps, one CTA per SM (the launch reserves enough shared memory), so each
+// SM runs one side's code only: the two sides' instruction working sets no
+// longer share an SM's instruction cache.  Every channel word is polled in
+// the reader's own shared memory and written remotely (DSMEM) by the other
+// side.  Replicas go round-robin over clusters, rounds separated by a
+// cluster barrier.
+template <int KD>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256)
+    des_cluster_kernel(const DevPoint* __restrict__ pts, int n_pts, int* __restrict__ unused,
+                       DevResult* __restrict__ res, int smem_per_rep) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = lane_id();
+  unsigned crank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  unsigned char* my = smem + warp * smem_per_rep;
+  // generic address of the same slice in the peer CTA
+  unsigned char* peer;
+  {
+    const unsigned long long mine = (unsigned long long)my;
+    unsigned long long rp;
+    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(rp) : "l"(mine), "r"(crank ^ 1u));
+    peer = (unsigned char*)rp;
+  }
+  for (int base = 0; base < n_pts; base += ncl * nw) {
+    const int pi = base + warp * ncl + cid;
+    const bool active = pi < n_pts;
+    if (active) chan_init((Chan*)(my + pts[pi].sm_chan), lane);
+    if (active && crank == 0 && lane == 0)
+      for (int i = 0; i < 24; ++i) res[pi].prof[i] = 0;
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (active) {
+      if (crank == 0) run_replica<KD, false, 1, true>(pts[pi], res[pi], my, peer);
+      else run_replica<KD, false, 2, true>(pts[pi], res[pi], my, peer);
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (active && crank == 0)
+      combine_pair(pts[pi], res[pi], (const Counters*)(my + pts[pi].sm_cnt),
+                   (const Counters*)(peer + pts[pi].sm_cnt2));
+    // the decode CTA's counters stay untouched until they are folded in
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
 }
 
@@ -1495,19 +1997,60 @@ __global__ void __launch_bounds__(256) finalize_kernel(const DevPoint* __restric
 // host-callable launchers (C++ linkage, used by sbs_host.cpp)
 // ---------------------------------------------------------------------------
 namespace sbs {
-// variant: bit 0 = dp_degree > 32 (KD 4), bit 1 = run records
+// variant: bit 0 = dp_degree > 32 (KD 4), bit 1 = run records, 4|5 = two-warp
+// replicas (smem_per_warp is then the per-pair slice, warps_per_block even)
 cudaError_t launch_des(int variant, const DevPoint* d_pts, int n_pts, int* d_counter,
                        DevResult* d_res, int smem_per_warp, int warps_per_block, int n_blocks,
                        cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(d_counter, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
-  size_t smem = (size_t)smem_per_warp * warps_per_block;
+  // one-warp variants: a slice per warp; two-warp variants: a slice per pair
+  size_t smem = (size_t)smem_per_warp * (variant >= 4 ? warps_per_block / 2 : warps_per_block);
   void (*k)(const DevPoint*, int, int*, DevResult*, int) =
       variant == 0 ? des_kernel<1, false> : variant == 1 ? des_kernel<4, false>
-    : variant == 2 ? des_kernel<1, true> : des_kernel<4, true>;
+    : variant == 2 ? des_kernel<1, true> : variant == 3 ? des_kernel<4, true>
+    : variant == 4 ? des_split_kernel<1> : des_split_kernel<4>;
   e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<n_blocks, 32 * warps_per_block, smem, st>>>(d_pts, n_pts, d_counter, d_res, smem_per_warp);
+  return cudaGetLastError();
+}
+
+// Two-warp replicas on 2-CTA clusters (variant 4|5 points).  Geometry: one
+// CTA per SM (reserved shared memory above half an SM's), as many clusters as
+// are co-resident, W replicas per cluster with W = ceil(n / clusters) <= 8.
+cudaError_t launch_des_cluster(int variant, const DevPoint* d_pts, int n_pts, DevResult* d_res,
+                               int smem_per_rep, cudaStream_t st) {
+  void (*k)(const DevPoint*, int, int*, DevResult*, int) =
+      variant == 4 ? des_cluster_kernel<1> : des_cluster_kernel<4>;
+  constexpr int kMaxSmem = 227 * 1024, kOnePerSm = 120 * 1024;
+  int wmax = 8;
+  while (wmax > 1 && wmax * smem_per_rep > kMaxSmem) --wmax;
+  if (smem_per_rep > kMaxSmem) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
+  if (e != cudaSuccess) return e;
+  static int max_clusters = 0;  // per process: one device kind
+  if (max_clusters == 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * 148, 1, 1);
+    cfg.blockDim = dim3(32 * wmax, 1, 1);
+    cfg.dynamicSmemBytes = kOnePerSm;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    e = cudaOccupancyMaxActiveClusters(&n, (void*)k, &cfg);
+    if (e != cudaSuccess) return e;
+    max_clusters = n > 0 ? n : 1;
+  }
+  int w = (n_pts + max_clusters - 1) / max_clusters;
+  w = w < 1 ? 1 : (w > wmax ? wmax : w);
+  const int ncl = (n_pts + w - 1) / w < max_clusters ? (n_pts + w - 1) / w : max_clusters;
+  size_t smem = (size_t)w * smem_per_rep;
+  if (smem < (size_t)kOnePerSm) smem = kOnePerSm;
+  k<<<2 * ncl, 32 * w, smem, st>>>(d_pts, n_pts, nullptr, d_res, smem_per_rep);
   return cudaGetLastError();
 }
 

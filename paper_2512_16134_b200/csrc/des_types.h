@@ -23,6 +23,37 @@ constexpr int kMaxPrefillDp = 128;  // 4 DP units per lane
 constexpr int kMaxWSize = 1024;     // exec-window ring in shared memory
 constexpr int kSmemWinKeys = 256;   // window keys kept in shared memory
 constexpr int kHistBins = 64;
+constexpr int kChanRecs = 32;       // prefill->decode hand-off records in flight
+constexpr int kChanKeys = 1024;     // hand-off waiter keys in flight
+constexpr int kChanComp = 256;      // decode completions returned to the prefill warp
+constexpr int kErrSplitTie = 7;     // two-warp replica met an unresolvable tie: rerun serially
+
+// Prefill-warp -> decode-warp hand-off channel of a two-warp replica (shared
+// memory).  One record per EndForward event: its time, the time its pass was
+// scheduled (= pass start), the prefill-warp index of the handler event that
+// scheduled it and of the EndForward event itself, and the decode-bound
+// requests it finished (waiter keys in a ring).
+struct ChanRec {
+  long long t, ts;
+  int ef_idx;    // prefill-warp event index of this EndForward
+  int h_idx;     // prefill-warp event index of the handler that scheduled it
+  int h_ext;     // that handler was an arrival/topology event (seq below internals)
+  int nk, k0, pad;
+};
+struct Chan {
+  volatile long long p_done;  // every prefill-warp event with time < p_done is processed
+  volatile int tail, head;    // records written / consumed
+  volatile int ktail, khead;  // keys written / consumed
+  volatile int abort;         // decode warp met an unresolvable tie
+  volatile int ctail, chead;  // decode completions written / accounted
+  volatile int d_done;        // decode warp finished (all completions published)
+  int n_ttft_p;               // prefill warp's TTFT appends
+  long long part[16];         // prefill warp's partial results
+  ChanRec rec[kChanRecs];
+  unsigned long long keys[kChanKeys];
+  long long comp_id[kChanComp];  // completion accounting is done by the prefill warp
+  long long comp_t[kChanComp];
+};
 
 enum Policy : int32_t { kSbs = 0, kImmediate = 1, kRoundRobin = 2, kLeastOutstanding = 3 };
 enum DecodePolicy : int32_t { kIqr = 0, kRandom = 1, kDecRoundRobin = 2 };
@@ -37,7 +68,7 @@ struct DevPoint {
   int32_t policy, decode_policy, n_limit, cap_batch;
   int32_t n_topo, n_drops, w_size;
   int32_t per_request;      // parity mode: also write completion + status
-  int32_t _pad0;
+  int32_t split;            // run as a prefill warp + decode warp pair
   // ---- constants (integer ns, FP64 engine coefficients)
   int64_t c_chunk, t_default, l_net, tps, horizon, warmup;
   double iqr_k, wd_mult, pf_base, pf_tok, dc_base, dc_req, dc_kv;
@@ -75,7 +106,7 @@ struct DevPoint {
   int32_t QP, QW, F, R, BC, QD;
   // ---- shared-memory carve (bytes, relative to the warp's slice)
   int32_t sm_pf_out, sm_pf_head, sm_pf_tail, sm_pf_rel, sm_pf_part;
-  int32_t sm_dPK, sm_dR, sm_dS, sm_dT, sm_dnst, sm_ulist, sm_bcnt, sm_hist, sm_wring, sm_wkeys, sm_cnt;
+  int32_t sm_dPK, sm_dR, sm_dS, sm_dT, sm_dnst, sm_ulist, sm_bcnt, sm_hist, sm_wring, sm_wkeys, sm_cnt, sm_cnt2, sm_chan;
   int32_t _pad2;
   int32_t sm_bytes;
   int32_t _pad1;
@@ -101,7 +132,7 @@ struct DevResult {
   int64_t ttft_sel[4];  // order statistics at ranks lo50, hi50, lo95, hi95
   int64_t ttft_hist[kHistBins];
   int64_t log_n;        // words written (== log_cap + 1 on overflow)
-  int64_t prof[16];     // SBS_PROF builds only: clock64 cycles per region
+  int64_t prof[24];     // SBS_PROF builds only: clock64 cycles per region
   int32_t error;
   int32_t _pad;
 };

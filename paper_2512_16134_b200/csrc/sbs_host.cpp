@@ -19,6 +19,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -34,6 +35,8 @@ namespace sbs {
 cudaError_t launch_des(int variant, const DevPoint* d_pts, int n_pts, int* d_counter,
                        DevResult* d_res, int smem_per_warp, int warps_per_block, int n_blocks,
                        cudaStream_t st);
+cudaError_t launch_des_cluster(int variant, const DevPoint* d_pts, int n_pts, DevResult* d_res,
+                               int smem_per_rep, cudaStream_t st);
 cudaError_t launch_finalize(const DevPoint* d_pts, int n_pts, DevResult* d_res, cudaStream_t st);
 struct PbaaArgs {
   int32_t n_windows;
@@ -283,6 +286,7 @@ struct PointHost {
   // capacities (grown on overflow)
   int32_t F = 0, QP = 0, QW = 0, BC = 0, QD = 0;
   int64_t LOG = 0;
+  int32_t split = 1;  // two-warp replica (cleared for an exact one-warp rerun)
   void* arena = nullptr;
   size_t arena_bytes = 0;
   void* fault_buf = nullptr;
@@ -300,7 +304,7 @@ struct sbs_sim {
   std::vector<PointHost> pts;
   std::vector<TraceDev> traces;
   std::vector<int> order;  // device slot -> point index (grouped by variant, cost-descending)
-  int group_begin[5] = {0, 0, 0, 0, 0};  // slots of kernel variant v: [group_begin[v], group_begin[v+1])
+  int group_begin[7] = {0, 0, 0, 0, 0, 0, 0};  // slots of kernel variant v: [group_begin[v], group_begin[v+1])
   sbs::DevPoint* d_pts = nullptr;
   sbs::DevResult* d_res = nullptr;
   int* d_counter = nullptr;
@@ -311,6 +315,7 @@ struct sbs_sim {
   int n_launches = 0;
   int64_t device_bytes = 0;
   int sm_count = 148;
+  int pair_mode = 2;  // two-warp replicas: 1 = one CTA, 2 = a 2-CTA cluster (SBS_SPLIT)
 };
 
 namespace {
@@ -347,6 +352,8 @@ void layout_smem(sbs::DevPoint& d) {
   d.sm_wring = take(8 * (size_t)d.w_size);
   d.sm_wkeys = take(8 * (size_t)sbs::kSmemWinKeys);
   d.sm_cnt = take(256);
+  d.sm_cnt2 = take(256);
+  d.sm_chan = take(sizeof(sbs::Chan));
   d.sm_bytes = (int32_t)off;
 }
 
@@ -367,6 +374,14 @@ void build_point(sbs_sim& s, PointHost& p) {
   d.cap_batch = c.decode_max_batch_per_dp;
   d.w_size = (int32_t)c.w_size;
   d.per_request = (s.flags & SBS_FLAG_PER_REQUEST) ? 1 : 0;
+  {
+    const char* e = std::getenv("SBS_SPLIT");
+    const bool allow = e == nullptr || std::atoi(e) != 0;
+    // the decode warp only pays off when the trace has decode work
+    // (completion-ring entries carry times in 48 bits)
+    d.split = (allow && p.split && !(s.flags & SBS_FLAG_LOGS) && t.max_output > 1 &&
+               seconds_to_ns(x.workload.duration_s) < (int64_t(1) << 47)) ? 1 : 0;
+  }
   d.c_chunk = c.c_chunk;
   d.t_default = seconds_to_ns(c.t_default_s);
   d.l_net = seconds_to_ns(c.l_net_s);
@@ -536,6 +551,7 @@ void grow_caps(PointHost& p) {
 }
 
 int variant_of(const PointHost& p) {
+  if (p.dp.split) return 4 | (p.dp.D > 32 ? 1 : 0);
   return (p.dp.D > 32 ? 1 : 0) | (p.dp.log != nullptr ? 2 : 0);
 }
 
@@ -548,19 +564,31 @@ void order_points(sbs_sim& s) {
     if (va != vb) return va < vb;
     return s.pts[a].cost > s.pts[b].cost;
   });
-  for (int v = 0; v <= 4; ++v) s.group_begin[v] = 0;
+  for (int v = 0; v <= 6; ++v) s.group_begin[v] = 0;
   for (int i = 0; i < n; ++i) s.group_begin[variant_of(s.pts[s.order[i]]) + 1] += 1;
-  for (int v = 1; v <= 4; ++v) s.group_begin[v] += s.group_begin[v - 1];
+  for (int v = 1; v <= 6; ++v) s.group_begin[v] += s.group_begin[v - 1];
 }
 
 void launch_all(sbs_sim& s, cudaStream_t st) {
   s.n_launches = 0;
-  for (int v = 0; v < 4; ++v) {
+  for (int v = 0; v < 6; ++v) {
     const int b = s.group_begin[v], e = s.group_begin[v + 1];
     if (e <= b) continue;
-    const int blocks = std::max(1, std::min(s.n_blocks, (e - b + s.warps_per_block - 1) / s.warps_per_block));
+    int wpb = s.warps_per_block, per_block = wpb;
+    if (v >= 4 && s.pair_mode == 2) {  // replica = a CTA pair of a 2-CTA cluster
+      CUDA_OR_THROW(sbs::launch_des_cluster(v, s.d_pts + b, e - b, s.d_res + b, s.smem_per_warp, st));
+      s.n_launches += 1;
+      continue;
+    }
+    if (v >= 4) {  // two warps per replica; at most two replicas per block
+      const int rpb = std::max(1, std::min(2, (e - b + s.sm_count - 1) / s.sm_count));
+      wpb = 2 * rpb;
+      per_block = rpb;
+      if ((size_t)rpb * s.smem_per_warp > 227 * 1024) { wpb = 2; per_block = 1; }
+    }
+    const int blocks = std::max(1, (e - b + per_block - 1) / per_block);
     CUDA_OR_THROW(sbs::launch_des(v, s.d_pts + b, e - b, s.d_counter + v, s.d_res + b,
-                                  s.smem_per_warp, s.warps_per_block, blocks, st));
+                                  s.smem_per_warp, wpb, blocks, st));
     s.n_launches += 1;
   }
   CUDA_OR_THROW(sbs::launch_finalize(s.d_pts, (int)s.order.size(), s.d_res, st));
@@ -748,6 +776,7 @@ int sbs_sim_create(const sbs_experiment* points, int32_t n_points, const sbs_tra
     s->flags = flags;
     CUDA_OR_THROW(cudaSetDevice(device));
     CUDA_OR_THROW(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, device));
+    if (const char* e = std::getenv("SBS_SPLIT")) s->pair_mode = std::atoi(e) == 1 ? 1 : 2;
     // traces
     s->traces.resize(n_traces);
     for (int i = 0; i < n_traces; ++i) {
@@ -783,7 +812,7 @@ int sbs_sim_create(const sbs_experiment* points, int32_t n_points, const sbs_tra
     order_points(*s);
     CUDA_OR_THROW(cudaMalloc(&s->d_pts, sizeof(sbs::DevPoint) * n_points));
     CUDA_OR_THROW(cudaMalloc(&s->d_res, sizeof(sbs::DevResult) * n_points));
-    CUDA_OR_THROW(cudaMalloc(&s->d_counter, 4 * sizeof(int)));
+    CUDA_OR_THROW(cudaMalloc(&s->d_counter, 8 * sizeof(int)));
     s->h_res.resize(n_points);
     upload_points(*s);
     return SBS_OK;
@@ -817,7 +846,7 @@ int sbs_sim_launch(sbs_sim* s, void* stream) {
 int32_t sbs_sim_launches_per_run(const sbs_sim* s) {
   // one des_kernel per variant group + finalize_kernel (memsets are not ours)
   int n = 1;
-  for (int v = 0; v < 4; ++v) n += s->group_begin[v + 1] > s->group_begin[v] ? 1 : 0;
+  for (int v = 0; v < 6; ++v) n += s->group_begin[v + 1] > s->group_begin[v] ? 1 : 0;
   return n;
 }
 
@@ -833,17 +862,29 @@ int sbs_sim_results(sbs_sim* s, sbs_aggregates* out, sbs_histograms* hist, void*
                                     cudaMemcpyDeviceToHost, st));
       CUDA_OR_THROW(cudaStreamSynchronize(st));
       bool overflow = false;
-      for (int i = 0; i < n; ++i)
-        if (s->h_res[i].error == SBS_ERR_OVERFLOW) {
-          overflow = true;
-          PointHost& p = s->pts[s->order[i]];
-          grow_caps(p);
-          s->device_bytes -= (int64_t)p.arena_bytes;
-          build_point(*s, p);
-          s->device_bytes += (int64_t)p.arena_bytes;
-        }
+      for (int i = 0; i < n; ++i) {
+        const int err = s->h_res[i].error;
+        if (err != SBS_ERR_OVERFLOW && err != sbs::kErrSplitTie) continue;
+        overflow = true;
+        PointHost& p = s->pts[s->order[i]];
+        if (err == SBS_ERR_OVERFLOW) grow_caps(p);
+        else p.split = 0;  // exact one-warp rerun of this replica
+        s->device_bytes -= (int64_t)p.arena_bytes;
+        build_point(*s, p);
+        s->device_bytes += (int64_t)p.arena_bytes;
+      }
       if (!overflow) break;
+      if (std::getenv("SBS_DEBUG")) {
+        int nt = 0, no = 0;
+        for (int i = 0; i < n; ++i) {
+          nt += s->h_res[i].error == sbs::kErrSplitTie;
+          no += s->h_res[i].error == SBS_ERR_OVERFLOW;
+        }
+        std::fprintf(stderr, "sbs: rerun attempt %d: %d split ties, %d overflows of %d\n", attempt, nt,
+                     no, n);
+      }
       if (attempt >= 12) throw Error{SBS_ERR_OVERFLOW, "device arena overflow persists"};
+      order_points(*s);
       upload_points(*s);
       for (auto& p : s->pts) reset_point(p, st);
       launch_all(*s, st);
@@ -907,10 +948,10 @@ int sbs_sim_log(sbs_sim* s, int32_t point, int64_t* words, int64_t cap, int64_t*
   });
 }
 
-int sbs_sim_profile_counters(const sbs_sim* s, int64_t* out16) {
-  for (int i = 0; i < 16; ++i) out16[i] = 0;
+int sbs_sim_profile_counters(const sbs_sim* s, int64_t* out) {
+  for (int i = 0; i < SBS_PROF_COUNTERS; ++i) out[i] = 0;
   for (const auto& r : s->h_res)
-    for (int i = 0; i < 16; ++i) out16[i] += r.prof[i];
+    for (int i = 0; i < SBS_PROF_COUNTERS; ++i) out[i] += r.prof[i];
   return SBS_OK;
 }
 

@@ -1,0 +1,54 @@
+"""GPU: two-warp replicas (a prefill warp and a decode warp per replica, see
+DESIGN.md "Two-warp replicas") give exactly the serial one-warp result:
+every per-request timestamp and every aggregate, including the non-reference
+extensions (TPOT sum, TTFT percentiles, histograms) whose FP64 sums depend on
+the lane that accumulated each request.  Mode 1: both warps in one CTA;
+mode 2: the two CTAs of a cluster (SBS_SPLIT)."""
+import copy
+
+import numpy as np
+import pytest
+
+import paper_2512_16134_b200 as P
+from tests.common import CASES
+
+pytestmark = pytest.mark.gpu
+COLS = ("dispatch", "prefill_start", "first_token", "completion", "status")
+
+
+def _run(cfg, split, monkeypatch):
+    monkeypatch.setenv("SBS_SPLIT", str(split))
+    return P.run_experiment(cfg, per_request=True)
+
+
+def _same(a, b, name):
+    for c in COLS:
+        assert np.array_equal(a["requests"][c], b["requests"][c]), f"{name}: {c}"
+    for k, v in a["agg"].items():
+        w = b["agg"][k]
+        if isinstance(v, np.ndarray):
+            assert np.array_equal(v, w), f"{name}: {k}"
+        elif isinstance(v, float) and np.isnan(v):
+            assert np.isnan(w), f"{name}: {k}"
+        else:
+            assert v == w, f"{name}: {k} {v!r} vs {w!r}"
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("name", ["decode_dp32", "cfg2_20s", "short_3k", "oracle_n8"])
+def test_split_equals_serial(name, mode, monkeypatch):
+    _same(_run(CASES[name], mode, monkeypatch), _run(CASES[name], 0, monkeypatch), name)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_split_equals_serial_random(mode, monkeypatch):
+    rng = np.random.default_rng(77)
+    for t in range(16):
+        c = copy.deepcopy(CASES[["decode_dp32", "cfg2_20s"][t % 2]])
+        c["workload"]["duration_s"] = float(rng.uniform(3, 20))
+        c["workload"]["rate_qps"] = float(c["workload"].get("rate_qps", 10) * rng.uniform(0.5, 2.5))
+        c["cluster"]["dp_degree"] = int(rng.choice([1, 4, 17, 64]))
+        c["cluster"]["l_net_s"] = float(rng.choice([0.0, 0.001, 0.02]))
+        c["scheduler"]["decode_policy"] = str(rng.choice(["iqr", "random", "round_robin"]))
+        c["sim"]["seed"] = int(rng.integers(0, 10**6))
+        _same(_run(c, mode, monkeypatch), _run(c, 0, monkeypatch), f"random#{t}")
