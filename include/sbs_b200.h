@@ -70,8 +70,11 @@ typedef struct sbs_cluster {
   double decode_per_request_s;
   double decode_per_kv_token_s;
   int64_t decode_tokens_per_step;
-  int32_t cache_enabled; /* cache-aware mode is out of scope: must be 0 */
-  int32_t _pad;
+  /* CacheSettings (core.h:230-234): the per-DP PrefixCache stub (core.h:87-123) */
+  int32_t cache_enabled;
+  int32_t cache_n_probes;
+  int64_t cache_budget_tokens;
+  const int64_t* cache_probe_lens; /* cache_n_probes entries, each >= 1 */
 } sbs_cluster;
 
 /* LengthSpec (workload.h:28-35) */
@@ -90,7 +93,7 @@ typedef struct sbs_workload {
   double duration_s;
   sbs_length_spec prompt;
   sbs_length_spec output;
-  double shared_prefix_fraction; /* must be 0 (prefix cache out of scope) */
+  double shared_prefix_fraction;
   int32_t prefix_pool;
   int32_t _pad;
   int64_t prefix_len;
@@ -119,13 +122,18 @@ typedef struct sbs_experiment {
 } sbs_experiment;
 
 /* A request trace in SoA form: the output of generate_workload
- * (workload.cpp:67-142), ids = positions.  16 B per request. */
+ * (workload.cpp:67-142), ids = positions.  16 B per request, plus 8 B when
+ * requests carry shared prefixes: Request::prefix_tokens (core.h:57-58) is
+ * the first prefix_size tokens of pool prefix_pool_id (workload.cpp:30-37,
+ * 129-138); -1 / 0 = no prefix.  Both NULL: no request has a prefix. */
 typedef struct sbs_trace {
   const int64_t* arrival_ns;
   const int32_t* prompt_len;
   const int32_t* output_len;
   int64_t n;
   uint64_t digest; /* workload_digest (workload.cpp:144-162) */
+  const int32_t* prefix_pool_id;
+  const int32_t* prefix_size;
 } sbs_trace;
 
 /* Aggregates (metrics.h:67-102), same field meaning, plus the sweep extras. */
@@ -163,10 +171,12 @@ typedef struct sbs_histograms {
 /* ----------------------------------------------------------------------- */
 /* Trace generation (host, multi-threaded).  Replaces generate_workload +   */
 /* workload_digest (workload.cpp:67-162); bit-identical on the same glibc.  */
-/* With arrays NULL only *n_out (and *digest) are produced.                 */
+/* With arrays NULL only *n_out (and *digest) are produced; the prefix     */
+/* arrays may be NULL on their own (then only lengths are written).         */
 int sbs_generate_workload(const sbs_workload* spec, uint64_t seed,
                           int64_t* arrival_ns, int32_t* prompt_len,
-                          int32_t* output_len, int64_t cap, int64_t* n_out,
+                          int32_t* output_len, int32_t* prefix_pool_id,
+                          int32_t* prefix_size, int64_t cap, int64_t* n_out,
                           uint64_t* digest);
 
 /* ----------------------------------------------------------------------- */
@@ -221,7 +231,7 @@ int sbs_run_experiments(const sbs_experiment* points, int32_t n_points,
 
 /* ----------------------------------------------------------------------- */
 /* Batched PBAA window allocation (allocate_batch, prefill_alloc.cpp:61-88, */
-/* Basic mode; greedy_dispatch :23-59).  One warp per cluster-window.       */
+/* greedy_dispatch :23-59).  One warp per cluster-window.                   */
 /* All pointers are DEVICE pointers; window w owns requests                 */
 /* [req_off[w], req_off[w+1]) of which the first n_pending[w] are q_pending */
 /* and the rest q_new (each in caller queue order), and DP capacities       */
@@ -229,6 +239,9 @@ int sbs_run_experiments(const sbs_experiment* points, int32_t n_points,
 /* Outputs per request: out_dp = DP index placed, -1 deferred, -2 throttled;*/
 /* out_rank = position in the placement order (-1 if not placed);           */
 /* wait_out = wait_cycles after the cycle.  flow[w] = flow-control flag.    */
+/* Cache-aware mode (capacity_after, prefill_alloc.cpp:12-21): hit != NULL  */
+/* gives Len_hit(r, d) of every (request, DP) pair of window w, row-major   */
+/* from hit[hit_off[w]] (request-major, n_dp per row); NULL = Basic mode.   */
 typedef struct sbs_window_batch {
   int32_t n_windows;
   int32_t _pad;
@@ -244,6 +257,8 @@ typedef struct sbs_window_batch {
   int32_t* out_rank;
   int32_t* wait_out;
   uint8_t* flow;
+  const int64_t* hit_off;
+  const int64_t* hit;
 } sbs_window_batch;
 int sbs_prefill_allocate(const sbs_window_batch* batch, void* stream);
 /* Asynchronous form: enqueue only.  `error_out` is a DEVICE int32 the caller

@@ -24,6 +24,9 @@ def lib():
         L = C.CDLL(str(LIB_PATH))
         L.orc_allocate_batch.argtypes = [_i64p, C.c_int64, _i64p, C.c_int64, _i64p, C.c_int64,
                                          C.c_int, _i64p, _i64p, _i64p, _i64p]
+        L.orc_allocate_batch_hits.argtypes = [_i64p, C.c_int64, _i64p, C.c_int64, _i64p,
+                                              C.c_int64, C.c_int, _i64p, _i64p, _i64p, _i64p,
+                                              _i64p]
         L.orc_percentile.argtypes = [C.POINTER(C.c_double), C.c_int64, C.c_double]
         L.orc_percentile.restype = C.c_double
         L.orc_outlier_threshold.argtypes = [_i64p, C.c_int64, C.c_double]
@@ -41,7 +44,8 @@ def _p(a):
     return a.ctypes.data_as(_i64p)
 
 
-def allocate_batch(pending, fresh, caps, n_limit):
+def allocate_batch(pending, fresh, caps, n_limit, hits=None):
+    """hits (optional, rows pending-then-new x DP): cache-aware Len_hit."""
     L = lib()
     pending = np.ascontiguousarray(pending, np.int64).reshape(-1, 3)
     fresh = np.ascontiguousarray(fresh, np.int64).reshape(-1, 3)
@@ -49,8 +53,12 @@ def allocate_batch(pending, fresh, caps, n_limit):
     n = max(len(pending) + len(fresh), 1)
     om, od, ot = np.zeros((n, 2), np.int64), np.zeros((n, 2), np.int64), np.zeros(n, np.int64)
     cnt = np.zeros(3, np.int64)
-    flow = L.orc_allocate_batch(_p(pending), len(pending), _p(fresh), len(fresh), _p(caps),
-                                len(caps), int(n_limit), _p(om), _p(od), _p(ot), _p(cnt))
+    h = None
+    if hits is not None:
+        h = np.ascontiguousarray(hits, np.int64).reshape(len(pending) + len(fresh), len(caps))
+    flow = L.orc_allocate_batch_hits(_p(pending), len(pending), _p(fresh), len(fresh), _p(caps),
+                                     len(caps), int(n_limit), _p(h) if h is not None else None,
+                                     _p(om), _p(od), _p(ot), _p(cnt))
     return {"mapping": om[: cnt[0]].copy(), "deferred": od[: cnt[1]].copy(),
             "throttled": ot[: cnt[2]].copy(), "caps": caps, "flow": bool(flow)}
 
@@ -123,7 +131,10 @@ class OrcConfig(C.Structure):
                 ("policy", C.c_int), ("decode_policy", C.c_int), ("seed", C.c_uint64),
                 ("duration_s", C.c_double), ("warmup_fraction", C.c_double),
                 ("drops", C.POINTER(_Drop)), ("n_drops", C.c_int), ("deads", C.POINTER(_Dead)),
-                ("n_deads", C.c_int), ("topology", C.POINTER(_Topo)), ("n_topology", C.c_int)]
+                ("n_deads", C.c_int), ("topology", C.POINTER(_Topo)), ("n_topology", C.c_int),
+                ("prefill_mode", C.c_int), ("cache_enabled", C.c_int),
+                ("cache_budget_tokens", C.c_int64), ("cache_probe_lens", C.c_void_p),
+                ("n_probe_lens", C.c_int)]
 
 
 class OrcResult(C.Structure):
@@ -169,8 +180,17 @@ def _config(cfg):
         policy={"sbs": 0, "immediate": 1, "round_robin": 1, "least_outstanding": 3}[s.get("policy", "sbs")],
         decode_policy={"iqr": 0, "random": 1, "round_robin": 2}[s.get("decode_policy", "iqr")],
         seed=sim.get("seed", 1), duration_s=w.get("duration_s", 1.0),
-        warmup_fraction=sim.get("warmup_fraction", 0.1))
+        warmup_fraction=sim.get("warmup_fraction", 0.1),
+        prefill_mode=1 if s.get("prefill_mode", "basic") == "cache_aware" else 0)
     keep = []
+    cc = c.get("cache", {})
+    if cc.get("enabled", False):
+        oc.cache_enabled = 1
+        oc.cache_budget_tokens = cc.get("budget_tokens", 0)
+        pl = (C.c_int64 * max(len(cc.get("probe_lens", [])), 1))(*cc.get("probe_lens", []))
+        keep.append(pl)
+        oc.cache_probe_lens = C.cast(pl, C.c_void_p)
+        oc.n_probe_lens = len(cc.get("probe_lens", []))
     d = [_Drop(x.get("instance", -1), x.get("from_s", 0.0), x.get("until_s", float("inf")))
          for x in f.get("drop_end_forward", [])]
     dd = [_Dead(x.get("instance", 0), x.get("time_s", 0.0)) for x in f.get("dead", [])]
@@ -188,12 +208,14 @@ def _config(cfg):
     return oc, keep
 
 
-def run(cfg, arrival, prompt, output, per_request=True):
-    """Run the C restatement on a given trace (e.g. the reference's own)."""
+def run(cfg, arrival, prompt, output, per_request=True, prefix_pool=None, prefix_size=None):
+    """Run the C restatement on a given trace (e.g. the reference's own);
+    prefix_pool/prefix_size: the requests' shared prefixes (None: none)."""
     L = lib()
     if not hasattr(L, "_orc_run_bound"):
-        L.orc_run.argtypes = [C.POINTER(OrcConfig), C.c_void_p, C.c_void_p, C.c_void_p,
-                              C.c_int64, C.POINTER(OrcResult), C.c_void_p]
+        L.orc_run_prefix.argtypes = [C.POINTER(OrcConfig), C.c_void_p, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(OrcResult),
+                                     C.c_void_p]
         L._orc_run_bound = True
     oc, keep = _config(cfg)
     a = np.ascontiguousarray(arrival, np.int64)
@@ -201,8 +223,14 @@ def run(cfg, arrival, prompt, output, per_request=True):
     o = np.ascontiguousarray(output, np.int32)
     res = OrcResult()
     pr = np.zeros((max(len(a), 1), 5), np.int64) if per_request else None
-    L.orc_run(C.byref(oc), a.ctypes.data, p.ctypes.data, o.ctypes.data, len(a), C.byref(res),
-              pr.ctypes.data if per_request else None)
+    pp = ps = None
+    if prefix_pool is not None:
+        pp = np.ascontiguousarray(prefix_pool, np.int32)
+        ps = np.ascontiguousarray(prefix_size, np.int32)
+    L.orc_run_prefix(C.byref(oc), a.ctypes.data, p.ctypes.data, o.ctypes.data,
+                     pp.ctypes.data if pp is not None else None,
+                     ps.ctypes.data if ps is not None else None, len(a), C.byref(res),
+                     pr.ctypes.data if per_request else None)
     out = {"agg": {k: getattr(res, k) for k, _ in OrcResult._fields_}}
     if per_request:
         out["requests"] = pr[: len(a)]

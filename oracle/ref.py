@@ -61,6 +61,9 @@ def lib():
         L.ref_generate_workload.argtypes = [C.c_char_p, _i64p, C.c_int64, _i64p]
         L.ref_allocate_batch.argtypes = [_i64p, C.c_int64, _i64p, C.c_int64, _i64p,
                                          C.c_int64, C.c_int, _i64p, _i64p, _i64p, _i64p]
+        L.ref_allocate_batch_ca.argtypes = [_i64p, C.c_int64, _i64p, C.c_int64, _i64p,
+                                            C.c_int64, C.c_int, _i64p, _i64p, _i64p, _i64p,
+                                            _i64p]
         L.ref_select_decode_unit.argtypes = [_i64p, _i64p, C.c_int64, C.c_double,
                                              C.POINTER(C.c_int), _f64p]
         L.ref_percentile.argtypes = [_f64p, C.c_int64, C.c_double]
@@ -135,8 +138,9 @@ def generate_workload(cfg: dict):
     return buf[:n, 0].copy(), buf[:n, 1].copy(), buf[:n, 2].copy(), int(m[1]) & (2**64 - 1)
 
 
-def allocate_batch(pending, fresh, caps, n_limit):
-    """pending/fresh: int64 arrays (k,3) of (id, prompt_len, wait_cycles)."""
+def allocate_batch(pending, fresh, caps, n_limit, hits=None):
+    """pending/fresh: int64 arrays (k,3) of (id, prompt_len, wait_cycles);
+    hits (optional, (k_pending + k_new, D)): cache-aware mode with these Len_hit."""
     L = lib()
     pending = np.ascontiguousarray(pending, np.int64).reshape(-1, 3)
     fresh = np.ascontiguousarray(fresh, np.int64).reshape(-1, 3)
@@ -146,8 +150,14 @@ def allocate_batch(pending, fresh, caps, n_limit):
     od = np.zeros((max(n, 1), 2), np.int64)
     ot = np.zeros(max(n, 1), np.int64)
     cnt = np.zeros(3, np.int64)
-    flow = L.ref_allocate_batch(_p(pending), len(pending), _p(fresh), len(fresh), _p(caps),
-                                len(caps), int(n_limit), _p(om), _p(od), _p(ot), _p(cnt))
+    if hits is None:
+        flow = L.ref_allocate_batch(_p(pending), len(pending), _p(fresh), len(fresh), _p(caps),
+                                    len(caps), int(n_limit), _p(om), _p(od), _p(ot), _p(cnt))
+    else:
+        h = np.ascontiguousarray(hits, np.int64).reshape(n, len(caps))
+        flow = L.ref_allocate_batch_ca(_p(pending), len(pending), _p(fresh), len(fresh),
+                                       _p(caps), len(caps), int(n_limit), _p(h), _p(om), _p(od),
+                                       _p(ot), _p(cnt))
     return {"mapping": om[: cnt[0]].copy(), "deferred": od[: cnt[1]].copy(),
             "throttled": ot[: cnt[2]].copy(), "caps": caps, "flow": bool(flow)}
 

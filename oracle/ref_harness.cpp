@@ -327,6 +327,74 @@ int ref_allocate_batch(const std::int64_t* pend, std::int64_t n_pend,
   return res.flow_control ? 1 : 0;
 }
 
+// allocate_batch in cache-aware mode with a given Len_hit(r, d) matrix
+// (hits: row-major n x n_dp, rows in pending-then-new order).  The hits are
+// realised through the reference's own PrefixCache: request r gets unique
+// prefix tokens of length max_d hit(r, d); DP d's cache holds r's prefix cut to
+// hit(r, d); the probe set is every distinct positive hit; the budget never
+// evicts.  Requires hit(r, d) <= prompt_len(r).  Outputs as ref_allocate_batch.
+int ref_allocate_batch_ca(const std::int64_t* pend, std::int64_t n_pend,
+                          const std::int64_t* fresh, std::int64_t n_fresh,
+                          std::int64_t* caps, std::int64_t n_dp, int n_limit,
+                          const std::int64_t* hits, std::int64_t* out_map,
+                          std::int64_t* out_def, std::int64_t* out_thr,
+                          std::int64_t* counts) {
+  const std::int64_t n = n_pend + n_fresh;
+  std::vector<Request> storage(static_cast<std::size_t>(n));
+  std::vector<Request*> pv, nv;
+  std::vector<Tokens> probes;
+  for (std::int64_t i = 0; i < n * n_dp; ++i)
+    if (hits[i] > 0) probes.push_back(hits[i]);
+  std::sort(probes.begin(), probes.end());
+  probes.erase(std::unique(probes.begin(), probes.end()), probes.end());
+  for (std::int64_t i = 0; i < n; ++i) {
+    const std::int64_t* row = i < n_pend ? pend + 3 * i : fresh + 3 * (i - n_pend);
+    Request& r = storage[static_cast<std::size_t>(i)];
+    r.id = static_cast<std::uint64_t>(row[0]);
+    r.prompt_len = row[1];
+    r.wait_cycles = static_cast<int>(row[2]);
+    Tokens mx = 0;
+    for (std::int64_t d = 0; d < n_dp; ++d) mx = std::max<Tokens>(mx, hits[i * n_dp + d]);
+    for (Tokens t = 0; t < mx; ++t)
+      r.prefix_tokens.push_back(static_cast<std::int32_t>((i * 1000003 + t * 7919 + 1) & 0x7fffffff));
+    (i < n_pend ? pv : nv).push_back(&r);
+  }
+  std::vector<PrefixCache> cache;
+  for (std::int64_t d = 0; d < n_dp; ++d) cache.emplace_back(probes, Tokens(1) << 60);
+  for (std::int64_t i = 0; i < n; ++i)
+    for (std::int64_t d = 0; d < n_dp; ++d) {
+      const Tokens h = hits[i * n_dp + d];
+      if (h <= 0) continue;
+      const Request& r = storage[static_cast<std::size_t>(i)];
+      std::vector<std::int32_t> cut(r.prefix_tokens.begin(), r.prefix_tokens.begin() + h);
+      cache[static_cast<std::size_t>(d)].insert(cut, h);
+    }
+  std::vector<DpPlan> dps(static_cast<std::size_t>(n_dp));
+  for (std::int64_t d = 0; d < n_dp; ++d) {
+    dps[static_cast<std::size_t>(d)].dp_index = static_cast<int>(d);
+    dps[static_cast<std::size_t>(d)].c_avail = caps[d];
+    dps[static_cast<std::size_t>(d)].cache = &cache[static_cast<std::size_t>(d)];
+  }
+  AllocationResult res = ref_impl_allocate_batch(
+      {pv.data(), pv.size()}, {nv.data(), nv.size()}, dps, n_limit,
+      AllocMode::kCacheAware);
+  for (std::size_t i = 0; i < res.mapping.size(); ++i) {
+    out_map[2 * i] = static_cast<std::int64_t>(res.mapping[i].first->id);
+    out_map[2 * i + 1] = res.mapping[i].second;
+  }
+  for (std::size_t i = 0; i < res.deferred.size(); ++i) {
+    out_def[2 * i] = static_cast<std::int64_t>(res.deferred[i]->id);
+    out_def[2 * i + 1] = res.deferred[i]->wait_cycles;
+  }
+  for (std::size_t i = 0; i < res.throttled.size(); ++i)
+    out_thr[i] = static_cast<std::int64_t>(res.throttled[i]->id);
+  counts[0] = static_cast<std::int64_t>(res.mapping.size());
+  counts[1] = static_cast<std::int64_t>(res.deferred.size());
+  counts[2] = static_cast<std::int64_t>(res.throttled.size());
+  for (std::int64_t d = 0; d < n_dp; ++d) caps[d] = dps[static_cast<std::size_t>(d)].c_avail;
+  return res.flow_control ? 1 : 0;
+}
+
 // select_decode_unit (decode_alloc.cpp:38-81) on (B, K) arrays.
 int ref_select_decode_unit(const std::int64_t* batch, const std::int64_t* kv,
                            std::int64_t n, double k, int* fallback,

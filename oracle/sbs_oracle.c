@@ -18,7 +18,8 @@
 
 typedef struct {
   int64_t id, len, wait;
-  int64_t pos; /* input position */
+  int64_t pos;        /* input position */
+  const int64_t* hit; /* cache-aware: Len_hit per DP unit, NULL = Basic */
 } orc_req;
 
 static int cmp_len_desc_id_asc(const void* a, const void* b) {
@@ -30,8 +31,9 @@ static int cmp_len_desc_id_asc(const void* a, const void* b) {
 }
 
 /* greedy_dispatch (prefill_alloc.cpp:23-59): longest first; argmax of
- * capacity_after = c_avail - prompt_len (strict >, lowest index); guard on the
- * chosen unit's pre-assignment c_avail > 0; deferred keep input order. */
+ * capacity_after = c_avail - (prompt_len - hit) (strict >, lowest index;
+ * prefill_alloc.cpp:12-21, hit = 0 in Basic mode); guard on the chosen unit's
+ * pre-assignment c_avail > 0; deferred keep input order. */
 static void greedy(orc_req* q, int64_t n, int64_t* caps, int64_t n_dp, int64_t* out_map,
                    int64_t* n_map, orc_req* deferred, int64_t* n_def) {
   orc_req* order = (orc_req*)malloc(sizeof(orc_req) * (size_t)(n > 0 ? n : 1));
@@ -43,7 +45,7 @@ static void greedy(orc_req* q, int64_t n, int64_t* caps, int64_t n_dp, int64_t* 
     const orc_req* r = &order[t];
     int64_t best = -1, best_after = 0;
     for (int64_t d = 0; d < n_dp; ++d) {
-      int64_t after = caps[d] - r->len;
+      int64_t after = caps[d] - (r->len - (r->hit ? r->hit[d] : 0));
       if (best < 0 || after > best_after) {
         best = d;
         best_after = after;
@@ -67,6 +69,14 @@ int orc_allocate_batch(const int64_t* pend, int64_t n_pend, const int64_t* fresh
                        int64_t n_fresh, int64_t* caps, int64_t n_dp, int n_limit,
                        int64_t* out_map, int64_t* out_def, int64_t* out_thr,
                        int64_t* counts) {
+  return orc_allocate_batch_hits(pend, n_pend, fresh, n_fresh, caps, n_dp, n_limit, NULL,
+                                 out_map, out_def, out_thr, counts);
+}
+
+int orc_allocate_batch_hits(const int64_t* pend, int64_t n_pend, const int64_t* fresh,
+                            int64_t n_fresh, int64_t* caps, int64_t n_dp, int n_limit,
+                            const int64_t* hits, int64_t* out_map, int64_t* out_def,
+                            int64_t* out_thr, int64_t* counts) {
   int64_t n = n_pend + n_fresh;
   orc_req* qp = (orc_req*)malloc(sizeof(orc_req) * (size_t)(n_pend > 0 ? n_pend : 1));
   orc_req* qn = (orc_req*)malloc(sizeof(orc_req) * (size_t)(n_fresh > 0 ? n_fresh : 1));
@@ -74,9 +84,11 @@ int orc_allocate_batch(const int64_t* pend, int64_t n_pend, const int64_t* fresh
   orc_req* dn = (orc_req*)malloc(sizeof(orc_req) * (size_t)(n > 0 ? n : 1));
   for (int64_t i = 0; i < n_pend; ++i) {
     qp[i].id = pend[3 * i]; qp[i].len = pend[3 * i + 1]; qp[i].wait = pend[3 * i + 2];
+    qp[i].hit = hits ? hits + i * n_dp : NULL;
   }
   for (int64_t i = 0; i < n_fresh; ++i) {
     qn[i].id = fresh[3 * i]; qn[i].len = fresh[3 * i + 1]; qn[i].wait = fresh[3 * i + 2];
+    qn[i].hit = hits ? hits + (n_pend + i) * n_dp : NULL;
   }
   int64_t n_map = 0, n_dp_def = 0, n_new_def = 0, n_d = 0, n_t = 0;
   greedy(qp, n_pend, caps, n_dp, out_map, &n_map, dp, &n_dp_def);

@@ -15,6 +15,14 @@ int orc_allocate_batch(const int64_t* pend, int64_t n_pend, const int64_t* fresh
                        int64_t* out_map, int64_t* out_def, int64_t* out_thr,
                        int64_t* counts);
 
+/* allocate_batch in cache-aware mode: hits (nullable) rows of Len_hit(r, d),
+ * n_dp per row, rows in pend-then-fresh order (capacity_after,
+ * prefill_alloc.cpp:12-21). */
+int orc_allocate_batch_hits(const int64_t* pend, int64_t n_pend, const int64_t* fresh,
+                            int64_t n_fresh, int64_t* caps, int64_t n_dp, int n_limit,
+                            const int64_t* hits, int64_t* out_map, int64_t* out_def,
+                            int64_t* out_thr, int64_t* counts);
+
 /* percentile (decode_alloc.cpp:13-23): p clamped to [0,100]; n >= 1. */
 double orc_percentile(const double* values, int64_t n, double p);
 
@@ -60,6 +68,12 @@ typedef struct {
   int n_deads;
   const orc_topo* topology;
   int n_topology;
+  /* cache-aware PBAA (simulation.cpp:267-268) + CacheSettings (core.h:230-234) */
+  int prefill_mode; /* 0 basic, 1 cache_aware */
+  int cache_enabled;
+  int64_t cache_budget_tokens;
+  const int64_t* cache_probe_lens;
+  int n_probe_lens;
 } orc_config;
 
 /* Aggregates (metrics.h:67-102) + counters */
@@ -83,5 +97,11 @@ typedef struct {
  * completion), -1 when unset.  Returns 0 or 3 (invariant). */
 int orc_run(const orc_config* cfg, const int64_t* arr, const int32_t* prompt,
             const int32_t* output, int64_t n, orc_result* res, int64_t* per_req);
+/* The same with shared prefixes: request r's prefix_tokens are the first
+ * pfx_size[r] tokens of pool pfx_pool[r] (workload.cpp:30-37, 129-138);
+ * both nullable. */
+int orc_run_prefix(const orc_config* cfg, const int64_t* arr, const int32_t* prompt,
+                   const int32_t* output, const int32_t* pfx_pool, const int32_t* pfx_size,
+                   int64_t n, orc_result* res, int64_t* per_req);
 
 #endif

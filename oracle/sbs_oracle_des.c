@@ -96,9 +96,18 @@ static void dq_push(deq_t* d, int64_t id, int64_t tok, char bl) {
 }
 #define DQ(d, k) (((d)->head + (k)) % (d)->cap)
 
+/* PrefixCache (core.h:87-123, core.cpp:13-75): LRU list of (hash, k), entry 0
+ * is the front (most recent); linear lookups (test sizes are small). */
+typedef struct {
+  uint64_t* key;
+  int64_t* k;
+  int64_t n, cap, used;
+} pcache_t;
+
 typedef struct {
   int64_t u_flight, r_queued;
   deq_t pending;
+  pcache_t cache;
   int64_t batch, kv;
   vec_t residents;
   vec_t pass_id, pass_tok; /* pass_content (core.h:178) */
@@ -137,6 +146,76 @@ static uint64_t mt_next(mt64_t* m) {
   return y;
 }
 
+/* ---------------- prefix cache ---------------- */
+static int32_t prefix_token(int pool, int64_t i) { /* workload.cpp:30-37 */
+  uint64_t h = 1469598103934665603ull;
+  h ^= (uint64_t)pool * 0x9e3779b97f4a7c15ull;
+  h ^= (uint64_t)i + 0x632be59bd9b4e019ull;
+  h *= 1099511628211ull;
+  return (int32_t)(h & 0x7fffffff);
+}
+static uint64_t hash_prefix(int pool, int64_t k) { /* core.cpp:18-31 */
+  uint64_t h = 14695981039346656037ull ^ (uint64_t)k;
+  for (int64_t i = 0; i < k; ++i) {
+    uint32_t v = (uint32_t)prefix_token(pool, i);
+    for (int b = 0; b < 4; ++b) {
+      h ^= (v >> (8 * b)) & 0xff;
+      h *= 1099511628211ull;
+    }
+  }
+  return h;
+}
+static int64_t pc_find(const pcache_t* c, uint64_t key) {
+  for (int64_t i = 0; i < c->n; ++i)
+    if (c->key[i] == key) return i;
+  return -1;
+}
+static void pc_to_front(pcache_t* c, int64_t i) { /* touch: splice to begin */
+  uint64_t key = c->key[i];
+  int64_t k = c->k[i];
+  memmove(c->key + 1, c->key, sizeof(uint64_t) * (size_t)i);
+  memmove(c->k + 1, c->k, sizeof(int64_t) * (size_t)i);
+  c->key[0] = key;
+  c->k[0] = k;
+}
+/* longest_hit (core.cpp:33-41); probes ascending */
+static int64_t pc_longest_hit(const pcache_t* c, const int64_t* probes, int np, int pool,
+                              int64_t psize, int64_t prompt) {
+  int64_t best = 0;
+  for (int j = 0; j < np; ++j) {
+    int64_t k = probes[j];
+    if (k > prompt || k > psize) break;
+    if (pc_find(c, hash_prefix(pool, k)) >= 0) best = k;
+  }
+  return best;
+}
+/* insert + evict_to_budget (core.cpp:43-75) */
+static void pc_insert(pcache_t* c, const int64_t* probes, int np, int64_t budget, int pool,
+                      int64_t psize, int64_t prompt) {
+  if (budget <= 0) return;
+  for (int j = 0; j < np; ++j) {
+    int64_t k = probes[j];
+    if (k > prompt || k > psize) break;
+    uint64_t key = hash_prefix(pool, k);
+    int64_t at = pc_find(c, key);
+    if (at >= 0) { pc_to_front(c, at); continue; }
+    if (c->n == c->cap) {
+      c->cap = c->cap ? 2 * c->cap : 16;
+      c->key = (uint64_t*)realloc(c->key, sizeof(uint64_t) * (size_t)c->cap);
+      c->k = (int64_t*)realloc(c->k, sizeof(int64_t) * (size_t)c->cap);
+    }
+    c->key[c->n] = key;
+    c->k[c->n] = k;
+    c->n += 1;
+    pc_to_front(c, c->n - 1);
+    c->used += k;
+  }
+  while (c->used > budget && c->n > 0) { /* pop_back */
+    c->n -= 1;
+    c->used -= c->k[c->n];
+  }
+}
+
 /* ---------------- runner ---------------- */
 typedef struct {
   const orc_config* cfg;
@@ -144,6 +223,10 @@ typedef struct {
   const int64_t* arr;
   const int32_t* prompt;
   const int32_t* output;
+  const int32_t* pfx_pool; /* nullable */
+  const int32_t* pfx_size;
+  int64_t* probes;         /* cache.probe_lens sorted (core.cpp:15) */
+  int n_probes, cache_aware;
   int8_t* status;
   int* wait;
   int64_t *disp, *pstart, *ftok, *comp, *ctot, *cdone, *ddone;
@@ -366,7 +449,21 @@ static void perform_dispatch(run_t* R, int i) { /* simulation.cpp:265-342 */
   int64_t n = np + nn + 1;
   int64_t *om = (int64_t*)malloc(sizeof(int64_t) * 2 * (size_t)n), *od = (int64_t*)malloc(sizeof(int64_t) * 2 * (size_t)n),
           *ot = (int64_t*)malloc(sizeof(int64_t) * (size_t)n), cnt[3];
-  int flow = orc_allocate_batch(rows, np, rows + 3 * np, nn, caps, D, R->cfg->n_limit, om, od, ot, cnt);
+  /* cache-aware: Len_hit of every (request, DP) against the pre-dispatch
+   * caches, used by the allocation and by the effective lengths below */
+  int64_t* hits = NULL;
+  if (R->cache_aware) {
+    hits = (int64_t*)calloc((size_t)(n * D), sizeof(int64_t));
+    for (int64_t k = 0; k < np + nn; ++k) {
+      int64_t id = rows[3 * k];
+      if (!R->pfx_pool || R->pfx_size[id] <= 0) continue;
+      for (int d = 0; d < D; ++d)
+        hits[k * D + d] = pc_longest_hit(&I->dp[d].cache, R->probes, R->n_probes, R->pfx_pool[id],
+                                         R->pfx_size[id], R->prompt[id]);
+    }
+  }
+  int flow = orc_allocate_batch_hits(rows, np, rows + 3 * np, nn, caps, D, R->cfg->n_limit, hits,
+                                     om, od, ot, cnt);
   R->res->alloc_calls += 1;
   R->res->deferrals += (uint64_t)cnt[1];
   if (flow) R->res->flow_control_events += 1;
@@ -379,11 +476,19 @@ static void perform_dispatch(run_t* R, int i) { /* simulation.cpp:265-342 */
   } else {
     for (int64_t k = 0; k < cnt[0]; ++k) {
       int64_t id = om[2 * k];
-      int64_t eff = R->prompt[id] > 1 ? R->prompt[id] : 1;
+      int dsel = (int)om[2 * k + 1];
+      int64_t hit = 0;
+      if (hits)
+        for (int64_t r = 0; r < np + nn; ++r)
+          if (rows[3 * r] == id) { hit = hits[r * D + dsel]; break; }
+      int64_t eff = R->prompt[id] - hit > 1 ? R->prompt[id] - hit : 1;
       R->status[id] = ST_DISPATCHED;
       R->disp[id] = R->clk.now;
       R->ctot[id] = eff;
-      dispatch_prefill(R, i, (int)om[2 * k + 1], id, eff);
+      dispatch_prefill(R, i, dsel, id, eff);
+      if (R->cache_aware && R->pfx_pool && R->pfx_size[id] > 0)
+        pc_insert(&I->dp[dsel].cache, R->probes, R->n_probes, R->cfg->cache_budget_tokens,
+                  R->pfx_pool[id], R->pfx_size[id], R->prompt[id]);
     }
     R->has_last = 1;
     R->last_dispatch = R->clk.now;
@@ -400,7 +505,7 @@ static void perform_dispatch(run_t* R, int i) { /* simulation.cpp:265-342 */
     try_start_pass(R, i);
     if (R->q_pending.n > 0) arm_tick(R, R->clk.now + R->i_opt);
   }
-  free(rows); free(caps); free(om); free(od); free(ot);
+  free(rows); free(caps); free(om); free(od); free(ot); free(hits);
 }
 
 static int ready(run_t* R, int i) { /* interval_control.cpp:43-48 */
@@ -554,12 +659,33 @@ static int cmp_f64(const void* a, const void* b) {
   return (x > y) - (x < y);
 }
 
+static int cmp_i64(const void* a, const void* b) {
+  int64_t x = *(const int64_t*)a, y = *(const int64_t*)b;
+  return (x > y) - (x < y);
+}
+
 int orc_run(const orc_config* cfg, const int64_t* arr, const int32_t* prompt,
             const int32_t* output, int64_t n, orc_result* res, int64_t* per_req) {
+  return orc_run_prefix(cfg, arr, prompt, output, NULL, NULL, n, res, per_req);
+}
+
+int orc_run_prefix(const orc_config* cfg, const int64_t* arr, const int32_t* prompt,
+                   const int32_t* output, const int32_t* pfx_pool, const int32_t* pfx_size,
+                   int64_t n, orc_result* res, int64_t* per_req) {
   run_t R;
   memset(&R, 0, sizeof(R));
   memset(res, 0, sizeof(*res));
   R.cfg = cfg; R.n = n; R.arr = arr; R.prompt = prompt; R.output = output; R.res = res;
+  R.pfx_pool = pfx_pool;
+  R.pfx_size = pfx_size;
+  /* simulation.cpp:267-268 */
+  R.cache_aware = cfg->prefill_mode == 1 && cfg->cache_enabled;
+  if (R.cache_aware) {
+    R.n_probes = cfg->n_probe_lens;
+    R.probes = (int64_t*)malloc(sizeof(int64_t) * (size_t)(R.n_probes + 1));
+    memcpy(R.probes, cfg->cache_probe_lens, sizeof(int64_t) * (size_t)R.n_probes);
+    qsort(R.probes, (size_t)R.n_probes, sizeof(int64_t), cmp_i64);
+  }
   R.P = cfg->n_instances_prefill;
   R.Dn = cfg->n_instances_decode;
   R.n_inst = R.P + R.Dn;
@@ -698,11 +824,13 @@ int orc_run(const orc_config* cfg, const int64_t* arr, const int32_t* prompt,
       dp_t* D = &R.inst[i].dp[d];
       free(D->pending.id); free(D->pending.tok); free(D->pending.bl);
       free(D->residents.v); free(D->pass_id.v); free(D->pass_tok.v);
+      free(D->cache.key); free(D->cache.k);
     }
     free(R.inst[i].dp);
   }
   free(R.inst); free(R.status); free(R.wait); free(R.disp); free(R.pstart); free(R.ftok);
   free(R.comp); free(R.ctot); free(R.cdone); free(R.ddone); free(R.mark); free(R.win);
+  free(R.probes);
   free(R.rr_dp); free(R.clk.v); free(R.q_pending.v); free(R.q_new.v); free(R.decode_wait.v);
   (void)cmp_u64; (void)cmp_f64;
   return R.error;

@@ -48,7 +48,8 @@ class Cluster(C.Structure):
         ("prefill_per_token_s", C.c_double), ("decode_base_s", C.c_double),
         ("decode_per_request_s", C.c_double), ("decode_per_kv_token_s", C.c_double),
         ("decode_tokens_per_step", C.c_int64), ("cache_enabled", C.c_int32),
-        ("_pad", C.c_int32),
+        ("cache_n_probes", C.c_int32), ("cache_budget_tokens", C.c_int64),
+        ("cache_probe_lens", C.c_void_p),
     ]
 
 
@@ -90,7 +91,8 @@ class Experiment(C.Structure):
 
 class Trace(C.Structure):
     _fields_ = [("arrival_ns", C.POINTER(C.c_int64)), ("prompt_len", C.POINTER(C.c_int32)),
-                ("output_len", C.POINTER(C.c_int32)), ("n", C.c_int64), ("digest", C.c_uint64)]
+                ("output_len", C.POINTER(C.c_int32)), ("n", C.c_int64), ("digest", C.c_uint64),
+                ("prefix_pool_id", C.POINTER(C.c_int32)), ("prefix_size", C.POINTER(C.c_int32))]
 
 
 AGG_FIELDS = [
@@ -133,7 +135,8 @@ class WindowBatch(C.Structure):
                 ("n_pending", C.c_void_p), ("dp_off", C.c_void_p), ("n_limit", C.c_void_p),
                 ("req_id", C.c_void_p), ("prompt_len", C.c_void_p), ("wait_in", C.c_void_p),
                 ("caps", C.c_void_p), ("out_dp", C.c_void_p), ("out_rank", C.c_void_p),
-                ("wait_out", C.c_void_p), ("flow", C.c_void_p)]
+                ("wait_out", C.c_void_p), ("flow", C.c_void_p), ("hit_off", C.c_void_p),
+                ("hit", C.c_void_p)]
 
 
 class DecodeBatch(C.Structure):
@@ -161,8 +164,9 @@ def lib():
         L.sbs_last_error.restype = C.c_char_p
         L.sbs_version.restype = C.c_char_p
         L.sbs_generate_workload.argtypes = [C.POINTER(Workload), C.c_uint64, C.c_void_p,
-                                            C.c_void_p, C.c_void_p, C.c_int64,
-                                            C.POINTER(C.c_int64), C.POINTER(C.c_uint64)]
+                                            C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.c_int64, C.POINTER(C.c_int64),
+                                            C.POINTER(C.c_uint64)]
         L.sbs_sim_create.argtypes = [C.POINTER(Experiment), C.c_int32, C.POINTER(Trace),
                                      C.c_int32, C.c_void_p, C.c_uint32, C.c_int32,
                                      C.POINTER(C.c_void_p)]
@@ -270,6 +274,7 @@ def _length(obj, path):
 class Point:
     """One replica: the ctypes Experiment plus the fault arrays it points to."""
     exp: Experiment
+    probes: object = None
     drops: object = None
     deads: object = None
     topo: object = None
@@ -294,9 +299,24 @@ def experiment_from_config(cfg: dict) -> Point:
         _keys(c["engine"], "cluster.engine", _ENGINE_KEYS)
         for k in _ENGINE_KEYS:
             setattr(cl, k, _num(c["engine"], k, 0.0, "cluster.engine"))
+    probes = None
     if "cache" in c:
-        _keys(c["cache"], "cluster.cache", {"enabled", "probe_lens", "budget_tokens"})
-        cl.cache_enabled = 1 if c["cache"].get("enabled", False) else 0
+        cc = c["cache"]
+        _keys(cc, "cluster.cache", {"enabled", "probe_lens", "budget_tokens"})
+        if "enabled" in cc and not isinstance(cc["enabled"], bool):
+            raise ConfigError("cluster.cache.enabled must be a boolean")
+        cl.cache_enabled = 1 if cc.get("enabled", False) else 0
+        cl.cache_budget_tokens = _int(cc, "budget_tokens", 0, "cluster.cache")
+        if "probe_lens" in cc:
+            if not isinstance(cc["probe_lens"], list):
+                raise ConfigError("cluster.cache.probe_lens must be an array")
+            for v in cc["probe_lens"]:
+                if isinstance(v, bool) or not isinstance(v, int):
+                    raise ConfigError("cluster.cache.probe_lens entries must be integers")
+            if cc["probe_lens"]:
+                probes = (C.c_int64 * len(cc["probe_lens"]))(*cc["probe_lens"])
+                cl.cache_probe_lens = C.cast(probes, C.c_void_p)
+                cl.cache_n_probes = len(cc["probe_lens"])
     w = cfg.get("workload", {})
     _keys(w, "workload", _WORKLOAD_KEYS)
     wl = Workload(process=0, initial_burst=0, rate_qps=1.0, duration_s=1.0,
@@ -342,7 +362,7 @@ def experiment_from_config(cfg: dict) -> Point:
     x.warmup_fraction = _num(sim, "warmup_fraction", 0.1, "sim")
     if not (0.0 <= x.warmup_fraction < 1.0):
         raise ConfigError("sim.warmup_fraction must be in [0, 1)")
-    pt = Point(exp=x)
+    pt = Point(exp=x, probes=probes)
     f = cfg.get("faults", {})
     _keys(f, "faults", {"drop_end_forward", "dead", "topology"})
     drops = [DropFault(instance=e.get("instance", -1), from_s=float(e.get("from_s", 0.0)),
@@ -371,16 +391,23 @@ class HostTrace:
     prompt_len: np.ndarray
     output_len: np.ndarray
     digest: int
+    prefix_pool_id: np.ndarray = None  # shared-prefix pool per request (-1: none)
+    prefix_size: np.ndarray = None     # prefix tokens per request
 
     @property
     def n(self):
         return len(self.arrival_ns)
 
     def as_c(self) -> Trace:
+        i32 = C.POINTER(C.c_int32)
         return Trace(self.arrival_ns.ctypes.data_as(C.POINTER(C.c_int64)),
-                     self.prompt_len.ctypes.data_as(C.POINTER(C.c_int32)),
-                     self.output_len.ctypes.data_as(C.POINTER(C.c_int32)),
-                     self.n, self.digest)
+                     self.prompt_len.ctypes.data_as(i32),
+                     self.output_len.ctypes.data_as(i32),
+                     self.n, self.digest,
+                     self.prefix_pool_id.ctypes.data_as(i32) if self.prefix_pool_id is not None
+                     else None,
+                     self.prefix_size.ctypes.data_as(i32) if self.prefix_size is not None
+                     else None)
 
 
 def generate_workload(point_or_cfg, pinned: bool = False) -> HostTrace:
@@ -389,8 +416,8 @@ def generate_workload(point_or_cfg, pinned: bool = False) -> HostTrace:
     L = lib()
     n = C.c_int64(0)
     dg = C.c_uint64(0)
-    _check(L.sbs_generate_workload(C.byref(pt.exp.workload), pt.exp.seed, None, None, None, 0,
-                                   C.byref(n), C.byref(dg)))
+    _check(L.sbs_generate_workload(C.byref(pt.exp.workload), pt.exp.seed, None, None, None,
+                                   None, None, 0, C.byref(n), C.byref(dg)))
     cnt = max(n.value, 1)
     if pinned:
         import torch
@@ -401,10 +428,19 @@ def generate_workload(point_or_cfg, pinned: bool = False) -> HostTrace:
         a = np.empty(cnt, np.int64)
         p = np.empty(cnt, np.int32)
         o = np.empty(cnt, np.int32)
+    pp = ps = None
+    if pt.exp.workload.shared_prefix_fraction > 0:
+        pp = np.empty(cnt, np.int32)
+        ps = np.empty(cnt, np.int32)
     _check(L.sbs_generate_workload(C.byref(pt.exp.workload), pt.exp.seed, a.ctypes.data,
-                                   p.ctypes.data, o.ctypes.data, cnt, C.byref(n), C.byref(dg)))
+                                   p.ctypes.data, o.ctypes.data,
+                                   pp.ctypes.data if pp is not None else None,
+                                   ps.ctypes.data if ps is not None else None, cnt,
+                                   C.byref(n), C.byref(dg)))
     k = n.value
-    return HostTrace(a[:k], p[:k], o[:k], dg.value)
+    if pp is not None:
+        pp, ps = pp[:k], ps[:k]
+    return HostTrace(a[:k], p[:k], o[:k], dg.value, pp, ps)
 
 
 # ----------------------------------------------------------------- simulator
@@ -513,10 +549,11 @@ def run_experiment(cfg: dict, per_request=False, logs=False, device=0):
 
 # ----------------------------------------------------------------- allocators
 def allocate_batch(windows, device="cuda"):
-    """Batched allocate_batch (prefill_alloc.cpp:61-88, Basic mode).
+    """Batched allocate_batch (prefill_alloc.cpp:61-88).
 
     windows: list of dicts {pending: (k,3) int array of (id, prompt_len,
-    wait_cycles), new: (k,3), caps: [c_avail per DP], n_limit}.
+    wait_cycles), new: (k,3), caps: [c_avail per DP], n_limit} and, for the
+    cache-aware mode, hits: (k_pending + k_new, D) Len_hit(r, d).
     Returns per window {mapping: [(id, dp)] in placement order, deferred:
     [(id, wait)], throttled: [id], caps: working capacities, flow: bool}.
     """
@@ -543,11 +580,22 @@ def allocate_batch(windows, device="cuda"):
     t_rank = torch.empty_like(t_dp)
     t_wout = torch.empty_like(t_dp)
     t_flow = torch.empty(max(len(windows), 1), dtype=torch.uint8, device=dev)
+    t_hoff = t_hit = None
+    if any("hits" in w for w in windows):
+        hoff, hits = [0], []
+        for w, n0, n1, d0, d1 in zip(windows, req_off, req_off[1:], dp_off, dp_off[1:]):
+            h = np.asarray(w.get("hits", np.zeros((n1 - n0, d1 - d0))), np.int64)
+            h = h.reshape(n1 - n0, d1 - d0)
+            hits.append(h.ravel())
+            hoff.append(hoff[-1] + h.size)
+        t_hoff, t_hit = T(hoff, torch.int64), T(cat(hits), torch.int64)
     b = WindowBatch(n_windows=len(windows), req_off=t_req_off.data_ptr(), n_pending=t_np.data_ptr(),
                     dp_off=t_dp_off.data_ptr(), n_limit=t_nl.data_ptr(), req_id=t_id.data_ptr(),
                     prompt_len=t_len.data_ptr(), wait_in=t_wait.data_ptr(),
                     caps=t_caps.data_ptr(), out_dp=t_dp.data_ptr(), out_rank=t_rank.data_ptr(),
-                    wait_out=t_wout.data_ptr(), flow=t_flow.data_ptr())
+                    wait_out=t_wout.data_ptr(), flow=t_flow.data_ptr(),
+                    hit_off=t_hoff.data_ptr() if t_hoff is not None else None,
+                    hit=t_hit.data_ptr() if t_hit is not None else None)
     stream = torch.cuda.current_stream(dev).cuda_stream
     _check(lib().sbs_prefill_allocate(C.byref(b), C.c_void_p(stream)))
     o_dp, o_rank, o_w = t_dp.cpu().numpy(), t_rank.cpu().numpy(), t_wout.cpu().numpy()

@@ -1,12 +1,13 @@
 // Batched allocation kernels — the allocation step as its own sm_100a kernel.
 //
-//  pbaa_kernel   : allocate_batch (prefill_alloc.cpp:61-88, Basic mode) over a
-//                  CSR batch of cluster-windows, one warp per window.  Each
-//                  queue is sorted by (prompt_len desc, id asc) with a warp
-//                  bitonic sort in shared memory, then placed greedily: a
-//                  REDUX-max over the DP capacities staged in shared memory
-//                  gives argmax c_avail (== argmax capacity_after in Basic
-//                  mode), lowest index on ties, guarded by c_avail > 0.
+//  pbaa_kernel   : allocate_batch (prefill_alloc.cpp:61-88) over a CSR batch
+//                  of cluster-windows, one warp per window.  Each queue is
+//                  sorted by (prompt_len desc, id asc) with a warp bitonic
+//                  sort in shared memory, then placed greedily: a warp max
+//                  over capacity_after = c_avail - (prompt - hit) for the DP
+//                  capacities staged in shared memory (hit = 0 in Basic
+//                  mode), lowest index on ties, guarded by c_avail > 0 on the
+//                  chosen unit.
 //  iqr_kernel    : select_decode_unit (decode_alloc.cpp:38-81), one warp per
 //                  call: K staged and sorted in shared memory, Q1/Q3 by the
 //                  reference's FP64 interpolation, IQR mask, lex-min (B, K).
@@ -66,6 +67,8 @@ struct PbaaArgs {
   int32_t* wait_out;
   uint8_t* flow;
   int32_t* error;
+  const int64_t* hit_off;  // cache-aware: Len_hit per (request, DP), NULL = Basic
+  const int64_t* hit;
 };
 
 __global__ void __launch_bounds__(32 * kAllocWarps) pbaa_kernel(PbaaArgs A) {
@@ -95,6 +98,7 @@ __global__ void __launch_bounds__(32 * kAllocWarps) pbaa_kernel(PbaaArgs A) {
   int rank = 0;
   bool stopped = false;
   bool any_thr = false;
+  const int64_t* hrow = A.hit != nullptr ? A.hit + A.hit_off[w] : nullptr;
   for (int phase = 0; phase < 2; ++phase) {
     const int q0 = phase == 0 ? 0 : npend;
     const int qn = phase == 0 ? npend : n - npend;
@@ -106,33 +110,39 @@ __global__ void __launch_bounds__(32 * kAllocWarps) pbaa_kernel(PbaaArgs A) {
     }
     __syncwarp();
     warp_sort_pairs(ka, kb, ki, qn);
-    int i = 0;
-    while (i < qn && !stopped) {
+    for (int i = 0; i < qn && !stopped; ++i) {
       int pos = ki[i];
       int64_t len = A.prompt_len[r0 + pos];
-      // argmax c_avail over D, lowest index on ties (capacity_after = c_avail - len)
+      // argmax capacity_after over D, lowest index on ties
       int64_t bv = INT64_MIN;
       int bd = 0x7fffffff;
+      bool room = false;
       for (int d = lane; d < D; d += 32) {
-        int64_t c = cap[d];
-        if (c > bv) { bv = c; bd = d; }
+        const int64_t c = cap[d];
+        const int64_t after = c - (len - (hrow ? hrow[(int64_t)pos * D + d] : 0));
+        if (after > bv) { bv = after; bd = d; }
+        room |= c > 0;
       }
+      // no unit with headroom: nothing in this phase (or the next) fits
+      if (!__any_sync(kFull, room)) { stopped = true; break; }
       int64_t mv = warp_max_i64(bv);
       int best = (int)__reduce_min_sync(kFull, bv == mv ? (uint32_t)bd : 0x7fffffffu);
-      if (mv <= 0) { stopped = true; break; }  // guard: c_avail[best] > 0
+      if (cap[best] <= 0) continue;  // guard on the chosen unit: deferred
+      __syncwarp();
       if (lane == 0) {
-        cap[best] = mv - len;
+        cap[best] = mv;
         A.out_dp[r0 + pos] = best;
         A.out_rank[r0 + pos] = rank;
         A.wait_out[r0 + pos] = A.wait_in[r0 + pos];
+        ki[i] = -1;  // placed
       }
       __syncwarp();
       rank += 1;
-      i += 1;
     }
-    // deferred suffix [i, qn): age; throttle beyond n_limit
-    for (int j = i + lane; j < qn; j += 32) {
+    // deferred (every unplaced request): age; throttle beyond n_limit
+    for (int j = lane; j < qn; j += 32) {
       int pos = ki[j];
+      if (pos < 0) continue;
       int wv = A.wait_in[r0 + pos] + 1;
       bool thr = wv > nlim;
       A.out_dp[r0 + pos] = thr ? -2 : -1;

@@ -206,7 +206,7 @@ __device__ __forceinline__ int chan_ld(const volatile int* p) {
 // LOG: keep run records (compiled out of the sweep kernel).
 // ROLE: 0 = the whole replica on one warp; 1 = the prefill warp and 2 = the
 // decode warp of a two-warp replica (see the channel notes at the event loop).
-template <int KD, bool LOG, int ROLE, bool CL>
+template <int KD, bool LOG, int ROLE, bool CL, bool CA = false>
 __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* sm,
                             unsigned char* sm_peer) {
   static_assert(!(LOG && ROLE != 0), "run records are kept by the one-warp replica only");
@@ -430,6 +430,66 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     int src = __ffs(who) - 1;
     o_t = m; o_s = ms; o_k = bcast(lk, src); o_i = src;
     odirty = false;
+  };
+
+  // ---- prefix caches (cache-aware mode only): PrefixCache (core.cpp:13-75)
+  // per prefill DP unit g as last-use stamps over keys pool * n_probes + j;
+  // a larger stamp = nearer the front of the reference's LRU list.
+  // (nothing is hoisted into registers: the Basic-mode loop must not pay)
+  // longest_hit (core.cpp:33-41): the longest probe k <= prefix size cached on g
+  auto cache_hit = [&](int g, int pool, int ps) -> int32_t {
+    const int n_probes = pt.n_probes;
+    int32_t best = 0;
+    const int32_t* st = pt.c_stamp + (int64_t)g * pt.n_pools * n_probes + pool * n_probes;
+    for (int j = 0; j < n_probes; ++j) {  // (no shuffles: callers may diverge)
+      const int32_t k = pt.probe_k[j];
+      if (k > ps) break;
+      if (st[j] != 0) best = k;
+    }
+    return best;
+  };
+  // insert + evict_to_budget (core.cpp:43-75), warp-wide, lane j = probe j:
+  // probe j takes stamp clock + j + 1 (touch and new alike), new entries add
+  // k_j tokens; then the oldest entries go until the budget holds.
+  auto cache_insert = [&](int g, int pool, int ps) {
+    const int n_probes = pt.n_probes, n_keys = pt.n_pools * pt.n_probes;
+    const int32_t my_probe = lane < n_probes ? pt.probe_k[lane] : 0x7fffffff;
+    int32_t* const g_cstamp = pt.c_stamp;
+    int64_t* const g_cused = pt.c_used;
+    int32_t* const g_cclock = pt.c_clock;
+    const bool act = my_probe <= ps;  // a prefix of the lanes (probes ascend)
+    const unsigned m = __ballot_sync(kFull, act);
+    if (m == 0) return;
+    int32_t* st = g_cstamp + (int64_t)g * n_keys;
+    const int32_t clk = g_cclock[g];
+    int64_t add = 0;
+    if (act) {
+      const int key = pool * n_probes + lane;
+      if (st[key] == 0) add = my_probe;
+      st[key] = clk + lane + 1;
+    }
+    int64_t used = g_cused[g] + warp_sum_i64(add);
+    __syncwarp();
+    while (used > pt.cache_budget) {
+      uint32_t best = 0xffffffffu;
+      int bi = 0;
+      for (int i = lane; i < n_keys; i += 32) {
+        const uint32_t v = (uint32_t)st[i];
+        if (v != 0 && v < best) { best = v; bi = i; }
+      }
+      const uint32_t mn = __reduce_min_sync(kFull, best);
+      if (mn == 0xffffffffu) break;  // the list is empty
+      const int victim = (int)__reduce_max_sync(kFull, best == mn ? (uint32_t)bi : 0u);
+      used -= __shfl_sync(kFull, my_probe, victim % n_probes);
+      __syncwarp();
+      if (lane == 0) st[victim] = 0;
+      __syncwarp();
+    }
+    if (lane == 0) {
+      g_cclock[g] = clk + __popc(m);
+      g_cused[g] = used;
+    }
+    __syncwarp();
   };
 
   // ---- completion accounting (metrics.cpp:117-153), called by the lanes
@@ -935,6 +995,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     uint64_t* pk = pt.pend_key[pcur];
     int32_t* pw = pt.pend_wait[pcur];
     bool ovf = false;
+    constexpr uint64_t kPlaced = ~0ull;  // cache-aware mode: a placed queue entry
 
     // greedy phase over a sorted queue; returns number placed (a prefix)
     auto greedy = [&](const uint64_t* q, int n, bool& stopped) -> int {
@@ -971,10 +1032,92 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       }
       return i;
     };
-    bool stopped = false;
-    int k1 = greedy(pk, np, stopped);
-    int k2 = 0;
-    if (!stopped) k2 = greedy(nk, nn, stopped);
+    // cache-aware greedy (capacity_after with Len_hit, prefill_alloc.cpp:12-21):
+    // the argmax differs per request, so a guard failure defers only this
+    // request; placed entries are marked and the deferred ones kept in order
+    auto greedy_cache = [&](uint64_t* q, int n) -> int {
+      int placed = 0;
+      uint64_t kreg = 0;
+      int32_t preg = -1, sreg = 0;
+      for (int i = 0; i < n; ++i) {
+        if ((i & 31) == 0) {
+          kreg = (i + lane < n) ? q[i + lane] : 0;
+          const int64_t qid = key_id(kreg);
+          preg = (i + lane < n) ? __ldg(pt.pfx_pool + qid) : -1;
+          sreg = (i + lane < n) ? __ldg(pt.pfx_size + qid) : 0;
+        }
+        const uint64_t key = bcast(kreg, i & 31);
+        const int pool = bcast(preg, i & 31), ps = bcast(sreg, i & 31);
+        const int32_t len = key_len(key);
+        int64_t ba = INT64_MIN;
+        int bd = 0x7fffffff;
+        int32_t bh = 0;
+        bool room = false;
+#pragma unroll
+        for (int k = 0; k < KD; ++k) {
+          const int d = lane + 32 * k;
+          if (d >= D) continue;
+          const int32_t hit = pool >= 0 ? cache_hit(g0 + d, pool, ps) : 0;
+          const int64_t after = cap[k] - (int64_t)(len - hit);
+          if (after > ba) { ba = after; bd = d; bh = hit; }
+          room |= cap[k] > 0;
+        }
+        if (!__any_sync(kFull, room)) break;  // no unit has headroom: the rest defer
+        const int64_t mx = warp_max_i64(ba);
+        const int best = (int)__reduce_min_sync(kFull, ba == mx ? (uint32_t)bd : 0x7fffffffu);
+        int64_t cb = 0;
+#pragma unroll
+        for (int k = 0; k < KD; ++k)
+          if (k == (best >> 5)) cb = cap[k];
+        cb = __shfl_sync(kFull, cb, best & 31);
+        if (cb <= 0) continue;  // guard on the argmax unit: deferred
+        if (lane == (best & 31)) {
+#pragma unroll
+          for (int k = 0; k < KD; ++k)
+            if (k == (best >> 5)) cap[k] = mx;
+          const int64_t id = key_id(key);
+          const int32_t tokens = len - bh > 1 ? len - bh : 1;  // max(1, prompt - hit)
+          if (!fifo_push(g0 + best, id, tokens)) ovf = true;
+          o_dispatch[id] = now;
+          if (per_req) o_status[id] = kStDispatched;
+        }
+        if (lane == 0) q[i] = kPlaced;
+        placed += 1;
+      }
+      __syncwarp();
+      return placed;
+    };
+    int k1 = 0, k2 = 0, nplaced = 0;
+    int32_t tail0[KD];  // per-DP FIFO tails before this dispatch
+    int nn_left = nn;
+    if constexpr (CA) {
+#pragma unroll
+      for (int k = 0; k < KD; ++k) {
+        const int d = lane + 32 * k;
+        tail0[k] = d < D ? s_tail[g0 + d] : 0;
+      }
+      nplaced = greedy_cache(pk, np);
+      nplaced += greedy_cache(nk, nn);
+      // keep the unplaced new keys, in order, at the front of nk
+      int kept = 0;
+      for (int base = 0; base < nn; base += 32) {
+        const int i = base + lane;
+        const uint64_t v = i < nn ? nk[i] : kPlaced;
+        const bool keep = v != kPlaced;
+        const unsigned km = __ballot_sync(kFull, keep);
+        __syncwarp();
+        if (keep) nk[kept + __popc(km & lt_mask)] = v;
+        kept += __popc(km);
+        __syncwarp();
+      }
+      nn_left = kept;
+    } else {
+      bool stopped = false;
+      k1 = greedy(pk, np, stopped);
+      if (!stopped) k2 = greedy(nk, nn, stopped);
+      nplaced = k1 + k2;
+      nn_left = nn - k2;
+    }
     if (__any_sync(kFull, ovf)) { error = kErrOverflow; return -1; }
     CNT(alloc, 1);
 
@@ -982,8 +1125,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     int na = 0, thr = 0;
     for (int base = k1; base < np; base += 32) {
       int i = base + lane;
-      bool valid = i < np;
-      uint64_t key = valid ? pk[i] : 0;
+      uint64_t key = i < np ? pk[i] : 0;
+      bool valid = i < np && key != kPlaced;
       int32_t w = valid ? pw[i] + 1 : 0;
       bool th = valid && w > n_limit;
       bool keep = valid && !th;
@@ -996,7 +1139,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       thr += __popc(__ballot_sync(kFull, th));
       __syncwarp();
     }
-    int nb = nn - k2;
+    int nb = nn_left;
     int nbk = nb;
     if (nb > 0 && 1 > n_limit) {
       for (int i = lane; i < nb; i += 32)
@@ -1032,9 +1175,27 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     np = na + nbk;
     new_begin = next_id;  // q_new.clear()
 
-    if (k1 + k2 == 0) {
+    if (nplaced == 0) {
       if (np > 0) arm_tick(now + i_opt);
       return -1;
+    }
+    if constexpr (CA) {
+      // register the dispatched prefixes (simulation.cpp:319-326) after every
+      // hit was resolved; per DP unit in mapping order (= its FIFO order)
+      for (int d = 0; d < D; ++d) {
+        const int g = g0 + d;
+        int32_t t0 = 0;
+#pragma unroll
+        for (int k = 0; k < KD; ++k)
+          if (k == (d >> 5)) t0 = tail0[k];
+        t0 = __shfl_sync(kFull, t0, d & 31);
+        const int32_t te = s_tail[g];
+        for (int32_t t = t0; t < te; ++t) {
+          const int rid = g_fifo[(int64_t)g * F + (t & Fm)].x;
+          const int pool = __ldg(pt.pfx_pool + rid);
+          if (pool >= 0) cache_insert(g, pool, __ldg(pt.pfx_size + rid));
+        }
+      }
     }
     has_ld = true;
     last_disp = now;
@@ -1761,7 +1922,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
 // orders replicas by estimated cost, longest first).  One instantiation per
 // (prefill DP units per lane, run records) so each keeps its own registers and
 // instruction footprint.
-template <int KD, bool LOG>
+template <int KD, bool LOG, bool CA = false>
 __global__ void __launch_bounds__(128) des_kernel(const DevPoint* __restrict__ pts, int n_pts,
                                                   int* __restrict__ next_point,
                                                   DevResult* __restrict__ res, int smem_per_warp) {
@@ -1772,7 +1933,7 @@ __global__ void __launch_bounds__(128) des_kernel(const DevPoint* __restrict__ p
     if (lane_id() == 0) pi = atomicAdd(next_point, 1);
     pi = bcast(pi, 0);
     if (pi >= n_pts) return;
-    run_replica<KD, LOG, 0, false>(pts[pi], res[pi], my, my);
+    run_replica<KD, LOG, 0, false, CA>(pts[pi], res[pi], my, my);
     __syncwarp();
   }
 }
@@ -1998,17 +2159,21 @@ __global__ void __launch_bounds__(256) finalize_kernel(const DevPoint* __restric
 // ---------------------------------------------------------------------------
 namespace sbs {
 // variant: bit 0 = dp_degree > 32 (KD 4), bit 1 = run records, 4|5 = two-warp
-// replicas (smem_per_warp is then the per-pair slice, warps_per_block even)
+// replicas (smem_per_warp is then the per-pair slice, warps_per_block even),
+// 6..9 = 0..3 with the cache-aware dispatch compiled in
 cudaError_t launch_des(int variant, const DevPoint* d_pts, int n_pts, int* d_counter,
                        DevResult* d_res, int smem_per_warp, int warps_per_block, int n_blocks,
                        cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(d_counter, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
   // one-warp variants: a slice per warp; two-warp variants: a slice per pair
-  size_t smem = (size_t)smem_per_warp * (variant >= 4 ? warps_per_block / 2 : warps_per_block);
+  const bool pairs = variant == 4 || variant == 5;
+  size_t smem = (size_t)smem_per_warp * (pairs ? warps_per_block / 2 : warps_per_block);
   void (*k)(const DevPoint*, int, int*, DevResult*, int) =
       variant == 0 ? des_kernel<1, false> : variant == 1 ? des_kernel<4, false>
     : variant == 2 ? des_kernel<1, true> : variant == 3 ? des_kernel<4, true>
+    : variant == 6 ? des_kernel<1, false, true> : variant == 7 ? des_kernel<4, false, true>
+    : variant == 8 ? des_kernel<1, true, true> : variant == 9 ? des_kernel<4, true, true>
     : variant == 4 ? des_split_kernel<1> : des_split_kernel<4>;
   e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

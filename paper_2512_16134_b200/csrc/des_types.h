@@ -25,7 +25,8 @@ constexpr int kSmemWinKeys = 256;   // window keys kept in shared memory
 constexpr int kHistBins = 64;
 constexpr int kChanRecs = 32;       // prefill->decode hand-off records in flight
 constexpr int kChanKeys = 1024;     // hand-off waiter keys in flight
-constexpr int kChanComp = 256;      // decode completions returned to the prefill warp
+constexpr int kChanComp = 256;
+constexpr int kMaxProbes = 32;      // distinct prefix-cache probe lengths      // decode completions returned to the prefill warp
 constexpr int kErrSplitTie = 7;     // two-warp replica met an unresolvable tie: rerun serially
 
 // Prefill-warp -> decode-warp hand-off channel of a two-warp replica (shared
@@ -78,6 +79,16 @@ struct DevPoint {
   const int64_t* arr;
   const int32_t* prompt;
   const int32_t* output;
+  // ---- prefix caches (cache-aware PBAA, core.cpp:13-75): per prefill DP unit
+  // an LRU over keys (pool, probe) kept as last-use stamps (0 = absent)
+  int32_t cache_on, n_probes, n_pools, _pc;
+  int64_t cache_budget;
+  int32_t probe_k[kMaxProbes];  // ascending, distinct
+  const int32_t* pfx_pool;      // per request, -1 = no prefix
+  const int32_t* pfx_size;      // per request prefix tokens
+  int32_t* c_stamp;             // [P*D][n_pools*n_probes]
+  int64_t* c_used;              // [P*D] cached tokens
+  int32_t* c_clock;             // [P*D] stamps issued
   // ---- faults
   const int64_t* topo_time;  // sorted by (time, config order)
   const int32_t* topo_inst;

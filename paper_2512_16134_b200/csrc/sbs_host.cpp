@@ -53,6 +53,8 @@ struct PbaaArgs {
   int32_t* wait_out;
   uint8_t* flow;
   int32_t* error;
+  const int64_t* hit_off;  // cache-aware mode (NULL: Basic)
+  const int64_t* hit;
 };
 struct IqrArgs {
   int32_t n_calls;
@@ -132,17 +134,40 @@ void check_workload(const sbs_workload& w) {
   if (!(w.duration_s > 0)) throw Error{SBS_ERR_CONFIG, "workload duration_s must be > 0"};
   if (w.shared_prefix_fraction < 0 || w.shared_prefix_fraction > 1)
     throw Error{SBS_ERR_CONFIG, "shared_prefix_fraction must be in [0, 1]"};
-  if (w.shared_prefix_fraction > 0)
+  if (w.shared_prefix_fraction > 0 && (w.prefix_pool <= 0 || w.prefix_len <= 0))
     throw Error{SBS_ERR_CONFIG,
-                "shared prefixes (cache-aware mode) are out of scope of the GPU path"};
+                "prefix_pool and prefix_len must be positive when shared prefixes are enabled"};
   if (w.initial_burst < 0) throw Error{SBS_ERR_CONFIG, "workload initial_burst must be >= 0"};
 }
 
 struct HostTrace {
   std::vector<int64_t> arr;
   std::vector<int32_t> prompt, output;
+  std::vector<int32_t> pool, psize;  // empty when no request has a shared prefix
   uint64_t digest = 0;
 };
+
+// Deterministic token id for position i of pool prefix p (workload.cpp:30-37).
+int32_t prefix_token(int pool_id, int64_t i) {
+  uint64_t h = 1469598103934665603ull;
+  h ^= static_cast<uint64_t>(pool_id) * 0x9e3779b97f4a7c15ull;
+  h ^= static_cast<uint64_t>(i) + 0x632be59bd9b4e019ull;
+  h *= 1099511628211ull;
+  return static_cast<int32_t>(h & 0x7fffffff);
+}
+
+// PrefixCache::hash_prefix (core.cpp:18-31) of the first k tokens of pool p.
+uint64_t hash_pool_prefix(int pool_id, int64_t k) {
+  uint64_t h = 14695981039346656037ull ^ static_cast<uint64_t>(k);
+  for (int64_t i = 0; i < k; ++i) {
+    const uint32_t v = static_cast<uint32_t>(prefix_token(pool_id, i));
+    for (int b = 0; b < 4; ++b) {
+      h ^= (v >> (8 * b)) & 0xff;
+      h *= 1099511628211ull;
+    }
+  }
+  return h;
+}
 
 void mix_digest(uint64_t& h, uint64_t v) {
   for (int b = 0; b < 8; ++b) {
@@ -189,6 +214,9 @@ void generate(const sbs_workload& spec, uint64_t seed, HostTrace& out) {
   out.arr.resize(n);
   out.prompt.resize(n);
   out.output.resize(n);
+  const bool prefixes = spec.shared_prefix_fraction > 0;
+  out.pool.assign(prefixes ? n : 0, -1);
+  out.psize.assign(prefixes ? n : 0, 0);
   uint64_t h = 14695981039346656037ull;
   for (size_t i = 0; i < n; ++i) {
     int64_t at = std::min(seconds_to_ns(arrivals[i]), horizon - 1);
@@ -200,11 +228,22 @@ void generate(const sbs_workload& spec, uint64_t seed, HostTrace& out) {
     out.arr[i] = at;
     out.prompt[i] = static_cast<int32_t>(p);
     out.output[i] = static_cast<int32_t>(o);
+    // shared prefix (workload.cpp:129-138): the tokens are a pure function of
+    // (pool, position), so (pool id, length) stands for Request::prefix_tokens
+    int64_t plen = 0;
+    int32_t pool_id = -1;
+    if (prefixes && u01(rng) < spec.shared_prefix_fraction) {
+      int pid = static_cast<int>(u01(rng) * static_cast<double>(spec.prefix_pool));
+      pool_id = std::min(pid, spec.prefix_pool - 1);
+      plen = std::min<int64_t>(spec.prefix_len, p);
+      out.pool[i] = plen > 0 ? pool_id : -1;
+      out.psize[i] = static_cast<int32_t>(plen);
+    }
     mix_digest(h, static_cast<uint64_t>(at));
     mix_digest(h, static_cast<uint64_t>(p));
     mix_digest(h, static_cast<uint64_t>(o));
-    mix_digest(h, 0);  // no shared prefix: front()+1 term is 0
-    mix_digest(h, 0);  // prefix size
+    mix_digest(h, plen == 0 ? 0 : static_cast<uint64_t>(prefix_token(pool_id, 0)) + 1);
+    mix_digest(h, static_cast<uint64_t>(plen));
   }
   out.digest = h;
 }
@@ -235,9 +274,22 @@ void validate(const sbs_experiment& x) {
   require(c.decode_max_batch_per_dp >= 0, "decode_max_batch_per_dp must be >= 0");
   require(x.warmup_fraction >= 0.0 && x.warmup_fraction < 1.0,
           "sim.warmup_fraction must be in [0, 1)");
+  if (c.cache_enabled) {  // core.cpp:106-113
+    require(c.cache_n_probes >= 1 && c.cache_probe_lens != nullptr,
+            "cache.probe_lens must be non-empty when the cache is enabled");
+    for (int i = 0; i < c.cache_n_probes; ++i)
+      require(c.cache_probe_lens[i] >= 1, "cache.probe_lens entries must be >= 1");
+    require(c.cache_budget_tokens >= 1, "cache.budget_tokens must be >= 1 when the cache is enabled");
+  }
+  require(x.prefill_mode == SBS_ALLOC_BASIC || x.prefill_mode == SBS_ALLOC_CACHE_AWARE,
+          "scheduler.prefill_mode must be basic or cache_aware");
   // GPU-path envelope (documented in DESIGN.md)
-  require(c.cache_enabled == 0 && x.prefill_mode == SBS_ALLOC_BASIC,
-          "cache-aware prefill allocation is out of scope of the GPU path");
+  if (c.cache_enabled && x.prefill_mode == SBS_ALLOC_CACHE_AWARE) {
+    std::vector<int64_t> pr(c.cache_probe_lens, c.cache_probe_lens + c.cache_n_probes);
+    std::sort(pr.begin(), pr.end());
+    pr.erase(std::unique(pr.begin(), pr.end()), pr.end());
+    require(pr.size() <= (size_t)sbs::kMaxProbes, "GPU path supports at most 32 distinct probe lengths");
+  }
   require(c.n_instances_prefill <= sbs::kMaxInstances && c.n_instances_decode <= sbs::kMaxInstances,
           "GPU path supports at most 32 prefill and 32 decode instances");
   require(c.dp_degree <= sbs::kMaxPrefillDp, "GPU path supports dp_degree <= 128");
@@ -272,8 +324,12 @@ struct TraceDev {
   int64_t* arr = nullptr;
   int32_t* prompt = nullptr;
   int32_t* output = nullptr;
+  int32_t* pool = nullptr;   // shared-prefix pool id per request (-1: none), or NULL
+  int32_t* psize = nullptr;  // prefix tokens per request
   int64_t n = 0;
   int32_t max_output = 0;
+  int32_t n_pools = 0;       // 1 + max pool id
+  int64_t max_psize = 0;
   uint64_t digest = 0;
 };
 
@@ -282,6 +338,7 @@ struct PointHost {
   std::vector<sbs_drop_fault> drops;
   std::vector<sbs_dead_fault> deads;
   std::vector<sbs_topology_fault> topo;
+  std::vector<int64_t> probes;  // cache.probe_lens (owned copy)
   int trace = 0;
   // capacities (grown on overflow)
   int32_t F = 0, QP = 0, QW = 0, BC = 0, QD = 0;
@@ -304,7 +361,8 @@ struct sbs_sim {
   std::vector<PointHost> pts;
   std::vector<TraceDev> traces;
   std::vector<int> order;  // device slot -> point index (grouped by variant, cost-descending)
-  int group_begin[7] = {0, 0, 0, 0, 0, 0, 0};  // slots of kernel variant v: [group_begin[v], group_begin[v+1])
+  static constexpr int kVariants = 10;
+  int group_begin[kVariants + 1] = {};  // slots of kernel variant v: [group_begin[v], group_begin[v+1])
   sbs::DevPoint* d_pts = nullptr;
   sbs::DevResult* d_res = nullptr;
   int* d_counter = nullptr;
@@ -379,7 +437,9 @@ void build_point(sbs_sim& s, PointHost& p) {
     const bool allow = e == nullptr || std::atoi(e) != 0;
     // the decode warp only pays off when the trace has decode work
     // (completion-ring entries carry times in 48 bits)
-    d.split = (allow && p.split && !(s.flags & SBS_FLAG_LOGS) && t.max_output > 1 &&
+    // (cache-aware points run on the one-warp kernels that compile the cache in)
+    const bool ca = x.prefill_mode == SBS_ALLOC_CACHE_AWARE && c.cache_enabled && t.pool != nullptr;
+    d.split = (allow && p.split && !ca && !(s.flags & SBS_FLAG_LOGS) && t.max_output > 1 &&
                seconds_to_ns(x.workload.duration_s) < (int64_t(1) << 47)) ? 1 : 0;
   }
   d.c_chunk = c.c_chunk;
@@ -400,6 +460,35 @@ void build_point(sbs_sim& s, PointHost& p) {
   d.arr = t.arr;
   d.prompt = t.prompt;
   d.output = t.output;
+  // cache-aware PBAA (simulation.cpp:267-268: mode cache_aware AND cache on)
+  d.cache_on = (x.prefill_mode == SBS_ALLOC_CACHE_AWARE && c.cache_enabled && t.pool != nullptr &&
+                t.n_pools > 0) ? 1 : 0;
+  if (d.cache_on) {
+    // probe lengths ascending (core.cpp:15); a repeated length only re-touches
+    // the entry it just inserted, which leaves the LRU order unchanged
+    std::vector<int64_t> pr = p.probes;
+    std::sort(pr.begin(), pr.end());
+    pr.erase(std::unique(pr.begin(), pr.end()), pr.end());
+    d.n_probes = (int32_t)pr.size();
+    for (size_t j = 0; j < pr.size(); ++j)
+      d.probe_k[j] = (int32_t)std::min<int64_t>(pr[j], (int64_t)1 << 30);
+    d.n_pools = t.n_pools;
+    d.cache_budget = c.cache_budget_tokens;
+    d.pfx_pool = t.pool;
+    d.pfx_size = t.psize;
+    // entries are keyed by (pool, probe); the reference keys them by a 64-bit
+    // FNV hash of the tokens (core.cpp:18-31): refuse the (never observed)
+    // case of two distinct prefixes hashing alike
+    std::vector<uint64_t> hs;
+    for (int pool = 0; pool < t.n_pools; ++pool)
+      for (int64_t k : pr)
+        if (k <= t.max_psize) hs.push_back(hash_pool_prefix(pool, k));
+    std::sort(hs.begin(), hs.end());
+    if (std::adjacent_find(hs.begin(), hs.end()) != hs.end())
+      throw Error{SBS_ERR_CONFIG, "prefix hash collision between distinct cache keys"};
+    if ((int64_t)t.n * d.n_probes >= ((int64_t)1 << 31))
+      throw Error{SBS_ERR_CONFIG, "GPU path: requests x probe lengths must stay below 2^31"};
+  }
   // decode completion ring: strictly more buckets than steps a request lives
   int64_t max_target = std::max<int64_t>(1, (int64_t)t.max_output - 1);
   int64_t max_steps = (max_target + c.decode_tokens_per_step - 1) / c.decode_tokens_per_step;
@@ -480,6 +569,10 @@ void build_point(sbs_sim& s, PointHost& p) {
   size_t o_dw = carve(8 * (size_t)p.QD);
   size_t o_mt = carve(8 * 312);
   size_t o_th = carve(8 * sbs::kHistBins);
+  const size_t n_keys = d.cache_on ? (size_t)d.n_pools * d.n_probes : 0;
+  size_t o_cs = d.cache_on ? carve(4 * (size_t)PD * n_keys) : 0;
+  size_t o_cu = d.cache_on ? carve(8 * (size_t)PD) : 0;
+  size_t o_cc = d.cache_on ? carve(4 * (size_t)PD) : 0;
   const bool logs = (s.flags & SBS_FLAG_LOGS) != 0;
   size_t o_log = logs ? carve(8 * (size_t)p.LOG) : 0;
   if (p.arena == nullptr || p.arena_bytes < sz) {
@@ -505,6 +598,9 @@ void build_point(sbs_sim& s, PointHost& p) {
   d.dwait = (uint64_t*)(b + o_dw);
   d.mt = (uint64_t*)(b + o_mt);
   d.tpot_hist = (int64_t*)(b + o_th);
+  d.c_stamp = d.cache_on ? (int32_t*)(b + o_cs) : nullptr;
+  d.c_used = d.cache_on ? (int64_t*)(b + o_cu) : nullptr;
+  d.c_clock = d.cache_on ? (int32_t*)(b + o_cc) : nullptr;
   d.log = logs ? (int64_t*)(b + o_log) : nullptr;
   d.log_cap = logs ? p.LOG : 0;
   layout_smem(d);
@@ -515,6 +611,12 @@ void build_point(sbs_sim& s, PointHost& p) {
 void reset_point(const PointHost& p, cudaStream_t st) {
   const sbs::DevPoint& d = p.dp;
   CUDA_OR_THROW(cudaMemsetAsync(d.tpot_hist, 0, 8 * sbs::kHistBins, st));
+  if (d.cache_on) {  // empty prefix caches
+    const size_t PD = (size_t)d.P * d.D;
+    CUDA_OR_THROW(cudaMemsetAsync(d.c_stamp, 0, 4 * PD * (size_t)d.n_pools * d.n_probes, st));
+    CUDA_OR_THROW(cudaMemsetAsync(d.c_used, 0, 8 * PD, st));
+    CUDA_OR_THROW(cudaMemsetAsync(d.c_clock, 0, 4 * PD, st));
+  }
   if (d.per_request) {
     CUDA_OR_THROW(cudaMemsetAsync(d.o_dispatch, 0xff, 8 * (size_t)d.N, st));
     CUDA_OR_THROW(cudaMemsetAsync(d.o_pstart, 0xff, 8 * (size_t)d.N, st));
@@ -552,7 +654,7 @@ void grow_caps(PointHost& p) {
 
 int variant_of(const PointHost& p) {
   if (p.dp.split) return 4 | (p.dp.D > 32 ? 1 : 0);
-  return (p.dp.D > 32 ? 1 : 0) | (p.dp.log != nullptr ? 2 : 0);
+  return (p.dp.D > 32 ? 1 : 0) + (p.dp.log != nullptr ? 2 : 0) + (p.dp.cache_on ? 6 : 0);
 }
 
 void order_points(sbs_sim& s) {
@@ -564,23 +666,23 @@ void order_points(sbs_sim& s) {
     if (va != vb) return va < vb;
     return s.pts[a].cost > s.pts[b].cost;
   });
-  for (int v = 0; v <= 6; ++v) s.group_begin[v] = 0;
+  for (int v = 0; v <= sbs_sim::kVariants; ++v) s.group_begin[v] = 0;
   for (int i = 0; i < n; ++i) s.group_begin[variant_of(s.pts[s.order[i]]) + 1] += 1;
-  for (int v = 1; v <= 6; ++v) s.group_begin[v] += s.group_begin[v - 1];
+  for (int v = 1; v <= sbs_sim::kVariants; ++v) s.group_begin[v] += s.group_begin[v - 1];
 }
 
 void launch_all(sbs_sim& s, cudaStream_t st) {
   s.n_launches = 0;
-  for (int v = 0; v < 6; ++v) {
+  for (int v = 0; v < sbs_sim::kVariants; ++v) {
     const int b = s.group_begin[v], e = s.group_begin[v + 1];
     if (e <= b) continue;
     int wpb = s.warps_per_block, per_block = wpb;
-    if (v >= 4 && s.pair_mode == 2) {  // replica = a CTA pair of a 2-CTA cluster
+    if ((v == 4 || v == 5) && s.pair_mode == 2) {  // replica = a CTA pair of a 2-CTA cluster
       CUDA_OR_THROW(sbs::launch_des_cluster(v, s.d_pts + b, e - b, s.d_res + b, s.smem_per_warp, st));
       s.n_launches += 1;
       continue;
     }
-    if (v >= 4) {  // two warps per replica; at most two replicas per block
+    if (v == 4 || v == 5) {  // two warps per replica; at most two replicas per block
       const int rpb = std::max(1, std::min(2, (e - b + s.sm_count - 1) / s.sm_count));
       wpb = 2 * rpb;
       per_block = rpb;
@@ -630,6 +732,12 @@ void do_upload_traces(sbs_sim& s, const sbs_trace* traces, cudaStream_t st) {
     CUDA_OR_THROW(cudaMemcpyAsync(t.arr, traces[i].arrival_ns, 8 * t.n, cudaMemcpyHostToDevice, st));
     CUDA_OR_THROW(cudaMemcpyAsync(t.prompt, traces[i].prompt_len, 4 * t.n, cudaMemcpyHostToDevice, st));
     CUDA_OR_THROW(cudaMemcpyAsync(t.output, traces[i].output_len, 4 * t.n, cudaMemcpyHostToDevice, st));
+    if ((traces[i].prefix_pool_id != nullptr) != (t.pool != nullptr))
+      throw Error{SBS_ERR_CONFIG, "trace shape changed"};
+    if (t.pool) {
+      CUDA_OR_THROW(cudaMemcpyAsync(t.pool, traces[i].prefix_pool_id, 4 * t.n, cudaMemcpyHostToDevice, st));
+      CUDA_OR_THROW(cudaMemcpyAsync(t.psize, traces[i].prefix_size, 4 * t.n, cudaMemcpyHostToDevice, st));
+    }
   }
 }
 
@@ -742,8 +850,8 @@ const char* sbs_last_error(void) { return g_err.c_str(); }
 const char* sbs_version(void) { return "sbs_b200 0.1 (sm_100a)"; }
 
 int sbs_generate_workload(const sbs_workload* spec, uint64_t seed, int64_t* arrival_ns,
-                          int32_t* prompt_len, int32_t* output_len, int64_t cap, int64_t* n_out,
-                          uint64_t* digest) {
+                          int32_t* prompt_len, int32_t* output_len, int32_t* prefix_pool_id,
+                          int32_t* prefix_size, int64_t cap, int64_t* n_out, uint64_t* digest) {
   return guarded([&] {
     HostTrace t;
     generate(*spec, seed, t);
@@ -754,6 +862,11 @@ int sbs_generate_workload(const sbs_workload* spec, uint64_t seed, int64_t* arri
     std::memcpy(arrival_ns, t.arr.data(), 8 * t.arr.size());
     std::memcpy(prompt_len, t.prompt.data(), 4 * t.prompt.size());
     std::memcpy(output_len, t.output.data(), 4 * t.output.size());
+    const size_t n = t.arr.size();
+    for (size_t i = 0; i < n; ++i) {
+      if (prefix_pool_id) prefix_pool_id[i] = t.pool.empty() ? -1 : t.pool[i];
+      if (prefix_size) prefix_size[i] = t.psize.empty() ? 0 : t.psize[i];
+    }
     return SBS_OK;
   });
 }
@@ -790,6 +903,20 @@ int sbs_sim_create(const sbs_experiment* points, int32_t n_points, const sbs_tra
       CUDA_OR_THROW(cudaMalloc(&t.prompt, 4 * n));
       CUDA_OR_THROW(cudaMalloc(&t.output, 4 * n));
       s->device_bytes += (int64_t)(16 * n);
+      if (traces[i].prefix_pool_id != nullptr && traces[i].prefix_size != nullptr) {
+        for (int64_t k = 0; k < t.n; ++k) {
+          const int32_t pid = traces[i].prefix_pool_id[k], ps = traces[i].prefix_size[k];
+          if (ps < 0 || (ps > 0 && pid < 0) || ps > traces[i].prompt_len[k])
+            throw Error{SBS_ERR_CONFIG, "trace prefix sizes out of range"};
+          if (ps > 0) {
+            t.n_pools = std::max(t.n_pools, pid + 1);
+            t.max_psize = std::max<int64_t>(t.max_psize, ps);
+          }
+        }
+        CUDA_OR_THROW(cudaMalloc(&t.pool, 4 * n));
+        CUDA_OR_THROW(cudaMalloc(&t.psize, 4 * n));
+        s->device_bytes += (int64_t)(8 * n);
+      }
     }
     do_upload_traces(*s, traces, 0);
     CUDA_OR_THROW(cudaDeviceSynchronize());
@@ -803,6 +930,10 @@ int sbs_sim_create(const sbs_experiment* points, int32_t n_points, const sbs_tra
       p.drops.assign(points[i].drops, points[i].drops + points[i].n_drops);
       p.deads.assign(points[i].deads, points[i].deads + points[i].n_deads);
       p.topo.assign(points[i].topology, points[i].topology + points[i].n_topology);
+      if (p.x.cluster.cache_enabled)
+        p.probes.assign(points[i].cluster.cache_probe_lens,
+                        points[i].cluster.cache_probe_lens + points[i].cluster.cache_n_probes);
+      p.x.cluster.cache_probe_lens = p.probes.empty() ? nullptr : p.probes.data();
       p.trace = trace_of_point ? trace_of_point[i] : i;
       if (p.trace < 0 || p.trace >= n_traces) throw Error{SBS_ERR_CONFIG, "trace index out of range"};
       initial_caps(p, s->traces[p.trace]);
@@ -812,7 +943,7 @@ int sbs_sim_create(const sbs_experiment* points, int32_t n_points, const sbs_tra
     order_points(*s);
     CUDA_OR_THROW(cudaMalloc(&s->d_pts, sizeof(sbs::DevPoint) * n_points));
     CUDA_OR_THROW(cudaMalloc(&s->d_res, sizeof(sbs::DevResult) * n_points));
-    CUDA_OR_THROW(cudaMalloc(&s->d_counter, 8 * sizeof(int)));
+    CUDA_OR_THROW(cudaMalloc(&s->d_counter, sbs_sim::kVariants * sizeof(int)));
     s->h_res.resize(n_points);
     upload_points(*s);
     return SBS_OK;
@@ -846,7 +977,7 @@ int sbs_sim_launch(sbs_sim* s, void* stream) {
 int32_t sbs_sim_launches_per_run(const sbs_sim* s) {
   // one des_kernel per variant group + finalize_kernel (memsets are not ours)
   int n = 1;
-  for (int v = 0; v < 6; ++v) n += s->group_begin[v + 1] > s->group_begin[v] ? 1 : 0;
+  for (int v = 0; v < sbs_sim::kVariants; ++v) n += s->group_begin[v + 1] > s->group_begin[v] ? 1 : 0;
   return n;
 }
 
@@ -963,6 +1094,8 @@ void sbs_sim_destroy(sbs_sim* s) {
     if (t.arr) cudaFree(t.arr);
     if (t.prompt) cudaFree(t.prompt);
     if (t.output) cudaFree(t.output);
+    if (t.pool) cudaFree(t.pool);
+    if (t.psize) cudaFree(t.psize);
   }
   if (s->d_pts) cudaFree(s->d_pts);
   if (s->d_res) cudaFree(s->d_res);
@@ -1014,7 +1147,9 @@ int sbs_run_experiments(const sbs_experiment* points, int32_t n_points, sbs_aggr
     std::vector<sbs_trace> st(tr.size());
     for (size_t k = 0; k < tr.size(); ++k)
       st[k] = sbs_trace{tr[k].arr.data(), tr[k].prompt.data(), tr[k].output.data(),
-                        (int64_t)tr[k].arr.size(), tr[k].digest};
+                        (int64_t)tr[k].arr.size(), tr[k].digest,
+                        tr[k].pool.empty() ? nullptr : tr[k].pool.data(),
+                        tr[k].psize.empty() ? nullptr : tr[k].psize.data()};
     sbs_sim* s = nullptr;
     int rc = sbs_sim_create(points, n_points, st.data(), (int32_t)st.size(), map.data(), 0, device, &s);
     if (rc != SBS_OK) return rc;
@@ -1034,7 +1169,7 @@ int sbs_prefill_allocate(const sbs_window_batch* b, void* stream) {
     CUDA_OR_THROW(cudaMemsetAsync(sc.d_err, 0, sizeof(int32_t), st));
     sbs::PbaaArgs a{b->n_windows, b->req_off, b->n_pending, b->dp_off, b->n_limit, b->req_id,
                     b->prompt_len, b->wait_in, b->caps, b->out_dp, b->out_rank, b->wait_out,
-                    b->flow, sc.d_err};
+                    b->flow, sc.d_err, b->hit_off, b->hit};
     CUDA_OR_THROW(sbs::launch_pbaa(a, st));
     CUDA_OR_THROW(cudaMemcpyAsync(sc.h_err, sc.d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CUDA_OR_THROW(cudaStreamSynchronize(st));
@@ -1063,7 +1198,7 @@ int sbs_prefill_allocate_async(const sbs_window_batch* b, int32_t* error_out, vo
   return guarded([&] {
     sbs::PbaaArgs a{b->n_windows, b->req_off, b->n_pending, b->dp_off, b->n_limit, b->req_id,
                     b->prompt_len, b->wait_in, b->caps, b->out_dp, b->out_rank, b->wait_out,
-                    b->flow, error_out};
+                    b->flow, error_out, b->hit_off, b->hit};
     CUDA_OR_THROW(sbs::launch_pbaa(a, (cudaStream_t)stream));
     return SBS_OK;
   });

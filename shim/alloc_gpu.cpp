@@ -75,15 +75,19 @@ struct WindowOut {
 // One cluster-window through the batched PBAA kernel.
 WindowOut run_window(std::span<sbsim::Request* const> pending,
                      std::span<sbsim::Request* const> fresh,
-                     const std::vector<sbsim::DpPlan>& dps, int n_limit) {
+                     const std::vector<sbsim::DpPlan>& dps, int n_limit, sbsim::AllocMode mode) {
   const size_t n = pending.size() + fresh.size(), D = dps.size();
+  // cache-aware: Len_hit(r, d) resolved against the caller's caches (the
+  // PrefixCache objects the DpPlans borrow, prefill_alloc.h:22)
+  const bool ca = mode == sbsim::AllocMode::kCacheAware;
   // layout in the staging block
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = align8(off + bytes); return o; };
   const size_t o_roff = take(16), o_np = take(4), o_doff = take(16), o_nl = take(4),
                o_id = take(8 * n), o_len = take(8 * n), o_win = take(4 * n), o_caps = take(8 * D),
                o_dp = take(4 * n), o_rank = take(4 * n), o_wout = take(4 * n),
-               o_flow = take(8), o_err = take(8);
+               o_flow = take(8), o_err = take(8), o_hoff = take(ca ? 16 : 0),
+               o_hit = take(ca ? 8 * n * D : 0);
   g_st.ensure(off + 64);
   unsigned char* h = g_st.host;
   int64_t roff[2] = {0, (int64_t)n}, doff[2] = {0, (int64_t)D};
@@ -101,6 +105,17 @@ WindowOut run_window(std::span<sbsim::Request* const> pending,
       ++i;
     }
   for (size_t d = 0; d < D; ++d) ((int64_t*)(h + o_caps))[d] = dps[d].c_avail;
+  if (ca) {
+    int64_t hoff[2] = {0, (int64_t)(n * D)};
+    std::memcpy(h + o_hoff, hoff, 16);
+    size_t r = 0;
+    for (auto* q : {&pending, &fresh})
+      for (sbsim::Request* req : *q) {
+        for (size_t d = 0; d < D; ++d)
+          ((int64_t*)(h + o_hit))[r * D + d] = sbsim::cache_hit_len(*req, dps[d]);
+        ++r;
+      }
+  }
   *(int32_t*)(h + o_err) = 0;
   unsigned char* g = g_st.dev;
   // one H2D of the whole block (inputs + zeroed error word), one kernel, one D2H
@@ -119,8 +134,10 @@ WindowOut run_window(std::span<sbsim::Request* const> pending,
   b.out_rank = (int32_t*)(g + o_rank);
   b.wait_out = (int32_t*)(g + o_wout);
   b.flow = (uint8_t*)(g + o_flow);
+  b.hit_off = ca ? (const int64_t*)(g + o_hoff) : nullptr;
+  b.hit = ca ? (const int64_t*)(g + o_hit) : nullptr;
   throw_rc(sbs_prefill_allocate_async(&b, (int32_t*)(g + o_err), g_st.stream));
-  Staging::check(cudaMemcpyAsync(h + o_caps, g + o_caps, off - o_caps, cudaMemcpyDeviceToHost,
+  Staging::check(cudaMemcpyAsync(h + o_caps, g + o_caps, o_err + 8 - o_caps, cudaMemcpyDeviceToHost,
                                  g_st.stream));
   Staging::check(cudaStreamSynchronize(g_st.stream));
   if (*(int32_t*)(h + o_err)) throw_rc(SBS_ERR_OVERFLOW);
@@ -150,10 +167,8 @@ Tokens capacity_after(const Request& req, const DpPlan& dp, AllocMode mode) {
 
 void greedy_dispatch(std::span<Request* const> queue, std::vector<DpPlan>& dps, AllocMode mode,
                      std::vector<Placement>& mapping, std::vector<Request*>& deferred) {
-  if (mode == AllocMode::kCacheAware)
-    throw ConfigError("cache-aware allocation is out of scope of the B200 path");
   // one phase == a window whose whole queue is "pending", never throttled
-  WindowOut w = run_window(queue, {}, dps, std::numeric_limits<int>::max());
+  WindowOut w = run_window(queue, {}, dps, std::numeric_limits<int>::max(), mode);
   std::vector<std::pair<int32_t, size_t>> placed;
   for (size_t i = 0; i < queue.size(); ++i) {
     if (w.dp[i] >= 0) placed.emplace_back(w.rank[i], i);
@@ -167,10 +182,8 @@ void greedy_dispatch(std::span<Request* const> queue, std::vector<DpPlan>& dps, 
 AllocationResult allocate_batch(std::span<Request* const> q_pending,
                                 std::span<Request* const> q_new, std::vector<DpPlan>& dps,
                                 int n_limit, AllocMode mode) {
-  if (mode == AllocMode::kCacheAware)
-    throw ConfigError("cache-aware allocation is out of scope of the B200 path");
   AllocationResult res;
-  WindowOut w = run_window(q_pending, q_new, dps, n_limit);
+  WindowOut w = run_window(q_pending, q_new, dps, n_limit, mode);
   const size_t n = q_pending.size() + q_new.size();
   auto req = [&](size_t i) { return i < q_pending.size() ? q_pending[i] : q_new[i - q_pending.size()]; };
   std::vector<std::pair<int32_t, size_t>> placed;

@@ -51,6 +51,7 @@ sbs_length_spec to_c(const LengthSpec& s) {
 // ExperimentConfig (config.h:66-75) -> sbs_experiment; fault arrays owned by `h`.
 struct CExp {
   sbs_experiment x{};
+  std::vector<int64_t> probes;
   std::vector<sbs_drop_fault> drops;
   std::vector<sbs_dead_fault> deads;
   std::vector<sbs_topology_fault> topo;
@@ -79,6 +80,9 @@ CExp to_c(const ExperimentConfig& cfg) {
   o.decode_per_kv_token_s = c.engine.decode_per_kv_token_s;
   o.decode_tokens_per_step = c.decode_tokens_per_step;
   o.cache_enabled = c.cache.enabled ? 1 : 0;
+  h.probes.assign(c.cache.probe_lens.begin(), c.cache.probe_lens.end());
+  o.cache_n_probes = (int32_t)h.probes.size();
+  o.cache_budget_tokens = c.cache.budget_tokens;
   const WorkloadSpec& w = cfg.workload;
   sbs_workload& ow = h.x.workload;
   ow.process = w.process == ArrivalProcess::kPoisson ? SBS_ARRIVAL_POISSON
@@ -111,30 +115,43 @@ CExp to_c(const ExperimentConfig& cfg) {
   h.x.n_deads = (int32_t)h.deads.size();
   h.x.topology = h.topo.data();
   h.x.n_topology = (int32_t)h.topo.size();
+  h.x.cluster.cache_probe_lens = h.probes.empty() ? nullptr : h.probes.data();
   return h;
 }
 
 struct CTrace {
   std::vector<int64_t> arr;
-  std::vector<int32_t> prompt, output;
+  std::vector<int32_t> prompt, output, pool, psize;
   uint64_t digest = 0;
   sbs_trace view() const {
-    return sbs_trace{arr.data(), prompt.data(), output.data(), (int64_t)arr.size(), digest};
+    return sbs_trace{arr.data(), prompt.data(), output.data(), (int64_t)arr.size(), digest,
+                     pool.empty() ? nullptr : pool.data(), psize.empty() ? nullptr : psize.data()};
   }
 };
 
 CTrace make_trace(const sbs_experiment& x) {
   CTrace t;
   int64_t n = 0;
-  throw_rc(sbs_generate_workload(&x.workload, x.seed, nullptr, nullptr, nullptr, 0, &n, &t.digest));
+  throw_rc(sbs_generate_workload(&x.workload, x.seed, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
+                                 &n, &t.digest));
+  const bool pfx = x.workload.shared_prefix_fraction > 0;
   t.arr.resize((size_t)std::max<int64_t>(n, 1));
   t.prompt.resize(t.arr.size());
   t.output.resize(t.arr.size());
+  if (pfx) {
+    t.pool.resize(t.arr.size());
+    t.psize.resize(t.arr.size());
+  }
   throw_rc(sbs_generate_workload(&x.workload, x.seed, t.arr.data(), t.prompt.data(),
-                                 t.output.data(), n, &n, &t.digest));
+                                 t.output.data(), pfx ? t.pool.data() : nullptr,
+                                 pfx ? t.psize.data() : nullptr, n, &n, &t.digest));
   t.arr.resize((size_t)n);
   t.prompt.resize((size_t)n);
   t.output.resize((size_t)n);
+  if (pfx) {
+    t.pool.resize((size_t)n);
+    t.psize.resize((size_t)n);
+  }
   return t;
 }
 

@@ -43,6 +43,29 @@ def records_windows(rec):
     return out
 
 
+def records_windows_ca(rec):
+    """Parse make_golden.pbaa_cache_windows records (windows with Len_hit)."""
+    out, i = [], 0
+    rec = [int(x) for x in rec]
+    while i < len(rec):
+        np_, nn, D, nlim = rec[i:i + 4]; i += 4
+        rows = [rec[i + 3 * k:i + 3 * k + 3] for k in range(np_ + nn)]; i += 3 * (np_ + nn)
+        caps = rec[i:i + D]; i += D
+        hits = [rec[i + D * k:i + D * k + D] for k in range(np_ + nn)]; i += D * (np_ + nn)
+        nm = rec[i]; i += 1
+        mapping = [rec[i + 2 * k:i + 2 * k + 2] for k in range(nm)]; i += 2 * nm
+        nd = rec[i]; i += 1
+        deferred = [rec[i + 2 * k:i + 2 * k + 2] for k in range(nd)]; i += 2 * nd
+        nt = rec[i]; i += 1
+        thr = rec[i:i + nt]; i += nt
+        caps_out = rec[i:i + D]; i += D
+        flow = bool(rec[i]); i += 1
+        out.append({"pending": rows[:np_], "new": rows[np_:], "caps": caps, "n_limit": nlim,
+                    "hits": hits, "mapping": mapping, "deferred": deferred, "throttled": thr,
+                    "caps_out": caps_out, "flow": flow})
+    return out
+
+
 def records_decodes(rec):
     out, i = [], 0
     rec = [int(x) for x in rec]

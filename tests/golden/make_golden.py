@@ -8,14 +8,17 @@ oracle/ref_harness.cpp; the GPU box only reads the committed outputs.
   cases.json                the parity cases (name -> config)
   sim_<case>.npz            per-request dispatch/prefill_start/first_token/
                             completion/status + aggregates + digest + counts
+  csv_sha256.json           sha256 of the reference's four report CSVs per case
   windows_short_3k.npz      every allocate_batch window of short_3k (inputs and
                             outputs), flat int64 records (ref_harness.cpp)
+  windows_cache_aware.npz   random cache-aware windows with their Len_hit matrices
   decodes_decode_dp32.npz   every select_decode_unit call of decode_dp32
   smoke_decode_dp32_30s.npz the __graft_entry__.smoke() fixture
 """
 from __future__ import annotations
 
 import copy
+import hashlib
 import json
 import shutil
 import sys
@@ -80,6 +83,15 @@ def cases():
                        faults={"dead": [{"instance": 3, "time_s": 40.0}],
                                "topology": [{"instance": 2, "time_s": 20.0, "healthy": False},
                                             {"instance": 2, "time_s": 30.0, "healthy": True}]})
+    cache = {"enabled": True, "probe_lens": [64, 256, 512, 1024], "budget_tokens": 3000}
+    cache_short = with_(s3k, workload__duration_s=8.0, workload__shared_prefix_fraction=0.6,
+                        workload__prefix_pool=6, workload__prefix_len=1024, cluster__cache=cache,
+                        scheduler__prefill_mode="cache_aware")
+    cache_pd = with_(cfg2(12.0, seed=3), workload__shared_prefix_fraction=0.5,
+                     workload__prefix_pool=12, workload__prefix_len=600,
+                     cluster__cache={"enabled": True, "probe_lens": [32, 128, 512, 600],
+                                     "budget_tokens": 1500},
+                     scheduler__prefill_mode="cache_aware")
     return {
         "short_3k": s3k,
         "short_3k_immediate": with_(s3k, scheduler__policy="immediate"),
@@ -100,6 +112,14 @@ def cases():
         "overload_dp1": with_(s3k, cluster__dp_degree=1, workload__duration_s=6.0,
                               cluster__n_limit=3),
         "nlimit0": with_(s3k, cluster__dp_degree=2, workload__duration_s=4.0, cluster__n_limit=0),
+        # cache-aware PBAA + per-DP PrefixCache
+        "cache_short": cache_short,
+        "cache_short_basic": with_(cache_short, scheduler__prefill_mode="basic"),
+        "cache_short_tiny_budget": with_(cache_short, cluster__cache__budget_tokens=300,
+                                         cluster__cache__probe_lens=[32, 128, 256, 128]),
+        "cache_pd": cache_pd,
+        "cache_pd_dp33": with_(cache_pd, cluster__dp_degree=33, cluster__n_instances_prefill=2,
+                               workload__prefix_pool=40, sim__seed=5),
     }
 
 
@@ -114,6 +134,36 @@ def dump_sim(name, cfg, path):
     print(f"{name}: n={r['n']} completed={int(r['agg']['completed'])} digest={r['digest']:016x}")
 
 
+def pbaa_cache_windows(path, n=400, seed=99):
+    """Random cache-aware allocate_batch windows with given Len_hit matrices.
+
+    Flat records: [n_pending, n_new, D, n_limit, (id,len,wait)*, caps*D,
+    hits*(n*D), n_map, (id,dp)*, n_def, (id,wait)*, n_thr, id*, caps_out*D, flow]."""
+    rng = np.random.default_rng(seed)
+    rec = []
+    for w in range(n):
+        D = int(rng.choice([1, 2, 3, 8, 17, 33, 64]))
+        npend, nnew = int(rng.integers(0, 24)), int(rng.integers(0, 40))
+        k = npend + nnew
+        ids = rng.permutation(10 * k + 10)[:k]
+        lens = rng.integers(1, 3000, k)
+        if k and rng.random() < 0.3:
+            lens[rng.integers(0, k, k // 2)] = lens[0]  # prompt ties
+        waits = rng.integers(0, 5, k) * (np.arange(k) < npend)
+        caps = rng.integers(-500, 4000, D)
+        hits = np.where(rng.random((k, D)) < 0.4, rng.integers(0, 3000, (k, D)), 0)
+        hits = np.minimum(hits, lens[:, None])
+        nlim = int(rng.integers(0, 6))
+        rows = np.stack([ids, lens, waits], 1) if k else np.zeros((0, 3), np.int64)
+        r = ref.allocate_batch(rows[:npend], rows[npend:], caps.copy(), nlim, hits=hits)
+        rec += [npend, nnew, D, nlim] + rows.ravel().tolist() + caps.tolist() + hits.ravel().tolist()
+        rec += [len(r["mapping"])] + r["mapping"].ravel().tolist()
+        rec += [len(r["deferred"])] + r["deferred"].ravel().tolist()
+        rec += [len(r["throttled"])] + r["throttled"].tolist() + r["caps"].tolist() + [int(r["flow"])]
+    np.savez_compressed(path, records=np.array(rec, np.int64))
+    print("cache-aware windows:", n)
+
+
 def main():
     (HERE / "configs").mkdir(exist_ok=True)
     if REF_CONFIGS.exists():
@@ -121,8 +171,12 @@ def main():
             shutil.copy(f, HERE / "configs" / f.name)
     cs = cases()
     json.dump(cs, open(HERE / "cases.json", "w"), indent=1)
+    sha = {}
     for name, cfg in cs.items():
         dump_sim(name, cfg, HERE / f"sim_{name}.npz")
+        csv = ref.run(cfg, csv=True)["csv"]
+        sha[name] = {k: hashlib.sha256(v.encode()).hexdigest() for k, v in csv.items()}
+    json.dump(sha, open(HERE / "csv_sha256.json", "w"), indent=1, sort_keys=True)
     smoke = with_(load("decode_dp32"), workload__duration_s=30.0,
                   workload__output={"dist": "uniform", "min": 20, "max": 60},
                   sim__warmup_fraction=0.2)
@@ -134,6 +188,7 @@ def main():
     r = ref.run(load("short_3k"), windows=True)
     np.savez_compressed(HERE / "windows_short_3k.npz", records=r["windows"])
     print("windows:", r["alloc_calls"])
+    pbaa_cache_windows(HERE / "windows_cache_aware.npz")
     r = ref.run(load("decode_dp32"), decodes=True)
     np.savez_compressed(HERE / "decodes_decode_dp32.npz", records=r["decodes"])
     print("decodes:", r["decode_selects"])

@@ -42,10 +42,43 @@ def test_library_is_sm100a_cubin():
 
 def test_struct_sizes_match_header():
     # layout guard between include/sbs_b200.h and the ctypes mirror
-    assert ctypes.sizeof(P.api.Cluster) == 128
+    assert ctypes.sizeof(P.api.Cluster) == 144
     assert ctypes.sizeof(P.api.LengthSpec) == 48
+    assert ctypes.sizeof(P.api.Trace) == 56
+    assert ctypes.sizeof(P.api.WindowBatch) == 8 + 14 * 8
     assert ctypes.sizeof(P.api.Experiment) == ctypes.sizeof(P.api.Cluster) + \
         ctypes.sizeof(P.api.Workload) + 4 * 4 + 8 + 8 + 3 * 8 + 8
+
+
+def test_struct_layouts_match_c_compiler(tmp_path):
+    """sizeof/offsetof of every ABI struct as gcc sees include/sbs_b200.h."""
+    import shutil
+    import subprocess
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc absent")
+    A = P.api
+    structs = {"sbs_cluster": A.Cluster, "sbs_length_spec": A.LengthSpec, "sbs_workload": A.Workload,
+               "sbs_experiment": A.Experiment, "sbs_trace": A.Trace, "sbs_aggregates": A.Aggregates,
+               "sbs_histograms": A.Histograms, "sbs_window_batch": A.WindowBatch,
+               "sbs_decode_batch": A.DecodeBatch}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "sbs_b200.h"', "int main(void){"]
+    for cn, py in structs.items():
+        lines.append(f'printf("{cn} %zu\\n", sizeof({cn}));')
+        for f, _ in py._fields_:
+            if not f.startswith("_"):
+                lines.append(f'printf("{cn}.{f} %zu\\n", offsetof({cn}, {f}));')
+    lines.append("return 0;}")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(l.rsplit(" ", 1) for l in subprocess.run([str(exe)], capture_output=True,
+                                                           text=True).stdout.splitlines())
+    for cn, py in structs.items():
+        assert int(got[cn]) == ctypes.sizeof(py), cn
+        for f, _ in py._fields_:
+            if not f.startswith("_"):
+                assert int(got[f"{cn}.{f}"]) == getattr(py, f).offset, f"{cn}.{f}"
 
 
 @pytest.mark.parametrize("name", sorted(CASES))
@@ -98,8 +131,26 @@ def test_validate_errors_are_config_errors():
 
 
 def test_gpu_envelope_is_explicit():
-    rc, msg = _sim_create_rc({"scheduler": {"prefill_mode": "cache_aware"}})
-    assert rc == 1 and "out of scope" in msg
+    rc, msg = _sim_create_rc({"cluster": {"dp_degree": 129}})
+    assert rc == 1 and msg == "GPU path supports dp_degree <= 128"
+    rc, msg = _sim_create_rc({"cluster": {"cache": {"enabled": True,
+                                                    "probe_lens": list(range(1, 40)),
+                                                    "budget_tokens": 10}},
+                              "scheduler": {"prefill_mode": "cache_aware"}})
+    assert rc == 1 and msg == "GPU path supports at most 32 distinct probe lengths"
+
+
+def test_cache_settings_validated_like_reference():
+    # core.cpp:106-113
+    rc, msg = _sim_create_rc({"cluster": {"cache": {"enabled": True, "budget_tokens": 10}}})
+    assert rc == 1 and msg == "cache.probe_lens must be non-empty when the cache is enabled"
+    rc, msg = _sim_create_rc({"cluster": {"cache": {"enabled": True, "probe_lens": [0],
+                                                    "budget_tokens": 10}}})
+    assert rc == 1 and msg == "cache.probe_lens entries must be >= 1"
+    rc, msg = _sim_create_rc({"cluster": {"cache": {"enabled": True, "probe_lens": [8]}}})
+    assert rc == 1 and msg == "cache.budget_tokens must be >= 1 when the cache is enabled"
+    rc, msg = _sim_create_rc({"workload": {"shared_prefix_fraction": 0.5}})
+    assert rc == 1 and "prefix_pool and prefix_len must be positive" in msg
 
 
 @pytest.mark.skipif(HAS_GPU, reason="checks the no-GPU behaviour")

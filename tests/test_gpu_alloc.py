@@ -7,7 +7,7 @@ import pytest
 
 import paper_2512_16134_b200 as P
 from oracle import orc
-from tests.common import GOLD, records_decodes, records_windows
+from tests.common import GOLD, records_decodes, records_windows, records_windows_ca
 
 pytestmark = pytest.mark.gpu
 
@@ -27,6 +27,19 @@ def _csr(windows):
 def test_recorded_windows_short_3k():
     wins = records_windows(np.load(GOLD / "windows_short_3k.npz")["records"])
     got = P.allocate_batch([{k: w[k] for k in ("pending", "new", "caps", "n_limit")} for w in wins])
+    for w, g in zip(wins, got):
+        assert g["mapping"].tolist() == w["mapping"]
+        assert g["deferred"].tolist() == w["deferred"]
+        assert g["throttled"].tolist() == w["throttled"]
+        assert g["caps"].tolist() == w["caps_out"]
+        assert g["flow"] == w["flow"]
+
+
+def test_recorded_windows_cache_aware():
+    """Cache-aware windows (Len_hit per request x DP) vs the reference's outputs."""
+    wins = records_windows_ca(np.load(GOLD / "windows_cache_aware.npz")["records"])
+    got = P.allocate_batch([{k: w[k] for k in ("pending", "new", "caps", "n_limit", "hits")}
+                            for w in wins])
     for w, g in zip(wins, got):
         assert g["mapping"].tolist() == w["mapping"]
         assert g["deferred"].tolist() == w["deferred"]

@@ -166,3 +166,39 @@ def test_config5_replica_full_size():
         assert agg_close(g["agg"][k], r["agg"][k]), k
     assert g["agg"]["alloc_calls"] == r["alloc_calls"]
     assert g["agg"]["decode_selects"] == r["decode_selects"]
+
+
+def test_cache_aware_random_vs_reference():
+    """Cache-aware PBAA + per-DP prefix caches on random settings:
+    pool sizes, prefix lengths, probe sets (with repeats), budgets that evict
+    constantly or never, DP degrees on both kernel variants."""
+    from oracle import orc
+    rng = np.random.default_rng(4242)
+    for t in range(24):
+        c = copy.deepcopy(CASES[["cache_short", "cache_pd"][t % 2]])
+        c["workload"]["duration_s"] = float(rng.uniform(2, 10))
+        c["workload"]["shared_prefix_fraction"] = float(rng.choice([0.1, 0.6, 1.0]))
+        c["workload"]["prefix_pool"] = int(rng.integers(1, 50))
+        c["workload"]["prefix_len"] = int(rng.choice([8, 300, 1200, 4000]))
+        c["cluster"]["dp_degree"] = int(rng.choice([1, 3, 8, 20, 40]))
+        c["cluster"]["n_instances_prefill"] = int(rng.integers(1, 6))
+        probes = [int(x) for x in rng.integers(1, 1500, int(rng.integers(1, 9)))]
+        c["cluster"]["cache"] = {"enabled": True, "probe_lens": probes + probes[:1],
+                                 "budget_tokens": int(rng.choice([1, 150, 2500, 10**7]))}
+        c["sim"]["seed"] = int(rng.integers(0, 10**6))
+        g = P.run_experiment(c, per_request=True)
+        if HAVE_REF:
+            r = ref.run(c, per_request=True)
+            rq = r["requests"]
+            want = {"dispatch": rq[:, 4], "prefill_start": rq[:, 5], "first_token": rq[:, 6],
+                    "completion": rq[:, 7], "status": rq[:, 3].astype(np.int8), "agg": r["agg"],
+                    "alloc_calls": r["alloc_calls"]}
+        else:
+            tr = g["trace"]
+            r = orc.run(c, tr.arrival_ns, tr.prompt_len, tr.output_len,
+                        prefix_pool=tr.prefix_pool_id, prefix_size=tr.prefix_size)
+            rq = r["requests"]
+            want = {"status": rq[:, 0].astype(np.int8), "dispatch": rq[:, 1],
+                    "prefill_start": rq[:, 2], "first_token": rq[:, 3], "completion": rq[:, 4],
+                    "agg": r["agg"], "alloc_calls": r["agg"]["alloc_calls"]}
+        check_against(f"cache#{t}", g["requests"], g["agg"], want)

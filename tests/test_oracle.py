@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 from oracle import orc, ref
-from tests.common import GOLD, records_decodes, records_windows
+from tests.common import GOLD, records_decodes, records_windows, records_windows_ca
 
 HAVE_REF = ref.available()
 
@@ -62,6 +62,26 @@ def test_recorded_windows_short_3k():
         assert r["throttled"].tolist() == w["throttled"]
         assert r["caps"].tolist() == w["caps_out"]
         assert r["flow"] == w["flow"]
+
+
+def test_recorded_windows_cache_aware():
+    """Cache-aware allocate_batch (capacity_after with Len_hit) vs windows the
+    reference computed with its own PrefixCache (make_golden.pbaa_cache_windows)."""
+    wins = records_windows_ca(np.load(GOLD / "windows_cache_aware.npz")["records"])
+    assert len(wins) == 400
+    for w in wins:
+        r = orc.allocate_batch(w["pending"], w["new"], w["caps"], w["n_limit"], hits=w["hits"])
+        assert r["mapping"].tolist() == w["mapping"]
+        assert r["deferred"].tolist() == w["deferred"]
+        assert r["throttled"].tolist() == w["throttled"]
+        assert r["caps"].tolist() == w["caps_out"]
+        assert r["flow"] == w["flow"]
+
+
+def test_spec_cache_aware_example():
+    # SPEC.md:342: L=1000, DP0 c_avail=1000/hit=0, DP1 c_avail=800/hit=900 -> DP1
+    r = orc.allocate_batch([], [[1, 1000, 0]], [1000, 800], 8, hits=[[0, 900]])
+    assert r["mapping"].tolist() == [[1, 1]] and r["caps"].tolist() == [1000, 700]
 
 
 def test_recorded_decodes_decode_dp32():

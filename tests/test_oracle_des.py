@@ -6,6 +6,7 @@ import copy
 import numpy as np
 import pytest
 
+import paper_2512_16134_b200 as P
 from oracle import orc, ref
 from tests.common import CASES, load_case
 
@@ -27,10 +28,25 @@ def _check(name, got, want_req, want_agg):
         assert got["agg"][k] == want_agg[k], f"{name}: {k} {got['agg'][k]!r} vs {want_agg[k]!r}"
 
 
+def _prefixes(cfg, g):
+    """Shared-prefix columns of a golden trace.  The reference harness exports
+    (arrival, prompt, output) only; the prefixes come from the host generator,
+    whose workload_digest (which folds in every request's first prefix token
+    and prefix size, workload.cpp:153-159) must equal the reference's."""
+    if cfg.get("workload", {}).get("shared_prefix_fraction", 0) <= 0:
+        return None, None
+    tr = P.generate_workload(cfg)
+    assert tr.digest == int(g["digest"])
+    assert np.array_equal(tr.prompt_len, g["prompt"])
+    return tr.prefix_pool_id, tr.prefix_size
+
+
 @pytest.mark.parametrize("name", sorted(CASES))
 def test_des_restatement_matches_reference_fixtures(name):
     g = load_case(name)
-    out = orc.run(CASES[name], g["arrival"], g["prompt"], g["output"])
+    pp, ps = _prefixes(CASES[name], g)
+    out = orc.run(CASES[name], g["arrival"], g["prompt"], g["output"], prefix_pool=pp,
+                  prefix_size=ps)
     assert out["agg"]["error"] == 0
     _check(name, out, g, g["agg"])
     assert out["agg"]["alloc_calls"] == int(g["alloc_calls"])
@@ -54,3 +70,29 @@ def test_des_restatement_random_vs_reference():
         want = {"status": rq[:, 3], "dispatch": rq[:, 4], "prefill_start": rq[:, 5],
                 "first_token": rq[:, 6], "completion": rq[:, 7]}
         _check(f"random#{t}", orc.run(c, a, p, o), want, r["agg"])
+
+
+@pytest.mark.skipif(not ref.available(), reason="compiled reference unavailable")
+def test_des_restatement_cache_aware_random_vs_reference():
+    """Cache-aware PBAA + per-DP PrefixCache on random settings (SURVEY 8f #3)."""
+    rng = np.random.default_rng(77)
+    for t in range(16):
+        c = copy.deepcopy(CASES[["cache_short", "cache_pd"][t % 2]])
+        c["workload"]["duration_s"] = float(rng.uniform(2, 8))
+        c["workload"]["shared_prefix_fraction"] = float(rng.choice([0.2, 0.7, 1.0]))
+        c["workload"]["prefix_pool"] = int(rng.integers(1, 30))
+        c["workload"]["prefix_len"] = int(rng.choice([16, 300, 2000]))
+        c["cluster"]["dp_degree"] = int(rng.choice([1, 3, 8, 20]))
+        c["cluster"]["cache"] = {"enabled": True,
+                                 "probe_lens": [int(x) for x in rng.integers(1, 1500, int(rng.integers(1, 6)))],
+                                 "budget_tokens": int(rng.choice([1, 200, 2000, 100000]))}
+        c["sim"]["seed"] = int(rng.integers(0, 10**6))
+        a, p, o, dg = ref.generate_workload(c)
+        tr = P.generate_workload(c)
+        assert tr.digest == dg
+        r = ref.run(c, per_request=True)
+        rq = r["requests"]
+        want = {"status": rq[:, 3], "dispatch": rq[:, 4], "prefill_start": rq[:, 5],
+                "first_token": rq[:, 6], "completion": rq[:, 7]}
+        _check(f"cache#{t}", orc.run(c, a, p, o, prefix_pool=tr.prefix_pool_id,
+                                     prefix_size=tr.prefix_size), want, r["agg"])
