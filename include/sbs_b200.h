@@ -218,6 +218,9 @@ int sbs_sim_log(sbs_sim* sim, int32_t point, int64_t* words, int64_t cap, int64_
  * counters summed over replicas (non-zero only in an SBS_PROF=1 build). */
 #define SBS_PROF_COUNTERS 24
 int sbs_sim_profile_counters(const sbs_sim* sim, int64_t* out);
+/* Device time of the DES kernels of the last sbs_sim_launch (CUDA events on
+ * its stream, finalize excluded); waits for them to finish. */
+int sbs_sim_des_ms(sbs_sim* sim, double* ms);
 /* Number of kernel launches enqueued by one sbs_sim_launch. */
 int32_t sbs_sim_launches_per_run(const sbs_sim* sim);
 /* Device bytes allocated for this simulator. */

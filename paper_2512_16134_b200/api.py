@@ -178,6 +178,7 @@ def lib():
         L.sbs_sim_log.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64,
                                   C.POINTER(C.c_int64)]
         L.sbs_sim_launches_per_run.argtypes = [C.c_void_p]
+        L.sbs_sim_des_ms.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
         L.sbs_sim_profile_counters.argtypes = [C.c_void_p, C.c_void_p]
         L.sbs_sim_device_bytes.argtypes = [C.c_void_p]
         L.sbs_sim_device_bytes.restype = C.c_int64
@@ -197,7 +198,7 @@ EXPORTED_SYMBOLS = [
     "sbs_sim_device_bytes",
     "sbs_sim_destroy", "sbs_run_experiments", "sbs_prefill_allocate",
     "sbs_prefill_allocate_async", "sbs_decode_select", "sbs_decode_select_async",
-    "sbs_last_error", "sbs_version", "sbs_sim_profile_counters",
+    "sbs_last_error", "sbs_version", "sbs_sim_profile_counters", "sbs_sim_des_ms",
 ]
 
 
@@ -506,6 +507,12 @@ class Simulator:
         out = (C.c_int64 * 24)()
         lib().sbs_sim_profile_counters(self.handle, out)
         return list(out)
+
+    def des_ms(self):
+        """Device ms of the DES kernels of the last launch (CUDA events)."""
+        ms = C.c_double(0)
+        _check(lib().sbs_sim_des_ms(self.handle, C.byref(ms)))
+        return ms.value
 
     @property
     def launches_per_run(self):

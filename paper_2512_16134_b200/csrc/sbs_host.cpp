@@ -374,6 +374,7 @@ struct sbs_sim {
   int64_t device_bytes = 0;
   int sm_count = 148;
   int pair_mode = 2;  // two-warp replicas: 1 = one CTA, 2 = a 2-CTA cluster (SBS_SPLIT)
+  cudaEvent_t ev_des[2] = {nullptr, nullptr};  // around the DES kernels of the last launch
 };
 
 namespace {
@@ -673,6 +674,11 @@ void order_points(sbs_sim& s) {
 
 void launch_all(sbs_sim& s, cudaStream_t st) {
   s.n_launches = 0;
+  if (s.ev_des[0] == nullptr) {
+    CUDA_OR_THROW(cudaEventCreate(&s.ev_des[0]));
+    CUDA_OR_THROW(cudaEventCreate(&s.ev_des[1]));
+  }
+  CUDA_OR_THROW(cudaEventRecord(s.ev_des[0], st));
   for (int v = 0; v < sbs_sim::kVariants; ++v) {
     const int b = s.group_begin[v], e = s.group_begin[v + 1];
     if (e <= b) continue;
@@ -693,6 +699,7 @@ void launch_all(sbs_sim& s, cudaStream_t st) {
                                   s.smem_per_warp, wpb, blocks, st));
     s.n_launches += 1;
   }
+  CUDA_OR_THROW(cudaEventRecord(s.ev_des[1], st));
   CUDA_OR_THROW(sbs::launch_finalize(s.d_pts, (int)s.order.size(), s.d_res, st));
   s.n_launches += 1;
 }
@@ -983,6 +990,18 @@ int32_t sbs_sim_launches_per_run(const sbs_sim* s) {
 
 int64_t sbs_sim_device_bytes(const sbs_sim* s) { return s->device_bytes; }
 
+int sbs_sim_des_ms(sbs_sim* s, double* ms) {
+  return guarded([&] {
+    if (s->ev_des[0] == nullptr) throw Error{SBS_ERR_INVARIANT, "no launch recorded"};
+    CUDA_OR_THROW(cudaSetDevice(s->device));
+    CUDA_OR_THROW(cudaEventSynchronize(s->ev_des[1]));
+    float f = 0.f;
+    CUDA_OR_THROW(cudaEventElapsedTime(&f, s->ev_des[0], s->ev_des[1]));
+    *ms = (double)f;
+    return SBS_OK;
+  });
+}
+
 int sbs_sim_results(sbs_sim* s, sbs_aggregates* out, sbs_histograms* hist, void* stream) {
   return guarded([&] {
     cudaStream_t st = (cudaStream_t)stream;
@@ -1100,6 +1119,8 @@ void sbs_sim_destroy(sbs_sim* s) {
   if (s->d_pts) cudaFree(s->d_pts);
   if (s->d_res) cudaFree(s->d_res);
   if (s->d_counter) cudaFree(s->d_counter);
+  for (auto& e : s->ev_des)
+    if (e) cudaEventDestroy(e);
   delete s;
 }
 
