@@ -662,36 +662,31 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     // (double)K <= th  <=>  K <= floor(th) for integer K < 2^53
     const double fth = floor(th);
     const int64_t thi = fth >= 281474976710656.0 ? (int64_t)kKMask : (fth < 0.0 ? -1 : (int64_t)fth);
-    uint64_t bs = UINT64_MAX, ba = UINT64_MAX;
-    int ps = 0x7fffffff, pa = 0x7fffffff, ns = 0;
+    // safe set empty <=> min K > th (fallback); a proper subset <=> max K > th
+    // (mask): both read off the sorted multiset, so the scan needs no count
+    const bool fallback = (int64_t)s_S[0] > thi;
+    if (fallback) CNT(fb, 1);
+    else if ((int64_t)s_S[nul - 1] > thi) CNT(mask, 1);
+    // lexicographic (B, K, position) as one u64: B << 48 | K << 16 | position
+    // (K < 2^32, position < 2^16)
+    uint64_t best = UINT64_MAX;
     if (ul_ident) {
       for (int i = lane; i < nul; i += 32) {
         const uint64_t k = s_PK[i];
-        const bool safe = (int64_t)(k & kKMask) <= thi;
-        ns += safe;
-        if (safe && k < bs) { bs = k; ps = i; }
-        if (k < ba) { ba = k; pa = i; }
+        const uint64_t c = (k & ~kKMask) | ((k & kKMask) << 16) | (uint64_t)i;
+        if ((fallback || (int64_t)(k & kKMask) <= thi) && c < best) best = c;
       }
     } else {
       for (int i = lane; i < nul; i += 32) {
         const uint64_t k = s_PK[s_ul[i]];
-        const bool safe = (int64_t)(k & kKMask) <= thi;
-        ns += safe;
-        if (safe && k < bs) { bs = k; ps = i; }
-        if (k < ba) { ba = k; pa = i; }
+        const uint64_t c = (k & ~kKMask) | ((k & kKMask) << 16) | (uint64_t)i;
+        if ((fallback || (int64_t)(k & kKMask) <= thi) && c < best) best = c;
       }
     }
-    ns = __reduce_add_sync(kFull, ns);
-    const bool fallback = ns == 0;
-    if (fallback) CNT(fb, 1);
-    else if (ns < nul) CNT(mask, 1);
-    const uint64_t key = fallback ? ba : bs;
-    const int pos = fallback ? pa : ps;
-    // key = B << 48 | K with K < 2^32: minimise (B, K, position) with 32-bit REDUX
-    const uint32_t kb = (uint32_t)(key >> 48), kk = (uint32_t)key;
-    const uint32_t mb = __reduce_min_sync(kFull, kb);
-    const uint32_t mk = __reduce_min_sync(kFull, kb == mb ? kk : 0xffffffffu);
-    const int sel = (int)__reduce_min_sync(kFull, (kb == mb && kk == mk) ? (uint32_t)pos : 0x7fffffffu);
+    const uint32_t hi = (uint32_t)(best >> 32);
+    const uint32_t mh = __reduce_min_sync(kFull, hi);
+    const uint32_t ml = __reduce_min_sync(kFull, hi == mh ? (uint32_t)best : 0xffffffffu);
+    const int sel = (int)(ml & 0xffffu);
     PROF_END(5);
     return sel;
   };
@@ -1575,6 +1570,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       } else {
         kind = 1;
       }
+      int step_j = -1;  // decode step handled: begin its next step after the drain
       if (kind == 0) {
         // ---- hand_off_finished (simulation.cpp:397-411) of one EndForward
         now = th;
@@ -1590,9 +1586,6 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         ndw += nk;
         rhead += 1;
         khead += nk;
-        PROF_BEGIN(4);
-        drain_decode();
-        PROF_END(4);
       } else if (kind == 1) {
         // ---- on_decode_step (simulation.cpp:497-512)
         now = td;
@@ -1606,12 +1599,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         finish_step(j);
         PROF_END(3);
         d_hk = 1;
-        PROF_BEGIN(15);
-        drain_decode();
-        PROF_END(15);
-        PROF_BEGIN(10);
-        if (!error) try_begin_step(j);
-        PROF_END(10);
+        step_j = j;
       } else {
         // ---- on_topology for a decode instance (simulation.cpp:382-388)
         now = tt;
@@ -1623,6 +1611,12 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         ul_dirty = true;
         S_valid = false;
         S_gathered = false;
+      }
+      if (kind != 2) {  // one call site: drain_decode is the largest inlined body
+        PROF_BEGIN(4);
+        drain_decode();
+        PROF_END(4);
+        if (step_j >= 0 && !error) try_begin_step(step_j);
       }
       if (error) aborted = true;
     }
