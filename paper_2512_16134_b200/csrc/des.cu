@@ -709,13 +709,17 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   };
 
   // drain_decode_admissions (simulation.cpp:413-484)
-  auto drain_decode = [&]() {
-    if (ndw == 0) return;
-    for (int j = 0; j < Dn; ++j) maybe_die_d(j);
-    warp_sort_buf(g_dwait, ndw);
+  // then_j >= 0: the decode step just finished on instance then_j, whose
+  // handler calls try_begin_decode_step after the drain (simulation.cpp:511);
+  // it joins the drain's own begins (a second begin of a touched instance is
+  // a no-op), so try_begin_step has a single call site.
+  auto drain_decode = [&](int then_j) {
     uint32_t touched = 0;
-    int32_t order_lane = -1;  // lane t holds the t-th touched instance
+    int32_t order_lane = -1;  // lane t holds the t-th instance to begin
     int ntouched = 0;
+    if (ndw > 0) {
+    for (int j = 0; j < Dn; ++j) maybe_die_d(j);
+    warp_sort_buf<true>(g_dwait, ndw);
     int wi = 0;
     uint64_t w_key = 0;
     int32_t w_prompt = 0, w_out = 0;
@@ -803,6 +807,11 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       }
     }
     ndw -= wi;
+    }
+    if (then_j >= 0 && !(touched & (1u << then_j))) {
+      if (lane == ntouched) order_lane = then_j;
+      ntouched += 1;
+    }
     for (int t = 0; t < ntouched; ++t) try_begin_step(bcast(order_lane, t));
   };
 
@@ -1364,8 +1373,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     (void)rel;
     const bool band_fast = !LOG && Dn == 1 && now >= warmup;
     // one interleaved butterfly for every per-step reduction (their shuffle
-    // latencies overlap instead of chaining)
-#pragma unroll
+    // latencies overlap instead of chaining); kept rolled (code size)
+#pragma unroll 1
     for (int o = 16; o > 0; o >>= 1) {
       const double w = __shfl_xor_sync(kFull, worst, o);
       const int64_t ex = __shfl_xor_sync(kFull, exc, o);
@@ -1614,9 +1623,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       }
       if (kind != 2) {  // one call site: drain_decode is the largest inlined body
         PROF_BEGIN(4);
-        drain_decode();
+        drain_decode(step_j);
         PROF_END(4);
-        if (step_j >= 0 && !error) try_begin_step(step_j);
       }
       if (error) aborted = true;
     }
@@ -1774,12 +1782,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     // ---- decode hand-off: hand_off_finished / on_decode_step tail
     if (ROLE == 0 && (kind == kEvEF || kind == kEvDS)) {
       PROF_BEGIN(4);
-      drain_decode();
+      drain_decode(step_j);
       PROF_END(4);
       if (error) break;
-      PROF_BEGIN(10);
-      if (step_j >= 0) try_begin_step(step_j);
-      PROF_END(10);
     }
     PROF_BEGIN(9);
     // ---- prefill passes and the SBS dispatch chain

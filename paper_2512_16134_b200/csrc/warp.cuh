@@ -66,32 +66,42 @@ __device__ __forceinline__ double warp_sum_f64(double v) {
 }
 
 // In-register bitonic sort of one uint64 key per lane, ascending by lane.
+// ROLLED: loops kept rolled where the caller is instruction-cache bound.
+__device__ __forceinline__ uint64_t bitonic_step(uint64_t x, int lane, int k, int j) {
+  const uint64_t y = __shfl_xor_sync(kFull, x, j);
+  const bool up = (lane & k) == 0;
+  const bool lower = (lane & j) == 0;
+  // lower lane keeps min when ascending block, max when descending
+  const bool take_min = (lower == up);
+  const uint64_t mn = x < y ? x : y, mx = x < y ? y : x;
+  return take_min ? mn : mx;
+}
+template <bool ROLLED = false>
 __device__ __forceinline__ uint64_t warp_sort32(uint64_t x) {
   const int lane = lane_id();
+  if constexpr (ROLLED) {
+#pragma unroll 1
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll 1
+      for (int j = k >> 1; j > 0; j >>= 1) x = bitonic_step(x, lane, k, j);
+  } else {
 #pragma unroll
-  for (int k = 2; k <= 32; k <<= 1) {
+    for (int k = 2; k <= 32; k <<= 1)
 #pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      uint64_t y = __shfl_xor_sync(kFull, x, j);
-      bool up = (lane & k) == 0;
-      bool lower = (lane & j) == 0;
-      // lower lane keeps min when ascending block, max when descending
-      bool take_min = (lower == up);
-      uint64_t mn = x < y ? x : y, mx = x < y ? y : x;
-      x = take_min ? mn : mx;
-    }
+      for (int j = k >> 1; j > 0; j >>= 1) x = bitonic_step(x, lane, k, j);
   }
   return x;
 }
 
 // Warp bitonic sort of n keys (ascending) in a buffer of capacity >= pow2(n)
 // (generic pointer: shared or global).  Pads with UINT64_MAX.
+template <bool ROLLED = false>
 __device__ __forceinline__ void warp_sort_buf(uint64_t* buf, int n) {
   const int lane = lane_id();
   if (n <= 1) return;
   if (n <= 32) {
     uint64_t x = lane < n ? buf[lane] : UINT64_MAX;
-    x = warp_sort32(x);
+    x = warp_sort32<ROLLED>(x);
     if (lane < n) buf[lane] = x;
     __syncwarp();
     return;
@@ -147,8 +157,10 @@ __device__ __forceinline__ void warp_radix_sort(Key* a, Key* t, uint32_t* hist, 
   Key* dst = t;
   for (int p = 0; p < passes; ++p) {
     const int sh = 8 * p;
+#pragma unroll 1
     for (int b = lane; b < 256; b += 32) hist[b] = 0;
     __syncwarp();
+#pragma unroll 1
     for (int i = lane; i < n; i += 32) atomicAdd(&hist[(unsigned)(src[i] >> sh) & 255u], 1u);
     __syncwarp();
     uint32_t v[8];
@@ -165,6 +177,7 @@ __device__ __forceinline__ void warp_radix_sort(Key* a, Key* t, uint32_t* hist, 
 #pragma unroll
     for (int k = 0; k < 8; ++k) { hist[8 * lane + k] = run; run += v[k]; }
     __syncwarp();
+#pragma unroll 1
     for (int base = 0; base < n; base += 32) {
       const int i = base + lane;
       const bool valid = i < n;
