@@ -276,11 +276,14 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   }
 
   if (kPre)
+#pragma unroll 1
     for (int g = lane; g < PD; g += 32) {
       s_out[g] = 0; s_head[g] = 0; s_tail[g] = 0; s_rel[g] = 0; s_part[g] = 0;
     }
   if (kDec) {
+#pragma unroll 1
     for (int u = lane; u < U; u += 32) { s_PK[u] = 0; s_R[u] = 0; s_nst[u] = 0; }
+#pragma unroll 1
     for (int b = lane; b < Dn * R; b += 32) s_bcnt[b] = 0;
   }
   __syncwarp();
@@ -576,6 +579,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   //      capped units (simulation.cpp:432-442)
   auto rebuild_ulist = [&]() {
     int cnt = 0;
+#pragma unroll 1
     for (int base = 0; base < U; base += 32) {
       int u = base + lane;
       int fl = __shfl_sync(kFull, dflags, (u < U ? u / Dd : 0) & 31);
@@ -599,12 +603,14 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     if (!S_gathered) {
       mx = 0;
       if (ul_ident) {
+#pragma unroll 1
         for (int i = lane; i < nul; i += 32) {
           uint64_t k = s_PK[i] & kKMask;
           s_S[i] = (uint32_t)k;
           mx = k > mx ? k : mx;
         }
       } else {
+#pragma unroll 1
         for (int i = lane; i < nul; i += 32) {
           uint64_t k = s_PK[s_ul[i]] & kKMask;
           s_S[i] = (uint32_t)k;
@@ -697,6 +703,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     const int c_old = warp_lower_bound<uint32_t>(s_S, nul, o);
     const int c_new = warp_lower_bound<uint32_t>(s_S, nul, nv);
     // shift S[c_old+1 .. c_new-1] left by one, then S[c_new-1] = newv
+#pragma unroll 1
     for (int base = c_old; base < c_new - 1; base += 32) {
       int i = base + lane;
       uint32_t v = (i < c_new - 1) ? s_S[i + 1] : 0;
@@ -798,6 +805,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     }
     // keep unadmitted waiters (still sorted)
     if (wi > 0 && wi < ndw) {
+#pragma unroll 1
       for (int base = 0; base < ndw - wi; base += 32) {
         int i = base + lane;
         uint64_t v = (i < ndw - wi) ? g_dwait[wi + i] : 0;
@@ -1296,6 +1304,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     const int4* ent = g_buckets + (int64_t)b * BC;
     int64_t exc = 0, rel = 0;
     PROF_BEGIN(11);
+#pragma unroll 1
     for (int base = 0; base < n; base += 32) {
       int e = base + lane;
       bool has = e < n;
@@ -1349,6 +1358,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     const bool gather = ul_ident && Dn == 1;  // s_S order == unit order
     uint64_t mx = 0, s1 = 0, s2lo = 0, s2hi = 0;  // sum K, sum K^2 (128-bit)
     double worst = 0.0;
+#pragma unroll 1
     for (int d = lane; d < Dd; d += 32) {
       const int u = u0 + d;
       const uint64_t k = s_PK[u];
@@ -1435,6 +1445,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       if (live) {
         const bool all = live == (Dn == 32 ? 0xffffffffu : ((1u << Dn) - 1u));
         int64_t s1 = 0, cnt = 0, vmin = kInf64, vmax = -1;
+#pragma unroll 1
         for (int u = lane; u < U; u += 32) {
           if (all || ((live >> (u / Dd)) & 1u)) {
             const int64_t v = (int64_t)(s_PK[u] & kKMask);
@@ -1458,6 +1469,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
               }
           var = bcast(var, 0);
         } else {
+#pragma unroll 1
           for (int u = lane; u < U; u += 32) {
             if (all || ((live >> (u / Dd)) & 1u)) {
               const double dv = __dsub_rn((double)(int64_t)(s_PK[u] & kKMask), mean);
@@ -1591,6 +1603,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         // record's are released at the next one, or exactly before a wait)
         if (lane == 0) { chR->head = rhead; chR->khead = khead; }
         pub_head = rhead;
+#pragma unroll 1
         for (int i = lane; i < nk; i += 32) g_dwait[ndw + i] = chL->keys[(k0 + i) % kChanKeys];
         ndw += nk;
         rhead += 1;
