@@ -161,6 +161,10 @@ struct Counters {
 
 // Development instrumentation: -DSBS_PROF accumulates clock64() cycles per
 // region (inclusive) into DevResult::prof.  Compiled out by default.
+// Branch hints: cold paths leave the hot instruction stream (block layout).
+#define SBS_LIKELY(x) __builtin_expect(!!(x), 1)
+#define SBS_UNLIKELY(x) __builtin_expect(!!(x), 0)
+
 #ifdef SBS_PROF
 #define PROF_BEGIN(r) const long long _pt##r = clock64()
 #define PROF_END(r) prof_acc[r] += clock64() - _pt##r
@@ -653,7 +657,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     if (!S_valid) rebuild_S();
     PROF_END(7);
     PROF_BEGIN(5);
-    if (pc_n != nul) {
+    if (SBS_UNLIKELY(pc_n != nul)) {
       const double r25 = __ddiv_rn(__dmul_rn((double)nul - 1.0, 25.0), 100.0);
       const double r75 = __ddiv_rn(__dmul_rn((double)nul - 1.0, 75.0), 100.0);
       lo25 = (int)floor(r25); hi25 = (int)ceil(r25); fr25 = __dsub_rn(r25, (double)lo25);
@@ -733,7 +737,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     uint64_t w_key = 0;
     int32_t w_prompt = 0, w_out = 0;
     while (wi < ndw) {
-      if (ul_dirty) rebuild_ulist();
+      if (SBS_UNLIKELY(ul_dirty)) rebuild_ulist();
       if (nul == 0) break;
       if ((wi & 31) == 0) {  // next 32 waiters: keys + lengths fetched in parallel
         w_key = (wi + lane < ndw) ? g_dwait[wi + lane] : 0;
@@ -746,7 +750,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       const int32_t prompt = bcast(w_prompt, wi & 31);
       const int32_t out = bcast(w_out, wi & 31);
       int pos;
-      if (dec_policy == kIqr) {
+      if (SBS_LIKELY(dec_policy == kIqr)) {
         pos = iqr_select();
       } else if (dec_policy == kRandom) {
         if (mti >= 312) { mt_twist(pt.mt); mti = 0; }
@@ -766,7 +770,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       const uint64_t k0 = s_PK[u];
       const uint64_t K0 = k0 & kKMask, B0 = k0 >> 48;
       const uint64_t K1 = K0 + (uint64_t)prompt;
-      if (B0 + 1 >= (1u << 15) || K1 >= (1ull << 32)) { error = kErrEnvelope; return; }
+      if (SBS_UNLIKELY(B0 + 1 >= (1u << 15) || K1 >= (1ull << 32))) { error = kErrEnvelope; return; }
       const bool stepping = d_flag(j, G_STEP);
       __syncwarp();
       if (lane == 0) {
@@ -783,7 +787,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       PROF_BEGIN(6);
       if (S_valid) S_update(K0, K1);
       PROF_END(6);
-      if (cap_batch > 0 && (int64_t)B0 + 1 >= cap_batch) ul_dirty = true;
+      if (SBS_UNLIKELY(cap_batch > 0 && (int64_t)B0 + 1 >= cap_batch)) ul_dirty = true;
       // completion ring: finishes at step d_step + ceil(target/tps)
       const int64_t target = (int64_t)out - 1;
       const int64_t nsteps = tps == 1 ? target : (target + tps - 1) / tps;
@@ -791,7 +795,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       const int64_t c = bcast(d_step, j) + nsteps;
       const int b = j * R + (int)(c & (R - 1));
       const int cnt = s_bcnt[b];
-      if (cnt >= BC) { error = kErrOverflow; return; }
+      if (SBS_UNLIKELY(cnt >= BC)) { error = kErrOverflow; return; }
       if (lane == 0) {
         g_buckets[(int64_t)b * BC + cnt] =
             make_int4((int)id, u, (int)(prompt + target + excess), (int)excess);
@@ -1421,7 +1425,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     if (g_log) log_rec(LOG_STEP, 2, now, gen, 0, 0, 0);  // record_step (simulation.cpp:507)
     PROF_END(13);
     PROF_BEGIN(14);
-    if (band_fast) {
+    if (SBS_LIKELY(band_fast)) {
       // single decode instance: the band comes from the step loop's exact sums
       // mean = sum/n (bit-identical); sum (v-mean)^2 = (n*sum v^2 - (sum v)^2)/n
       if (d_flag(0, G_HEALTHY) && !d_flag(0, G_DEAD) && lane == 0) {
@@ -1545,7 +1549,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       const bool have = rhead < tail;
       const ChanRec* rc = &chL->rec[rhead % kChanRecs];
       const int64_t th = have ? rc->t : kInf64;
-      if (aborted) {  // keep the prefill warp unblocked until it finishes
+      if (SBS_UNLIKELY(aborted)) {  // keep the prefill warp unblocked until it finishes
         if (have) {
           rhead += 1;
           khead += rc->nk;
@@ -1600,7 +1604,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         const int nk = rc->nk, k0 = rc->k0;
         d_hk = 0;
         d_hi = rc->ef_idx;
-        if (ndw + nk + 32 > QD) { error = kErrOverflow; aborted = true; continue; }
+        if (SBS_UNLIKELY(ndw + nk + 32 > QD)) { error = kErrOverflow; aborted = true; continue; }
         // release the previous record's slots (its reads are long complete; this
         // record's are released at the next one, or exactly before a wait)
         if (lane == 0) { chR->head = rhead; chR->khead = khead; }
