@@ -95,7 +95,7 @@ __device__ __forceinline__ double pct_sorted(const int64_t* S, int n, double p) 
 }
 
 // mt19937_64 (std::mersenne_twister_engine<uint64_t,64,312,156,31,...>).
-__device__ void mt_twist(uint64_t* mt) {
+__device__ __forceinline__ void mt_twist(uint64_t* mt) {
   const int lane = lane_id();
   constexpr uint64_t UM = 0xFFFFFFFF80000000ull, LM = 0x7FFFFFFFull;
   constexpr uint64_t MA = 0xB5026F5AA96619E9ull;
@@ -132,6 +132,7 @@ __device__ void mt_twist(uint64_t* mt) {
   }
   __syncwarp();
 }
+__device__ __noinline__ void mt_twist_ool(uint64_t* mt) { mt_twist(mt); }
 
 __device__ __forceinline__ uint64_t mt_temper(uint64_t y) {
   y ^= (y >> 29) & 0x5555555555555555ull;
@@ -204,6 +205,65 @@ __device__ __forceinline__ int chan_ld(const volatile int* p) {
     __threadfence_block();
   }
   return v;
+}
+
+// kv_band (metrics.cpp:50-72) over every healthy, live decode unit, out of
+// line (the single-instance sweep path computes the band in the step loop):
+// the mean from the exact integer sum (bit-identical to the reference, whose
+// partial sums are exact integers), then the reference's second pass
+// sum (v - mean)^2 in FP64: lane partials + tree (<= 1e-15 rel.), or, when run
+// records are kept (seq), sequentially in unit order (bit-exact).  Warp-wide.
+__device__ __forceinline__ void kv_band_general_impl(const uint64_t* s_PK, int U, int Dd, int Dn,
+                                             unsigned live, bool seq, double* band,
+                                             int64_t* out_min, int64_t* out_max) {
+  const int lane = lane_id();
+  const bool all = live == (Dn == 32 ? 0xffffffffu : ((1u << Dn) - 1u));
+  int64_t s1 = 0, cnt = 0, vmin = kInf64, vmax = -1;
+#pragma unroll 1
+  for (int u = lane; u < U; u += 32) {
+    if (all || ((live >> (u / Dd)) & 1u)) {
+      const int64_t v = (int64_t)(s_PK[u] & kKMask);
+      s1 += v;
+      cnt += 1;
+      vmin = v < vmin ? v : vmin;
+      vmax = v > vmax ? v : vmax;
+    }
+  }
+  s1 = warp_sum_i64(s1);
+  cnt = __reduce_add_sync(kFull, (unsigned)cnt);
+  const double n_d = (double)cnt;
+  const double mean = __ddiv_rn((double)s1, n_d);
+  double var = 0.0;
+  if (seq) {
+    if (lane == 0)
+      for (int u = 0; u < U; ++u)
+        if (all || ((live >> (u / Dd)) & 1u)) {
+          const double dv = __dsub_rn((double)(int64_t)(s_PK[u] & kKMask), mean);
+          var = __dadd_rn(var, __dmul_rn(dv, dv));
+        }
+    var = __shfl_sync(kFull, var, 0);
+  } else {
+#pragma unroll 1
+    for (int u = lane; u < U; u += 32) {
+      if (all || ((live >> (u / Dd)) & 1u)) {
+        const double dv = __dsub_rn((double)(int64_t)(s_PK[u] & kKMask), mean);
+        var = __dadd_rn(var, __dmul_rn(dv, dv));
+      }
+    }
+    var = warp_sum_f64(var);
+  }
+  band[0] = mean;
+  band[1] = sqrt(__ddiv_rn(var, n_d));
+  *out_min = warp_min_i64(vmin);
+  *out_max = warp_max_i64(vmax);
+}
+// Out-of-line copy for the decode warp of a two-warp replica (its hot loop is
+// instruction-cache bound); the one-warp kernels keep it inline (a call site
+// costs them more in register allocation than the code it moves out).
+__device__ __noinline__ void kv_band_general_ool(const uint64_t* s_PK, int U, int Dd, int Dn,
+                                                 unsigned live, bool seq, double* band,
+                                                 int64_t* out_min, int64_t* out_max) {
+  kv_band_general_impl(s_PK, U, Dd, Dn, live, seq, band, out_min, out_max);
 }
 
 // KD: prefill DP units per lane, 1 (dp_degree <= 32) or 4 (<= 128).
@@ -753,7 +813,10 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       if (SBS_LIKELY(dec_policy == kIqr)) {
         pos = iqr_select();
       } else if (dec_policy == kRandom) {
-        if (mti >= 312) { mt_twist(pt.mt); mti = 0; }
+        if (mti >= 312) {
+          if constexpr (ROLE == 2) mt_twist_ool(pt.mt); else mt_twist(pt.mt);
+          mti = 0;
+        }
         uint64_t y = mt_temper(pt.mt[mti]);
         mti += 1;
         double u01 = (double)(y >> 11) * 0x1.0p-53;
@@ -1449,45 +1512,14 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       // or, when run records are kept, sequentially in unit order (bit-exact).
       unsigned live = __ballot_sync(kFull, lane < Dn && (dflags & G_HEALTHY) && !(dflags & G_DEAD));
       if (live) {
-        const bool all = live == (Dn == 32 ? 0xffffffffu : ((1u << Dn) - 1u));
-        int64_t s1 = 0, cnt = 0, vmin = kInf64, vmax = -1;
-#pragma unroll 1
-        for (int u = lane; u < U; u += 32) {
-          if (all || ((live >> (u / Dd)) & 1u)) {
-            const int64_t v = (int64_t)(s_PK[u] & kKMask);
-            s1 += v;
-            cnt += 1;
-            vmin = v < vmin ? v : vmin;
-            vmax = v > vmax ? v : vmax;
-          }
-        }
-        s1 = warp_sum_i64(s1);
-        cnt = __reduce_add_sync(kFull, (unsigned)cnt);
-        const double n_d = (double)cnt;
-        const double mean = __ddiv_rn((double)s1, n_d);
-        double var = 0.0;
+        double band[2];
+        int64_t vmin, vmax;
+        if constexpr (ROLE == 2)
+          kv_band_general_ool(s_PK, U, Dd, Dn, live, g_log != nullptr, band, &vmin, &vmax);
+        else
+          kv_band_general_impl(s_PK, U, Dd, Dn, live, g_log != nullptr, band, &vmin, &vmax);
+        const double mean = band[0], sigma = band[1];
         if (g_log) {
-          if (lane == 0)
-            for (int u = 0; u < U; ++u)
-              if (all || ((live >> (u / Dd)) & 1u)) {
-                const double dv = __dsub_rn((double)(int64_t)(s_PK[u] & kKMask), mean);
-                var = __dadd_rn(var, __dmul_rn(dv, dv));
-              }
-          var = bcast(var, 0);
-        } else {
-#pragma unroll 1
-          for (int u = lane; u < U; u += 32) {
-            if (all || ((live >> (u / Dd)) & 1u)) {
-              const double dv = __dsub_rn((double)(int64_t)(s_PK[u] & kKMask), mean);
-              var = __dadd_rn(var, __dmul_rn(dv, dv));
-            }
-          }
-          var = warp_sum_f64(var);
-        }
-        const double sigma = sqrt(__ddiv_rn(var, n_d));
-        if (g_log) {
-          vmin = warp_min_i64(vmin);
-          vmax = warp_max_i64(vmax);
           log_rec(LOG_KV, 5, now, __double_as_longlong(mean), __double_as_longlong(sigma), vmin, vmax);
         }
         if (now >= warmup && lane == 0) {
