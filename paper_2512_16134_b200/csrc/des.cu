@@ -741,11 +741,14 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     // (K < 2^32, position < 2^16)
     uint64_t best = UINT64_MAX;
     if (ul_ident) {
+      // rolled, with the next unit's load issued ahead (hides the smem latency)
+      uint64_t k = lane < nul ? s_PK[lane] : 0;
 #pragma unroll 1
       for (int i = lane; i < nul; i += 32) {
-        const uint64_t k = s_PK[i];
+        const uint64_t kn = i + 32 < nul ? s_PK[i + 32] : 0;
         const uint64_t c = (k & ~kKMask) | ((k & kKMask) << 16) | (uint64_t)i;
         if ((fallback || (int64_t)(k & kKMask) <= thi) && c < best) best = c;
+        k = kn;
       }
     } else {
 #pragma unroll 1
