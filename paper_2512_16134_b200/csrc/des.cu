@@ -326,6 +326,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   int16_t* s_ul = (int16_t*)(sm + pt.sm_ulist);
   uint16_t* s_bcnt = (uint16_t*)(sm + pt.sm_bcnt);
   uint32_t* s_hist = (uint32_t*)(sm + pt.sm_hist);
+  int4* s_stage = (int4*)(sm + pt.sm_stage);     // step-in-progress completers, per instance
   int64_t* s_wr = (int64_t*)(sm + pt.sm_wring);
   uint64_t* s_wk = (uint64_t*)(sm + pt.sm_wkeys);
   Counters* cn = (Counters*)(sm + (ROLE == 2 ? pt.sm_cnt2 : pt.sm_cnt));
@@ -709,6 +710,20 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     }
     seq++;
     odirty = true;
+    // This step's completion bucket is final now (requests admitted from here
+    // on complete at a later step): copy its head into shared memory while the
+    // step runs, so finish_step reads it without a global round trip.
+    {
+      const int64_t s1 = bcast(d_step, j);
+      const int bb = j * R + (int)(s1 & (R - 1));
+      const int nb = s_bcnt[bb];
+      if (lane < nb && lane < kStageEntries) {
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(s_stage + j * kStageEntries + lane);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst),
+                     "l"(g_buckets + (int64_t)bb * BC + lane) : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
   };
 
   // IQR select over the unit list (decode_alloc.cpp:38-81); returns position.
@@ -1374,6 +1389,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     const int b = j * R + (int)(s & (R - 1));
     const int n = s_bcnt[b];
     const int4* ent = g_buckets + (int64_t)b * BC;
+    const int4* stg = s_stage + j * kStageEntries;  // entries < kStageEntries (lane-owned copies)
+    asm volatile("cp.async.wait_all;" ::: "memory");
     int64_t exc = 0, rel = 0;
     PROF_BEGIN(11);
 #pragma unroll 1
@@ -1394,7 +1411,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
           __nanosleep(64);
         }
         if (has) {
-          const int4 v = ent[e];
+          const int4 v = e < kStageEntries ? stg[e] : ent[e];
           const int pos = ctail + lane, slot = pos % kChanComp;
           const uint64_t lap = (uint64_t)((pos / kChanComp) & 0xFFFF) << 48;
           chR->comp_t[slot] = (int64_t)((uint64_t)now | lap);
@@ -1408,7 +1425,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         continue;
       }
       if (has) {
-        const int4 v = ent[e];
+        const int4 v = e < kStageEntries ? stg[e] : ent[e];
         id = v.x;
         ft = o_ftok[id];  // every load of the completer issued before any use
         arr = __ldg(g_arr + id);
@@ -1459,16 +1476,16 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
 #pragma unroll 1
     for (int o = 16; o > 0; o >>= 1) {
       const double w = __shfl_xor_sync(kFull, worst, o);
-      const int64_t ex = __shfl_xor_sync(kFull, exc, o);
       const uint64_t a1 = __shfl_xor_sync(kFull, s1, o);
       const uint64_t lo = __shfl_xor_sync(kFull, s2lo, o);
       const uint64_t hi = __shfl_xor_sync(kFull, s2hi, o);
       worst = w > worst ? w : worst;
-      exc += ex;
       s1 += a1;
       s2lo += lo;
       s2hi += hi + (s2lo < lo);
     }
+    // (completers' excess <= n * tps and K < 2^32: single 32-bit REDUX each)
+    exc = (int64_t)__reduce_add_sync(kFull, (uint32_t)exc);
     const int64_t stamped = bcast(d_res_begin, j);
     const int64_t gen = tps * stamped - exc;
     (void)rel;
@@ -1480,7 +1497,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     S_valid = false;
     if (gather) {
       S_gathered = true;
-      S_mx = (uint64_t)warp_max_i64((int64_t)mx);
+      S_mx = (uint64_t)__reduce_max_sync(kFull, (uint32_t)mx);
     }
     if (cap_batch > 0 && n > 0) ul_dirty = true;
     __syncwarp();
@@ -1908,6 +1925,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   }
   }  // ROLE != 2
 
+  asm volatile("cp.async.wait_all;" ::: "memory");  // staged buckets: nothing in flight
   // ---- results
   tpot_sum = warp_sum_f64(tpot_sum);
   tpot_n = warp_sum_i64(tpot_n);

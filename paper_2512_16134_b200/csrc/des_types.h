@@ -26,7 +26,8 @@ constexpr int kHistBins = 64;
 constexpr int kChanRecs = 32;       // prefill->decode hand-off records in flight
 constexpr int kChanKeys = 1024;     // hand-off waiter keys in flight
 constexpr int kChanComp = 256;
-constexpr int kMaxProbes = 32;      // distinct prefix-cache probe lengths      // decode completions returned to the prefill warp
+constexpr int kMaxProbes = 32;
+constexpr int kStageEntries = 32;   // completion-bucket entries staged in smem per decode step      // distinct prefix-cache probe lengths      // decode completions returned to the prefill warp
 constexpr int kErrSplitTie = 7;     // two-warp replica met an unresolvable tie: rerun serially
 
 // Prefill-warp -> decode-warp hand-off channel of a two-warp replica (shared
@@ -118,7 +119,7 @@ struct DevPoint {
   // ---- shared-memory carve (bytes, relative to the warp's slice)
   int32_t sm_pf_out, sm_pf_head, sm_pf_tail, sm_pf_rel, sm_pf_part;
   int32_t sm_dPK, sm_dR, sm_dS, sm_dT, sm_dnst, sm_ulist, sm_bcnt, sm_hist, sm_wring, sm_wkeys, sm_cnt, sm_cnt2, sm_chan;
-  int32_t _pad2;
+  int32_t sm_stage;  // per decode instance: the completion bucket of its step in progress
   int32_t sm_bytes;
   int32_t _pad1;
 };

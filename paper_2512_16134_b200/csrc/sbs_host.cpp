@@ -408,6 +408,7 @@ void layout_smem(sbs::DevPoint& d) {
   d.sm_ulist = take(2 * U);
   d.sm_bcnt = take(2 * (size_t)d.Dn * d.R);
   d.sm_hist = take(4 * 256);
+  d.sm_stage = take(16 * (size_t)sbs::kStageEntries * d.Dn);
   d.sm_wring = take(8 * (size_t)d.w_size);
   d.sm_wkeys = take(8 * (size_t)sbs::kSmemWinKeys);
   d.sm_cnt = take(256);
