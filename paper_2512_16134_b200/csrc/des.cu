@@ -491,7 +491,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     int lk = kEvEF;
     if (wd_t < lt || (wd_t == lt && wd_s < ls)) { lt = wd_t; ls = wd_s; lk = kEvWD; }
     if (ds_t < lt || (ds_t == lt && ds_s < ls)) { lt = ds_t; ls = ds_s; lk = kEvDS; }
-    int64_t m = warp_min_i64(lt);
+    int64_t m = warp_min_nonneg_i64(lt);  // event times are >= 0 (kInf64 when none)
     uint32_t cs = (lt == m) ? ls : 0xffffffffu;
     uint32_t ms = __reduce_min_sync(kFull, cs);
     unsigned who = __ballot_sync(kFull, lt == m && ls == ms);
@@ -682,7 +682,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
           mx = k > mx ? k : mx;
         }
       }
-      mx = (uint64_t)warp_max_i64((int64_t)mx);
+      mx = (uint64_t)__reduce_max_sync(kFull, (uint32_t)mx);  // K < 2^32
     }
     S_gathered = false;
     __syncwarp();
@@ -954,7 +954,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       terms[k] = assigned >= c_chunk ? 1.0
                : assigned == 0 ? 0.0 : __ddiv_rn((double)assigned, (double)c_chunk);
     }
-    amax = warp_max_i64(amax);
+    amax = (int64_t)__reduce_max_sync(kFull, (uint32_t)amax);  // 0 <= assigned <= c_chunk < 2^31
     if (g_log) {  // record_pass (simulation.cpp:229, metrics.cpp:76-86)
       if (log_n + 3 + D > log_cap) {
         log_n = log_cap + 1;
@@ -1351,7 +1351,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
           if (v < bv) { bv = v; bg = g; }
         }
       }
-      int64_t mv = warp_min_i64(bv);
+      int64_t mv = warp_min_nonneg_i64(bv);  // outstanding tokens >= 0 (kInf64 when none)
       int g = (int)__reduce_min_sync(kFull, bv == mv ? (uint32_t)bg : 0x7fffffffu);
       if (mv != kInf64) { tp = g / D; tdp = g % D; }
     } else {

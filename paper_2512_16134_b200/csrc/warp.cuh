@@ -59,6 +59,15 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
   return v;
 }
 
+// min of non-negative int64 values by two 32-bit REDUX (high word, then the
+// low word among the lanes holding the minimal high word)
+__device__ __forceinline__ int64_t warp_min_nonneg_i64(int64_t v) {
+  const uint32_t hi = (uint32_t)((uint64_t)v >> 32), lo = (uint32_t)v;
+  const uint32_t mh = __reduce_min_sync(kFull, hi);
+  const uint32_t ml = __reduce_min_sync(kFull, hi == mh ? lo : 0xffffffffu);
+  return (int64_t)(((uint64_t)mh << 32) | ml);
+}
+
 __device__ __forceinline__ double warp_sum_f64(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(kFull, v, o));
