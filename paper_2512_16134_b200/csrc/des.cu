@@ -1446,6 +1446,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     // of completers); completers release B and prompt + decode_done of K
     const bool gather = ul_ident && Dn == 1;  // s_S order == unit order
     uint64_t mx = 0, s1 = 0, s2lo = 0, s2hi = 0;  // sum K, sum K^2 (128-bit)
+    const bool band_fast = !LOG && Dn == 1 && now >= warmup;
     double worst = 0.0;
 #pragma unroll 1
     for (int d = lane; d < Dd; d += 32) {
@@ -1470,19 +1471,27 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     PROF_END(12);
     PROF_BEGIN(13);
     (void)rel;
-    const bool band_fast = !LOG && Dn == 1 && now >= warmup;
-    // one interleaved butterfly for every per-step reduction (their shuffle
-    // latencies overlap instead of chaining); kept rolled (code size)
-#pragma unroll 1
-    for (int o = 16; o > 0; o >>= 1) {
-      const double w = __shfl_xor_sync(kFull, worst, o);
-      const uint64_t a1 = __shfl_xor_sync(kFull, s1, o);
-      const uint64_t lo = __shfl_xor_sync(kFull, s2lo, o);
-      const uint64_t hi = __shfl_xor_sync(kFull, s2hi, o);
-      worst = w > worst ? w : worst;
-      s1 += a1;
-      s2lo += lo;
-      s2hi += hi + (s2lo < lo);
+    // per-step reductions as independent 32-bit REDUX: the step time's max
+    // over non-negative doubles is the max of their bit patterns; the exact
+    // sums are split into chunks whose 32-lane sums cannot overflow 32 bits
+    // (lane partials: sum K < 2^36, sum K^2 < 2^68)
+    {
+      const uint64_t wb = (uint64_t)__double_as_longlong(worst);
+      const uint32_t wh = __reduce_max_sync(kFull, (uint32_t)(wb >> 32));
+      const uint32_t wl = __reduce_max_sync(kFull, (uint32_t)(wb >> 32) == wh ? (uint32_t)wb : 0u);
+      worst = __longlong_as_double((long long)(((uint64_t)wh << 32) | wl));
+    }
+    if (band_fast) {
+      const uint32_t a_hi = __reduce_add_sync(kFull, (uint32_t)(s1 >> 16));
+      const uint32_t a_lo = __reduce_add_sync(kFull, (uint32_t)(s1 & 0xffffu));
+      const uint32_t c0 = __reduce_add_sync(kFull, (uint32_t)(s2lo & 0xffffffu));
+      const uint32_t c1 = __reduce_add_sync(kFull, (uint32_t)((s2lo >> 24) & 0xffffffu));
+      const uint32_t c2 = __reduce_add_sync(kFull, (uint32_t)(((s2lo >> 48) | (s2hi << 16)) & 0xffffffu));
+      s1 = ((uint64_t)a_hi << 16) + a_lo;
+      typedef unsigned __int128 u128;
+      const u128 sq = (u128)c0 + ((u128)c1 << 24) + ((u128)c2 << 48);
+      s2lo = (uint64_t)sq;
+      s2hi = (uint64_t)(sq >> 64);
     }
     // (completers' excess <= n * tps and K < 2^32: single 32-bit REDUX each)
     exc = (int64_t)__reduce_add_sync(kFull, (uint32_t)exc);
