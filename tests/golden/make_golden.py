@@ -112,6 +112,9 @@ def cases():
         "overload_dp1": with_(s3k, cluster__dp_degree=1, workload__duration_s=6.0,
                               cluster__n_limit=3),
         "nlimit0": with_(s3k, cluster__dp_degree=2, workload__duration_s=4.0, cluster__n_limit=0),
+        # round engine coefficients: EndForward / decode-step ties at equal ns
+        # deep enough that a two-warp replica reruns on one warp (kErrSplitTie)
+        "split_tie_round_coeffs": {"cluster": {"n_instances_prefill": 2, "n_instances_decode": 1, "dp_degree": 2, "dp_degree_decode": 32, "c_chunk": 4000, "t_default_s": 0.06, "w_size": 64, "l_net_s": 0.0, "n_limit": 64, "decode_max_batch_per_dp": 0, "engine": {"prefill_base_s": 0.01, "prefill_per_token_s": 0.0, "decode_base_s": 0.01, "decode_per_request_s": 0.0, "decode_per_kv_token_s": 0.0}}, "workload": {"process": "poisson", "rate_qps": 50.0, "duration_s": 20.0, "prompt": {"dist": "uniform", "min": 10, "max": 100}, "output": {"dist": "uniform", "min": 2, "max": 3}}, "scheduler": {"policy": "sbs", "decode_policy": "iqr"}, "sim": {"seed": 361518, "warmup_fraction": 0.7}},
         # cache-aware PBAA + per-DP PrefixCache
         "cache_short": cache_short,
         "cache_short_basic": with_(cache_short, scheduler__prefill_mode="basic"),

@@ -52,3 +52,28 @@ def test_split_equals_serial_random(mode, monkeypatch):
         c["scheduler"]["decode_policy"] = str(rng.choice(["iqr", "random", "round_robin"]))
         c["sim"]["seed"] = int(rng.integers(0, 10**6))
         _same(_run(c, mode, monkeypatch), _run(c, 0, monkeypatch), f"random#{t}")
+
+
+def test_split_tie_rerun_is_exact():
+    """A case whose equal-ns EndForward/step ties exceed the two-warp ordering
+    rules: the replica reports kErrSplitTie and the host reruns it on one warp
+    (SBS_DEBUG reports the rerun); the result is still the reference's."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from tests.common import load_case
+    code = ("import json,sys; sys.path.insert(0,'.'); import paper_2512_16134_b200 as P; "
+            "from tests.common import CASES; g=P.run_experiment(CASES['split_tie_round_coeffs'], "
+            "per_request=True); print(json.dumps({k: g['requests'][k].tolist() for k in "
+            "('dispatch','prefill_start','first_token','completion')}))")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for mode in ("1", "2"):
+        p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=root,
+                           env=dict(os.environ, SBS_DEBUG="1", SBS_SPLIT=mode), timeout=300)
+        assert p.returncode == 0, p.stderr[-2000:]
+        assert "split ties" in p.stderr, "the case no longer exercises the one-warp rerun"
+        got = json.loads(p.stdout.strip().splitlines()[-1])
+        want = load_case("split_tie_round_coeffs")
+        for k in got:
+            assert np.array_equal(np.array(got[k], np.int64), want[k]), (mode, k)
