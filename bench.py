@@ -93,10 +93,12 @@ def workload_points(name, rank, world, replicas=None, duration=None):
                 cfgs)
     if name == "cfg4":
         # 1024-point grid l_net x rate x dp, 128 per GPU at 8 GPUs (i mod 8 == rank)
+        # (dp outermost, so i mod 8 strides over rates: every rank gets every
+        # dp_degree and l_net, which balances cost across ranks)
         pts = []
-        for ln in [0, 1, 2, 5, 10, 20, 50, 100]:
-            for rate in range(200, 520, 20):
-                for dp in [1, 2, 4, 8, 16, 32, 64, 128]:
+        for dp in [1, 2, 4, 8, 16, 32, 64, 128]:
+            for ln in [0, 1, 2, 5, 10, 20, 50, 100]:
+                for rate in range(200, 520, 20):
                     pts.append((ln / 1000.0, float(rate), dp))
         per = replicas or 128
         mine = [p for i, p in enumerate(pts) if i % 8 == rank % 8][:per]
