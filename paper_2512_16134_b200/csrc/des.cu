@@ -2243,7 +2243,7 @@ namespace sbs {
 // 6..9 = 0..3 with the cache-aware dispatch compiled in
 cudaError_t launch_des(int variant, const DevPoint* d_pts, int n_pts, int* d_counter,
                        DevResult* d_res, int smem_per_warp, int warps_per_block, int n_blocks,
-                       cudaStream_t st) {
+                       int min_smem, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(d_counter, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
   // one-warp variants: a slice per warp; two-warp variants: a slice per pair
@@ -2255,6 +2255,7 @@ cudaError_t launch_des(int variant, const DevPoint* d_pts, int n_pts, int* d_cou
     : variant == 6 ? des_kernel<1, false, true> : variant == 7 ? des_kernel<4, false, true>
     : variant == 8 ? des_kernel<1, true, true> : variant == 9 ? des_kernel<4, true, true>
     : variant == 4 ? des_split_kernel<1> : des_split_kernel<4>;
+  if (min_smem > 0 && smem < (size_t)min_smem) smem = (size_t)min_smem;  // CTAs per SM cap
   e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k<<<n_blocks, 32 * warps_per_block, smem, st>>>(d_pts, n_pts, d_counter, d_res, smem_per_warp);

@@ -34,7 +34,7 @@
 namespace sbs {
 cudaError_t launch_des(int variant, const DevPoint* d_pts, int n_pts, int* d_counter,
                        DevResult* d_res, int smem_per_warp, int warps_per_block, int n_blocks,
-                       cudaStream_t st);
+                       int min_smem, cudaStream_t st);
 cudaError_t launch_des_cluster(int variant, const DevPoint* d_pts, int n_pts, DevResult* d_res,
                                int smem_per_rep, cudaStream_t st);
 cudaError_t launch_finalize(const DevPoint* d_pts, int n_pts, DevResult* d_res, cudaStream_t st);
@@ -375,6 +375,9 @@ struct sbs_sim {
   int sm_count = 148;
   int pair_mode = 2;  // two-warp replicas: 1 = one CTA, 2 = a 2-CTA cluster (SBS_SPLIT)
   cudaEvent_t ev_des[2] = {nullptr, nullptr};  // around the DES kernels of the last launch
+  // one stream per kernel variant: the variant groups run side by side
+  cudaStream_t vstream[kVariants] = {};
+  cudaEvent_t ev_join[kVariants] = {};
 };
 
 namespace {
@@ -678,28 +681,50 @@ void launch_all(sbs_sim& s, cudaStream_t st) {
   if (s.ev_des[0] == nullptr) {
     CUDA_OR_THROW(cudaEventCreate(&s.ev_des[0]));
     CUDA_OR_THROW(cudaEventCreate(&s.ev_des[1]));
+    for (int v = 0; v < sbs_sim::kVariants; ++v) {
+      CUDA_OR_THROW(cudaStreamCreateWithFlags(&s.vstream[v], cudaStreamNonBlocking));
+      CUDA_OR_THROW(cudaEventCreateWithFlags(&s.ev_join[v], cudaEventDisableTiming));
+    }
   }
+  // Geometry of the one-warp-per-replica groups: when all their CTAs fit one
+  // per SM, reserve enough shared memory that no SM takes two (the block
+  // scheduler would otherwise pack them and leave SMs idle).
+  int total_blocks = 0;
+  for (int v = 0; v < sbs_sim::kVariants; ++v) {
+    const int n = s.group_begin[v + 1] - s.group_begin[v];
+    if (n <= 0 || ((v == 4 || v == 5) && s.pair_mode == 2)) continue;
+    const int per = (v == 4 || v == 5) ? 2 : s.warps_per_block;
+    total_blocks += (n + per - 1) / per;
+  }
+  const int min_smem = total_blocks <= s.sm_count ? 116 * 1024 : 0;
   CUDA_OR_THROW(cudaEventRecord(s.ev_des[0], st));
+  int used[sbs_sim::kVariants] = {};
   for (int v = 0; v < sbs_sim::kVariants; ++v) {
     const int b = s.group_begin[v], e = s.group_begin[v + 1];
     if (e <= b) continue;
+    // fork: each variant group on its own stream after everything queued on st
+    cudaStream_t vs = s.vstream[v];
+    CUDA_OR_THROW(cudaStreamWaitEvent(vs, s.ev_des[0], 0));
+    used[v] = 1;
     int wpb = s.warps_per_block, per_block = wpb;
     if ((v == 4 || v == 5) && s.pair_mode == 2) {  // replica = a CTA pair of a 2-CTA cluster
-      CUDA_OR_THROW(sbs::launch_des_cluster(v, s.d_pts + b, e - b, s.d_res + b, s.smem_per_warp, st));
-      s.n_launches += 1;
-      continue;
+      CUDA_OR_THROW(sbs::launch_des_cluster(v, s.d_pts + b, e - b, s.d_res + b, s.smem_per_warp, vs));
+    } else {
+      if (v == 4 || v == 5) {  // two warps per replica; at most two replicas per block
+        const int rpb = std::max(1, std::min(2, (e - b + s.sm_count - 1) / s.sm_count));
+        wpb = 2 * rpb;
+        per_block = rpb;
+        if ((size_t)rpb * s.smem_per_warp > 227 * 1024) { wpb = 2; per_block = 1; }
+      }
+      const int blocks = std::max(1, (e - b + per_block - 1) / per_block);
+      CUDA_OR_THROW(sbs::launch_des(v, s.d_pts + b, e - b, s.d_counter + v, s.d_res + b,
+                                    s.smem_per_warp, wpb, blocks, min_smem, vs));
     }
-    if (v == 4 || v == 5) {  // two warps per replica; at most two replicas per block
-      const int rpb = std::max(1, std::min(2, (e - b + s.sm_count - 1) / s.sm_count));
-      wpb = 2 * rpb;
-      per_block = rpb;
-      if ((size_t)rpb * s.smem_per_warp > 227 * 1024) { wpb = 2; per_block = 1; }
-    }
-    const int blocks = std::max(1, (e - b + per_block - 1) / per_block);
-    CUDA_OR_THROW(sbs::launch_des(v, s.d_pts + b, e - b, s.d_counter + v, s.d_res + b,
-                                  s.smem_per_warp, wpb, blocks, st));
+    CUDA_OR_THROW(cudaEventRecord(s.ev_join[v], vs));
     s.n_launches += 1;
   }
+  for (int v = 0; v < sbs_sim::kVariants; ++v)  // join
+    if (used[v]) CUDA_OR_THROW(cudaStreamWaitEvent(st, s.ev_join[v], 0));
   CUDA_OR_THROW(cudaEventRecord(s.ev_des[1], st));
   CUDA_OR_THROW(sbs::launch_finalize(s.d_pts, (int)s.order.size(), s.d_res, st));
   s.n_launches += 1;
@@ -1122,6 +1147,10 @@ void sbs_sim_destroy(sbs_sim* s) {
   if (s->d_counter) cudaFree(s->d_counter);
   for (auto& e : s->ev_des)
     if (e) cudaEventDestroy(e);
+  for (int v = 0; v < sbs_sim::kVariants; ++v) {
+    if (s->vstream[v]) cudaStreamDestroy(s->vstream[v]);
+    if (s->ev_join[v]) cudaEventDestroy(s->ev_join[v]);
+  }
   delete s;
 }
 
