@@ -431,8 +431,13 @@ def generate_workload(point_or_cfg, pinned: bool = False) -> HostTrace:
         o = np.empty(cnt, np.int32)
     pp = ps = None
     if pt.exp.workload.shared_prefix_fraction > 0:
-        pp = np.empty(cnt, np.int32)
-        ps = np.empty(cnt, np.int32)
+        if pinned:
+            import torch
+            pp = torch.empty(cnt, dtype=torch.int32, pin_memory=True).numpy()
+            ps = torch.empty(cnt, dtype=torch.int32, pin_memory=True).numpy()
+        else:
+            pp = np.empty(cnt, np.int32)
+            ps = np.empty(cnt, np.int32)
     _check(L.sbs_generate_workload(C.byref(pt.exp.workload), pt.exp.seed, a.ctypes.data,
                                    p.ctypes.data, o.ctypes.data,
                                    pp.ctypes.data if pp is not None else None,

@@ -2300,6 +2300,41 @@ cudaError_t launch_des_cluster(int variant, const DevPoint* d_pts, int n_pts, De
   return cudaGetLastError();
 }
 
+// Trace upload in one launch: every (host source, device destination, bytes)
+// segment is copied by the device straight from pinned host memory (mapped
+// under unified addressing), one CTA per segment slice, 16-byte accesses when
+// both ends are aligned.  Replaces one cudaMemcpyAsync per trace array.
+struct CopySeg {
+  const unsigned char* src;
+  unsigned char* dst;
+  int64_t bytes;
+};
+__global__ void __launch_bounds__(256) gather_kernel(const CopySeg* __restrict__ segs, int n_segs) {
+  const int64_t chunk = 1 << 16;  // bytes per CTA
+  int64_t b = blockIdx.x;
+  for (int s = 0; s < n_segs; ++s) {
+    const int64_t nb = (segs[s].bytes + chunk - 1) / chunk;
+    if (b >= nb) { b -= nb; continue; }
+    const unsigned char* src = segs[s].src + b * chunk;
+    unsigned char* dst = segs[s].dst + b * chunk;
+    const int64_t n = min(chunk, segs[s].bytes - b * chunk);
+    if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {
+      const int64_t n16 = n >> 4;
+      for (int64_t i = threadIdx.x; i < n16; i += blockDim.x)
+        ((int4*)dst)[i] = __ldcs(((const int4*)src) + i);
+      for (int64_t i = (n16 << 4) + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+    } else {
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+    }
+    return;
+  }
+}
+cudaError_t launch_gather(const CopySeg* d_segs, int n_segs, int64_t n_blocks, cudaStream_t st) {
+  if (n_segs == 0 || n_blocks == 0) return cudaSuccess;
+  gather_kernel<<<(unsigned)n_blocks, 256, 0, st>>>(d_segs, n_segs);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_finalize(const DevPoint* d_pts, int n_pts, DevResult* d_res, cudaStream_t st) {
   if (n_pts == 0) return cudaSuccess;
   finalize_kernel<<<n_pts, 256, 0, st>>>(d_pts, d_res);

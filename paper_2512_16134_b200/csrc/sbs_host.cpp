@@ -38,6 +38,12 @@ cudaError_t launch_des(int variant, const DevPoint* d_pts, int n_pts, int* d_cou
 cudaError_t launch_des_cluster(int variant, const DevPoint* d_pts, int n_pts, DevResult* d_res,
                                int smem_per_rep, cudaStream_t st);
 cudaError_t launch_finalize(const DevPoint* d_pts, int n_pts, DevResult* d_res, cudaStream_t st);
+struct CopySeg {
+  const unsigned char* src;
+  unsigned char* dst;
+  int64_t bytes;
+};
+cudaError_t launch_gather(const CopySeg* d_segs, int n_segs, int64_t n_blocks, cudaStream_t st);
 struct PbaaArgs {
   int32_t n_windows;
   const int64_t* req_off;
@@ -378,6 +384,11 @@ struct sbs_sim {
   // one stream per kernel variant: the variant groups run side by side
   cudaStream_t vstream[kVariants] = {};
   cudaEvent_t ev_join[kVariants] = {};
+  // trace re-upload in one gather launch (segment table, pinned host + device)
+  sbs::CopySeg* h_segs = nullptr;
+  sbs::CopySeg* d_segs = nullptr;
+  int seg_cap = 0;
+  cudaEvent_t ev_segs = nullptr;  // the previous gather has consumed h_segs
 };
 
 namespace {
@@ -757,7 +768,62 @@ void upload_points(sbs_sim& s) {
   s.n_blocks = std::max(1, std::min(need, max_blocks));
 }
 
+// Host source readable by the device (pinned memory under unified addressing)?
+bool device_readable(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost && a.devicePointer == p;
+}
+
+// One gather launch when every source is pinned host memory; false otherwise.
+bool upload_traces_gather(sbs_sim& s, const sbs_trace* traces, cudaStream_t st) {
+  std::vector<sbs::CopySeg> segs;
+  for (size_t i = 0; i < s.traces.size(); ++i) {
+    const TraceDev& t = s.traces[i];
+    if (t.n == 0) continue;
+    const void* src[5] = {traces[i].arrival_ns, traces[i].prompt_len, traces[i].output_len,
+                          traces[i].prefix_pool_id, traces[i].prefix_size};
+    void* dst[5] = {t.arr, t.prompt, t.output, t.pool, t.psize};
+    const int64_t bytes[5] = {8 * t.n, 4 * t.n, 4 * t.n, 4 * t.n, 4 * t.n};
+    for (int k = 0; k < 5; ++k) {
+      if (dst[k] == nullptr) continue;
+      if (!device_readable(src[k])) return false;
+      segs.push_back({(const unsigned char*)src[k], (unsigned char*)dst[k], bytes[k]});
+    }
+  }
+  if (segs.empty()) return true;
+  if ((int)segs.size() > s.seg_cap) {
+    if (s.h_segs) cudaFreeHost(s.h_segs);
+    if (s.d_segs) cudaFree(s.d_segs);
+    s.seg_cap = (int)segs.size();
+    CUDA_OR_THROW(cudaMallocHost(&s.h_segs, sizeof(sbs::CopySeg) * s.seg_cap));
+    CUDA_OR_THROW(cudaMalloc(&s.d_segs, sizeof(sbs::CopySeg) * s.seg_cap));
+    if (s.ev_segs == nullptr) CUDA_OR_THROW(cudaEventCreateWithFlags(&s.ev_segs, cudaEventDisableTiming));
+  } else if (s.ev_segs) {
+    CUDA_OR_THROW(cudaEventSynchronize(s.ev_segs));  // previous table no longer in use
+  }
+  int64_t blocks = 0;
+  for (size_t k = 0; k < segs.size(); ++k) {
+    s.h_segs[k] = segs[k];
+    blocks += (segs[k].bytes + (1 << 16) - 1) >> 16;
+  }
+  CUDA_OR_THROW(cudaMemcpyAsync(s.d_segs, s.h_segs, sizeof(sbs::CopySeg) * segs.size(),
+                                cudaMemcpyHostToDevice, st));
+  CUDA_OR_THROW(sbs::launch_gather(s.d_segs, (int)segs.size(), blocks, st));
+  CUDA_OR_THROW(cudaEventRecord(s.ev_segs, st));
+  return true;
+}
+
 void do_upload_traces(sbs_sim& s, const sbs_trace* traces, cudaStream_t st) {
+  for (size_t i = 0; i < s.traces.size(); ++i) {
+    if (traces[i].n != s.traces[i].n) throw Error{SBS_ERR_CONFIG, "trace shape changed"};
+    if ((traces[i].prefix_pool_id != nullptr) != (s.traces[i].pool != nullptr))
+      throw Error{SBS_ERR_CONFIG, "trace shape changed"};
+  }
+  if (s.traces.size() > 1 && upload_traces_gather(s, traces, st)) return;
   for (size_t i = 0; i < s.traces.size(); ++i) {
     TraceDev& t = s.traces[i];
     if (traces[i].n != t.n) throw Error{SBS_ERR_CONFIG, "trace shape changed"};
@@ -1151,6 +1217,9 @@ void sbs_sim_destroy(sbs_sim* s) {
     if (s->vstream[v]) cudaStreamDestroy(s->vstream[v]);
     if (s->ev_join[v]) cudaEventDestroy(s->ev_join[v]);
   }
+  if (s->h_segs) cudaFreeHost(s->h_segs);
+  if (s->d_segs) cudaFree(s->d_segs);
+  if (s->ev_segs) cudaEventDestroy(s->ev_segs);
   delete s;
 }
 

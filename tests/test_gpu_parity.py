@@ -202,3 +202,25 @@ def test_cache_aware_random_vs_reference():
                     "prefill_start": rq[:, 2], "first_token": rq[:, 3], "completion": rq[:, 4],
                     "agg": r["agg"], "alloc_calls": r["agg"]["alloc_calls"]}
         check_against(f"cache#{t}", g["requests"], g["agg"], want)
+
+
+def test_trace_reupload_pinned_gather_and_pageable():
+    """sbs_sim_upload_traces: pinned host traces go up in one gather launch,
+    pageable ones by copies; both give the same simulation."""
+    names = ["decode_dp32", "short_3k", "cfg2_20s", "cache_short"]
+    pts = [P.experiment_from_config(CASES[n]) for n in names]
+    pinned = [P.generate_workload(p, pinned=True) for p in pts]
+    pageable = [P.generate_workload(p) for p in pts]
+    sim = P.Simulator(pts, pageable, per_request=True)
+    try:
+        outs = []
+        for trs in (pinned, pageable, pinned):
+            sim.upload_traces(trs)
+            sim.launch()
+            aggs = sim.results()
+            outs.append([sim.requests(i)["completion"].copy() for i in range(len(names))])
+            for i, n in enumerate(names):
+                assert aggs[i]["error"] == 0
+                assert np.array_equal(outs[-1][i], load_case(n)["completion"]), n
+    finally:
+        sim.close()
