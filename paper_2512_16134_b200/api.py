@@ -123,6 +123,15 @@ class Aggregates(C.Structure):
         return {f: getattr(self, f) for f, _ in AGG_FIELDS if not f.startswith("_")}
 
 
+_NP_OF = {C.c_uint64: "<u8", C.c_int64: "<i8", C.c_double: "<f8", C.c_int32: "<i4"}
+# numpy view of an Aggregates array (bulk conversion in results())
+_AGG_NAMES = [f for f, _ in AGG_FIELDS if not f.startswith("_")]
+_AGG_DTYPE = np.dtype({"names": _AGG_NAMES,
+                       "formats": [_NP_OF[t] for f, t in AGG_FIELDS if not f.startswith("_")],
+                       "offsets": [getattr(Aggregates, f).offset for f in _AGG_NAMES],
+                       "itemsize": C.sizeof(Aggregates)})
+
+
 HIST_BINS = 64
 
 
@@ -486,7 +495,8 @@ class Simulator:
         hist = Histograms() if histograms else None
         _check(lib().sbs_sim_results(self.handle, out, C.byref(hist) if hist else None,
                                      C.c_void_p(stream)))
-        res = [a.to_dict() for a in out]
+        rows = np.frombuffer(out, dtype=_AGG_DTYPE).tolist()
+        res = [dict(zip(_AGG_NAMES, r)) for r in rows]
         return (res, hist) if histograms else res
 
     def requests(self, point: int):
