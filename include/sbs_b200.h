@@ -194,7 +194,9 @@ int sbs_sim_create(const sbs_experiment* points, int32_t n_points,
                    const sbs_trace* traces, int32_t n_traces,
                    const int32_t* trace_of_point, uint32_t flags,
                    int32_t device, sbs_sim** out);
-/* Re-upload host traces (same shapes) on `stream` (H2D of 16 B/request). */
+/* Re-upload host traces (same shapes) on `stream` (16 B/request).  When every
+ * array is pinned host memory the device gathers them in one launch (a copy
+ * kernel over the mapped host pages); otherwise one copy per array. */
 int sbs_sim_upload_traces(sbs_sim* sim, const sbs_trace* traces, void* stream);
 /* Enqueue one full simulation of every point (DES kernel + finalize kernel). */
 int sbs_sim_launch(sbs_sim* sim, void* stream);

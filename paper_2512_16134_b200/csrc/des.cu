@@ -83,17 +83,6 @@ __device__ __forceinline__ int hist_bin(int64_t v) {
   return b < kHistBins ? b : kHistBins - 1;
 }
 
-// percentile (decode_alloc.cpp:13-23) over a sorted int64 multiset.
-__device__ __forceinline__ double pct_sorted(const int64_t* S, int n, double p) {
-  double rank = __ddiv_rn(__dmul_rn((double)n - 1.0, p), 100.0);
-  double fl = floor(rank), ce = ceil(rank);
-  int lo = (int)fl, hi = (int)ce;
-  double vlo = (double)S[lo];
-  if (lo == hi) return vlo;
-  double frac = __dsub_rn(rank, (double)lo);
-  return __dadd_rn(vlo, __dmul_rn(frac, __dsub_rn((double)S[hi], vlo)));
-}
-
 // mt19937_64 (std::mersenne_twister_engine<uint64_t,64,312,156,31,...>).
 __device__ __forceinline__ void mt_twist(uint64_t* mt) {
   const int lane = lane_id();
