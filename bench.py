@@ -198,6 +198,17 @@ def cpu_sample_spec(workload):
     return {"replicas_per_core": 2, "duration": None}
 
 
+def cpu_model():
+    """Host CPU model string (state the CPU beside the core count)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
         return 0
@@ -228,7 +239,7 @@ def run_reference_arm(args, rank, world):
         "config": {"workload": desc, "sample": sample},
         "allocations_per_s": allocs / wall,
         "cpu_baseline": {"value": v, "unit": "sim-req/s", "cores": threads, "kind": "reference",
-                         "sample": sample},
+                         "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": v, "unit": "sim-req/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -376,6 +387,7 @@ def main():
             nrep = min(len(cfgs), threads * spec["replicas_per_core"])
             wall, gen, allocs, dsel, n = cpu_reference(cfgs, threads, nrep, spec["duration"])
             cpu = {"value": gen / wall, "unit": "sim-req/s", "cores": threads, "kind": "reference",
+                   "cpu_model": cpu_model(),
                    "sample": f"{n} replicas of {args.workload}"
                              + (f" at duration {spec['duration']:g} s" if spec["duration"] else "")
                              + f" ({gen:.0f} simulated requests) on {threads} threads, "
