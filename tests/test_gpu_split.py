@@ -77,3 +77,41 @@ def test_split_tie_rerun_is_exact():
         want = load_case("split_tie_round_coeffs")
         for k in got:
             assert np.array_equal(np.array(got[k], np.int64), want[k]), (mode, k)
+
+
+def test_multi_instance_decode_with_faults_vs_reference():
+    """Two-warp replicas with several decode instances, decode/prefill topology
+    changes, dead decode instances, batch caps and tps > 1 (the decode warp's
+    own topology handling) against the reference (or the C restatement)."""
+    from oracle import orc, ref
+    have_ref = ref.available()
+    rng = np.random.default_rng(3)
+    for t in range(12):
+        c = copy.deepcopy(CASES[["decode_dp32", "cfg2_20s"][t % 2]])
+        Pn, Dn = int(rng.integers(1, 4)), int(rng.choice([2, 3, 5]))
+        c["cluster"].update({"n_instances_prefill": Pn, "n_instances_decode": Dn,
+                             "dp_degree_decode": int(rng.choice([4, 16, 40])),
+                             "decode_max_batch_per_dp": int(rng.choice([0, 3, 20])),
+                             "decode_tokens_per_step": int(rng.choice([1, 2, 5]))})
+        dur = float(rng.uniform(5, 20))
+        c["workload"]["duration_s"] = dur
+        c["scheduler"]["decode_policy"] = str(rng.choice(["iqr", "iqr", "random", "round_robin"]))
+        c["sim"]["seed"] = int(rng.integers(0, 10**6))
+        c["faults"] = {"topology": [{"instance": int(rng.integers(0, Pn + Dn)),
+                                     "time_s": float(rng.uniform(0, dur)),
+                                     "healthy": bool(rng.random() < 0.5)} for _ in range(3)],
+                       "dead": [{"instance": int(rng.integers(Pn, Pn + Dn)),
+                                 "time_s": float(rng.uniform(0, dur))}]}
+        g = P.run_experiment(c, per_request=True)
+        if have_ref:
+            rq = ref.run(c, per_request=True)["requests"]
+            want = {"status": rq[:, 3], "dispatch": rq[:, 4], "prefill_start": rq[:, 5],
+                    "first_token": rq[:, 6], "completion": rq[:, 7]}
+        else:
+            tr = g["trace"]
+            rq = orc.run(c, tr.arrival_ns, tr.prompt_len, tr.output_len)["requests"]
+            want = {"status": rq[:, 0], "dispatch": rq[:, 1], "prefill_start": rq[:, 2],
+                    "first_token": rq[:, 3], "completion": rq[:, 4]}
+        for k in COLS:
+            assert np.array_equal(np.asarray(g["requests"][k], np.int64),
+                                  np.asarray(want[k], np.int64)), (t, k)
