@@ -1082,6 +1082,10 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     warp_sort_buf(nk, nn);
     uint64_t* pk = pt.pend_key[pcur];
     int32_t* pw = pt.pend_wait[pcur];
+#ifdef SBS_PROF
+    prof_acc[22] += np;
+    prof_acc[23] += nn;
+#endif
     bool ovf = false;
     constexpr uint64_t kPlaced = ~0ull;  // cache-aware mode: a placed queue entry
 
