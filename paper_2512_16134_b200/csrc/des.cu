@@ -2081,14 +2081,17 @@ __device__ __forceinline__ void pair_sync(int pair) {
   asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory");
 }
 
+// Warps [0, R) are the prefill warps and [R, 2R) the decode warps of R pairs,
+// so with R = 4 every scheduler partition (warp % 4) holds one decode warp.
 template <int KD>
-__global__ void __launch_bounds__(128) des_split_kernel(const DevPoint* __restrict__ pts, int n_pts,
+__global__ void __launch_bounds__(256) des_split_kernel(const DevPoint* __restrict__ pts, int n_pts,
                                                         int* __restrict__ next_point,
                                                         DevResult* __restrict__ res,
                                                         int smem_per_pair) {
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ int s_pi[2];
-  const int warp = threadIdx.x >> 5, pair = warp >> 1, role = warp & 1, lane = lane_id();
+  __shared__ int s_pi[4];
+  const int npairs = blockDim.x >> 6;
+  const int warp = threadIdx.x >> 5, pair = warp % npairs, role = warp / npairs, lane = lane_id();
   unsigned char* my = smem + pair * smem_per_pair;
   for (;;) {
     if (role == 0 && lane == 0) s_pi[pair] = atomicAdd(next_point, 1);

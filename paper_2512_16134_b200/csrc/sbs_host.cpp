@@ -704,7 +704,8 @@ void launch_all(sbs_sim& s, cudaStream_t st) {
   for (int v = 0; v < sbs_sim::kVariants; ++v) {
     const int n = s.group_begin[v + 1] - s.group_begin[v];
     if (n <= 0 || ((v == 4 || v == 5) && s.pair_mode == 2)) continue;
-    const int per = (v == 4 || v == 5) ? 2 : s.warps_per_block;
+    const int per = (v == 4 || v == 5) ? std::max(1, std::min(4, (n + s.sm_count - 1) / s.sm_count))
+                                       : s.warps_per_block;
     total_blocks += (n + per - 1) / per;
   }
   const int min_smem = total_blocks <= s.sm_count ? 116 * 1024 : 0;
@@ -721,11 +722,11 @@ void launch_all(sbs_sim& s, cudaStream_t st) {
     if ((v == 4 || v == 5) && s.pair_mode == 2) {  // replica = a CTA pair of a 2-CTA cluster
       CUDA_OR_THROW(sbs::launch_des_cluster(v, s.d_pts + b, e - b, s.d_res + b, s.smem_per_warp, vs));
     } else {
-      if (v == 4 || v == 5) {  // two warps per replica; at most two replicas per block
-        const int rpb = std::max(1, std::min(2, (e - b + s.sm_count - 1) / s.sm_count));
+      if (v == 4 || v == 5) {  // two warps per replica; up to four replicas per block
+        int rpb = std::max(1, std::min(4, (e - b + s.sm_count - 1) / s.sm_count));
+        while (rpb > 1 && (size_t)rpb * s.smem_per_warp > 227 * 1024) --rpb;
         wpb = 2 * rpb;
         per_block = rpb;
-        if ((size_t)rpb * s.smem_per_warp > 227 * 1024) { wpb = 2; per_block = 1; }
       }
       const int blocks = std::max(1, (e - b + per_block - 1) / per_block);
       CUDA_OR_THROW(sbs::launch_des(v, s.d_pts + b, e - b, s.d_counter + v, s.d_res + b,
