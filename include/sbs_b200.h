@@ -200,6 +200,14 @@ int sbs_sim_create(const sbs_experiment* points, int32_t n_points,
 int sbs_sim_upload_traces(sbs_sim* sim, const sbs_trace* traces, void* stream);
 /* Enqueue one full simulation of every point (DES kernel + finalize kernel). */
 int sbs_sim_launch(sbs_sim* sim, void* stream);
+/* Double-buffered traces: with 2 slots the next step's traces can be uploaded
+ * (sbs_sim_upload_traces_slot, e.g. on a copy stream) while a launch reads the
+ * other slot (sbs_sim_launch_slot).  The caller orders the streams: a slot is
+ * not re-uploaded while a launch that reads it is in flight.  Slot 0 is the
+ * one sbs_sim_create / sbs_sim_upload_traces / sbs_sim_launch use. */
+int sbs_sim_enable_trace_slots(sbs_sim* sim, int32_t n_slots);
+int sbs_sim_upload_traces_slot(sbs_sim* sim, const sbs_trace* traces, int32_t slot, void* stream);
+int sbs_sim_launch_slot(sbs_sim* sim, int32_t slot, void* stream);
 /* Synchronise `stream`, copy results back, finish the aggregate arithmetic. */
 int sbs_sim_results(sbs_sim* sim, sbs_aggregates* out, sbs_histograms* hist,
                     void* stream);

@@ -181,6 +181,9 @@ def lib():
                                      C.POINTER(C.c_void_p)]
         L.sbs_sim_upload_traces.argtypes = [C.c_void_p, C.POINTER(Trace), C.c_void_p]
         L.sbs_sim_launch.argtypes = [C.c_void_p, C.c_void_p]
+        L.sbs_sim_enable_trace_slots.argtypes = [C.c_void_p, C.c_int32]
+        L.sbs_sim_upload_traces_slot.argtypes = [C.c_void_p, C.POINTER(Trace), C.c_int32, C.c_void_p]
+        L.sbs_sim_launch_slot.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
         L.sbs_sim_results.argtypes = [C.c_void_p, C.POINTER(Aggregates), C.POINTER(Histograms),
                                       C.c_void_p]
         L.sbs_sim_requests.argtypes = [C.c_void_p, C.c_int32] + [C.c_void_p] * 5
@@ -208,6 +211,7 @@ EXPORTED_SYMBOLS = [
     "sbs_sim_destroy", "sbs_run_experiments", "sbs_prefill_allocate",
     "sbs_prefill_allocate_async", "sbs_decode_select", "sbs_decode_select_async",
     "sbs_last_error", "sbs_version", "sbs_sim_profile_counters", "sbs_sim_des_ms",
+    "sbs_sim_enable_trace_slots", "sbs_sim_upload_traces_slot", "sbs_sim_launch_slot",
 ]
 
 
@@ -481,14 +485,18 @@ class Simulator:
         self.handle = h
         self.n = n
 
-    def upload_traces(self, traces=None, stream=0):
+    def upload_traces(self, traces=None, stream=0, slot=0):
         if traces is not None:
             self.traces = list(traces)
             self._tr = (Trace * len(self.traces))(*[t.as_c() for t in self.traces])
-        _check(lib().sbs_sim_upload_traces(self.handle, self._tr, C.c_void_p(stream)))
+        _check(lib().sbs_sim_upload_traces_slot(self.handle, self._tr, slot, C.c_void_p(stream)))
 
-    def launch(self, stream=0):
-        _check(lib().sbs_sim_launch(self.handle, C.c_void_p(stream)))
+    def enable_trace_slots(self, n=2):
+        """Second trace buffer set: upload step k+1 while step k runs."""
+        _check(lib().sbs_sim_enable_trace_slots(self.handle, n))
+
+    def launch(self, stream=0, slot=0):
+        _check(lib().sbs_sim_launch_slot(self.handle, slot, C.c_void_p(stream)))
 
     def results(self, stream=0, histograms=False):
         out = (Aggregates * self.n)()

@@ -332,6 +332,13 @@ struct TraceDev {
   int32_t* output = nullptr;
   int32_t* pool = nullptr;   // shared-prefix pool id per request (-1: none), or NULL
   int32_t* psize = nullptr;  // prefix tokens per request
+  // second trace buffer set (sbs_sim_enable_trace_slots(2)): the next step's
+  // traces go up while the current step runs
+  int64_t* arr1 = nullptr;
+  int32_t* prompt1 = nullptr;
+  int32_t* output1 = nullptr;
+  int32_t* pool1 = nullptr;
+  int32_t* psize1 = nullptr;
   int64_t n = 0;
   int32_t max_output = 0;
   int32_t n_pools = 0;       // 1 + max pool id
@@ -389,6 +396,9 @@ struct sbs_sim {
   sbs::CopySeg* d_segs = nullptr;
   int seg_cap = 0;
   cudaEvent_t ev_segs = nullptr;  // the previous gather has consumed h_segs
+  int n_slots = 1;                 // trace buffer sets
+  int cur_slot = 0;                // the set the last launch read
+  sbs::DevPoint* d_pts1 = nullptr; // point descriptors pointing at set 1
 };
 
 namespace {
@@ -689,6 +699,7 @@ void order_points(sbs_sim& s) {
 
 void launch_all(sbs_sim& s, cudaStream_t st) {
   s.n_launches = 0;
+  const sbs::DevPoint* dp = s.cur_slot ? s.d_pts1 : s.d_pts;
   if (s.ev_des[0] == nullptr) {
     CUDA_OR_THROW(cudaEventCreate(&s.ev_des[0]));
     CUDA_OR_THROW(cudaEventCreate(&s.ev_des[1]));
@@ -720,7 +731,7 @@ void launch_all(sbs_sim& s, cudaStream_t st) {
     used[v] = 1;
     int wpb = s.warps_per_block, per_block = wpb;
     if ((v == 4 || v == 5) && s.pair_mode == 2) {  // replica = a CTA pair of a 2-CTA cluster
-      CUDA_OR_THROW(sbs::launch_des_cluster(v, s.d_pts + b, e - b, s.d_res + b, s.smem_per_warp, vs));
+      CUDA_OR_THROW(sbs::launch_des_cluster(v, dp + b, e - b, s.d_res + b, s.smem_per_warp, vs));
     } else {
       if (v == 4 || v == 5) {  // two warps per replica; up to four replicas per block
         int rpb = std::max(1, std::min(4, (e - b + s.sm_count - 1) / s.sm_count));
@@ -729,7 +740,7 @@ void launch_all(sbs_sim& s, cudaStream_t st) {
         per_block = rpb;
       }
       const int blocks = std::max(1, (e - b + per_block - 1) / per_block);
-      CUDA_OR_THROW(sbs::launch_des(v, s.d_pts + b, e - b, s.d_counter + v, s.d_res + b,
+      CUDA_OR_THROW(sbs::launch_des(v, dp + b, e - b, s.d_counter + v, s.d_res + b,
                                     s.smem_per_warp, wpb, blocks, min_smem, vs));
     }
     CUDA_OR_THROW(cudaEventRecord(s.ev_join[v], vs));
@@ -738,7 +749,7 @@ void launch_all(sbs_sim& s, cudaStream_t st) {
   for (int v = 0; v < sbs_sim::kVariants; ++v)  // join
     if (used[v]) CUDA_OR_THROW(cudaStreamWaitEvent(st, s.ev_join[v], 0));
   CUDA_OR_THROW(cudaEventRecord(s.ev_des[1], st));
-  CUDA_OR_THROW(sbs::launch_finalize(s.d_pts, (int)s.order.size(), s.d_res, st));
+  CUDA_OR_THROW(sbs::launch_finalize(dp, (int)s.order.size(), s.d_res, st));
   s.n_launches += 1;
 }
 
@@ -752,6 +763,20 @@ void upload_points(sbs_sim& s) {
   s.smem_per_warp = (int)align_up((size_t)smem, 128);
   CUDA_OR_THROW(cudaMemcpy(s.d_pts, h.data(), sizeof(sbs::DevPoint) * h.size(),
                            cudaMemcpyHostToDevice));
+  if (s.n_slots == 2) {  // the same points reading trace set 1
+    for (size_t i = 0; i < h.size(); ++i) {
+      const TraceDev& t = s.traces[s.pts[s.order[i]].trace];
+      h[i].arr = t.arr1;
+      h[i].prompt = t.prompt1;
+      h[i].output = t.output1;
+      if (h[i].cache_on) {
+        h[i].pfx_pool = t.pool1;
+        h[i].pfx_size = t.psize1;
+      }
+    }
+    CUDA_OR_THROW(cudaMemcpy(s.d_pts1, h.data(), sizeof(sbs::DevPoint) * h.size(),
+                             cudaMemcpyHostToDevice));
+  }
   // occupancy: warps per block 4 unless shared memory forces fewer
   const int max_smem_block = 227 * 1024;
   // spread replicas over every SM first: warps of one SM share its issue
@@ -780,14 +805,16 @@ bool device_readable(const void* p) {
 }
 
 // One gather launch when every source is pinned host memory; false otherwise.
-bool upload_traces_gather(sbs_sim& s, const sbs_trace* traces, cudaStream_t st) {
+bool upload_traces_gather(sbs_sim& s, const sbs_trace* traces, int slot, cudaStream_t st) {
   std::vector<sbs::CopySeg> segs;
   for (size_t i = 0; i < s.traces.size(); ++i) {
     const TraceDev& t = s.traces[i];
     if (t.n == 0) continue;
     const void* src[5] = {traces[i].arrival_ns, traces[i].prompt_len, traces[i].output_len,
                           traces[i].prefix_pool_id, traces[i].prefix_size};
-    void* dst[5] = {t.arr, t.prompt, t.output, t.pool, t.psize};
+    void* dst[5] = {slot ? (void*)t.arr1 : t.arr, slot ? (void*)t.prompt1 : t.prompt,
+                    slot ? (void*)t.output1 : t.output, slot ? (void*)t.pool1 : t.pool,
+                    slot ? (void*)t.psize1 : t.psize};
     const int64_t bytes[5] = {8 * t.n, 4 * t.n, 4 * t.n, 4 * t.n, 4 * t.n};
     for (int k = 0; k < 5; ++k) {
       if (dst[k] == nullptr) continue;
@@ -818,25 +845,28 @@ bool upload_traces_gather(sbs_sim& s, const sbs_trace* traces, cudaStream_t st) 
   return true;
 }
 
-void do_upload_traces(sbs_sim& s, const sbs_trace* traces, cudaStream_t st) {
+void do_upload_traces(sbs_sim& s, const sbs_trace* traces, cudaStream_t st, int slot = 0) {
   for (size_t i = 0; i < s.traces.size(); ++i) {
     if (traces[i].n != s.traces[i].n) throw Error{SBS_ERR_CONFIG, "trace shape changed"};
     if ((traces[i].prefix_pool_id != nullptr) != (s.traces[i].pool != nullptr))
       throw Error{SBS_ERR_CONFIG, "trace shape changed"};
   }
-  if (s.traces.size() > 1 && upload_traces_gather(s, traces, st)) return;
+  if (slot < 0 || slot >= s.n_slots) throw Error{SBS_ERR_CONFIG, "trace slot out of range"};
+  if (s.traces.size() > 1 && upload_traces_gather(s, traces, slot, st)) return;
   for (size_t i = 0; i < s.traces.size(); ++i) {
     TraceDev& t = s.traces[i];
-    if (traces[i].n != t.n) throw Error{SBS_ERR_CONFIG, "trace shape changed"};
     if (t.n == 0) continue;
-    CUDA_OR_THROW(cudaMemcpyAsync(t.arr, traces[i].arrival_ns, 8 * t.n, cudaMemcpyHostToDevice, st));
-    CUDA_OR_THROW(cudaMemcpyAsync(t.prompt, traces[i].prompt_len, 4 * t.n, cudaMemcpyHostToDevice, st));
-    CUDA_OR_THROW(cudaMemcpyAsync(t.output, traces[i].output_len, 4 * t.n, cudaMemcpyHostToDevice, st));
-    if ((traces[i].prefix_pool_id != nullptr) != (t.pool != nullptr))
-      throw Error{SBS_ERR_CONFIG, "trace shape changed"};
+    CUDA_OR_THROW(cudaMemcpyAsync(slot ? t.arr1 : t.arr, traces[i].arrival_ns, 8 * t.n,
+                                  cudaMemcpyHostToDevice, st));
+    CUDA_OR_THROW(cudaMemcpyAsync(slot ? t.prompt1 : t.prompt, traces[i].prompt_len, 4 * t.n,
+                                  cudaMemcpyHostToDevice, st));
+    CUDA_OR_THROW(cudaMemcpyAsync(slot ? t.output1 : t.output, traces[i].output_len, 4 * t.n,
+                                  cudaMemcpyHostToDevice, st));
     if (t.pool) {
-      CUDA_OR_THROW(cudaMemcpyAsync(t.pool, traces[i].prefix_pool_id, 4 * t.n, cudaMemcpyHostToDevice, st));
-      CUDA_OR_THROW(cudaMemcpyAsync(t.psize, traces[i].prefix_size, 4 * t.n, cudaMemcpyHostToDevice, st));
+      CUDA_OR_THROW(cudaMemcpyAsync(slot ? t.pool1 : t.pool, traces[i].prefix_pool_id, 4 * t.n,
+                                    cudaMemcpyHostToDevice, st));
+      CUDA_OR_THROW(cudaMemcpyAsync(slot ? t.psize1 : t.psize, traces[i].prefix_size, 4 * t.n,
+                                    cudaMemcpyHostToDevice, st));
     }
   }
 }
@@ -1064,12 +1094,49 @@ int sbs_sim_upload_traces(sbs_sim* s, const sbs_trace* traces, void* stream) {
   });
 }
 
-int sbs_sim_launch(sbs_sim* s, void* stream) {
+int sbs_sim_launch_slot(sbs_sim* s, int32_t slot, void* stream) {
   return guarded([&] {
+    if (slot < 0 || slot >= s->n_slots) throw Error{SBS_ERR_CONFIG, "trace slot out of range"};
     cudaStream_t st = (cudaStream_t)stream;
     CUDA_OR_THROW(cudaSetDevice(s->device));
+    s->cur_slot = slot;
     for (auto& p : s->pts) reset_point(p, st);
     launch_all(*s, st);
+    return SBS_OK;
+  });
+}
+
+int sbs_sim_launch(sbs_sim* s, void* stream) { return sbs_sim_launch_slot(s, 0, stream); }
+
+int sbs_sim_upload_traces_slot(sbs_sim* s, const sbs_trace* traces, int32_t slot, void* stream) {
+  return guarded([&] {
+    CUDA_OR_THROW(cudaSetDevice(s->device));
+    do_upload_traces(*s, traces, (cudaStream_t)stream, slot);
+    return SBS_OK;
+  });
+}
+
+int sbs_sim_enable_trace_slots(sbs_sim* s, int32_t n) {
+  return guarded([&] {
+    if (n != 1 && n != 2) throw Error{SBS_ERR_CONFIG, "trace slots must be 1 or 2"};
+    CUDA_OR_THROW(cudaSetDevice(s->device));
+    if (n == 2 && s->n_slots == 1) {
+      for (auto& t : s->traces) {
+        const size_t m = (size_t)std::max<int64_t>(t.n, 1);
+        CUDA_OR_THROW(cudaMalloc(&t.arr1, 8 * m));
+        CUDA_OR_THROW(cudaMalloc(&t.prompt1, 4 * m));
+        CUDA_OR_THROW(cudaMalloc(&t.output1, 4 * m));
+        s->device_bytes += (int64_t)(16 * m);
+        if (t.pool) {
+          CUDA_OR_THROW(cudaMalloc(&t.pool1, 4 * m));
+          CUDA_OR_THROW(cudaMalloc(&t.psize1, 4 * m));
+          s->device_bytes += (int64_t)(8 * m);
+        }
+      }
+      CUDA_OR_THROW(cudaMalloc(&s->d_pts1, sizeof(sbs::DevPoint) * s->pts.size()));
+      s->n_slots = 2;
+      upload_points(*s);
+    }
     return SBS_OK;
   });
 }
@@ -1208,8 +1275,11 @@ void sbs_sim_destroy(sbs_sim* s) {
     if (t.output) cudaFree(t.output);
     if (t.pool) cudaFree(t.pool);
     if (t.psize) cudaFree(t.psize);
+    for (void* q : {(void*)t.arr1, (void*)t.prompt1, (void*)t.output1, (void*)t.pool1, (void*)t.psize1})
+      if (q) cudaFree(q);
   }
   if (s->d_pts) cudaFree(s->d_pts);
+  if (s->d_pts1) cudaFree(s->d_pts1);
   if (s->d_res) cudaFree(s->d_res);
   if (s->d_counter) cudaFree(s->d_counter);
   for (auto& e : s->ev_des)

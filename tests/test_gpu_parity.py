@@ -224,3 +224,23 @@ def test_trace_reupload_pinned_gather_and_pageable():
                 assert np.array_equal(outs[-1][i], load_case(n)["completion"]), n
     finally:
         sim.close()
+
+
+def test_trace_slots_alternate():
+    """Two trace slots: launches alternate slots (uploads into the idle one)
+    and every launch reproduces the reference; relaunch reuses the last slot."""
+    names = ["decode_dp32", "cfg2_20s", "cache_short"]
+    pts = [P.experiment_from_config(CASES[n]) for n in names]
+    trs = [P.generate_workload(p, pinned=True) for p in pts]
+    sim = P.Simulator(pts, trs, per_request=True)
+    try:
+        sim.enable_trace_slots(2)
+        sim.upload_traces(slot=1)
+        for k in range(4):
+            sim.launch(slot=k & 1)
+            aggs = sim.results()
+            for i, n in enumerate(names):
+                assert aggs[i]["error"] == 0
+                assert np.array_equal(sim.requests(i)["completion"], load_case(n)["completion"]), (k, n)
+    finally:
+        sim.close()
