@@ -1,4 +1,7 @@
-// Persistent discrete-event simulator of the SBS cluster, one warp per replica.
+// Persistent discrete-event simulator of the SBS cluster: one warp per
+// replica, or a prefill warp + a decode warp per replica (two-warp replicas,
+// default for points with decode work, see the channel notes at the event
+// loop and DESIGN.md §3.8).
 //
 // Reproduces reference Runner::run (simulation.cpp:136-169) event for event:
 // every event fires in the reference's (time, seq) order, every allocation
@@ -35,7 +38,15 @@
 //    sorted K multiset, updated in O(U/32) per admission and re-sorted by a
 //    warp LSD radix sort after a decode step.  Step begin is O(1): resident
 //    count and max_u(per_req*B + per_kv*K) are maintained incrementally; the
-//    KV band uses exact per-instance sums of K and K^2.
+//    KV band uses exact per-instance sums of K and K^2.  A step's completion
+//    bucket is final when the step begins and is staged into shared memory
+//    by cp.async while the step runs.
+//  * Cache-aware PBAA (prefill_alloc.cpp:12-21): per prefill DP unit the
+//    PrefixCache LRU is a table of last-use stamps (compiled in only for the
+//    CA kernel variants).
+//  * The hot loops are instruction-cache bound: warp loops stay rolled, cold
+//    paths carry branch hints or sit out of line, and warp reductions use
+//    32-bit REDUX where the operands allow.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -2074,8 +2085,8 @@ __device__ void combine_pair(const DevPoint& pt, DevResult& res, const Counters*
   }
 }
 
-// Two-warp replicas: warp 2k runs the prefill side, warp 2k+1 the decode side
-// of the same replica (shared-memory slice + hand-off channel), synchronised
+// Two-warp replicas in one CTA (SBS_SPLIT=1): the prefill and decode warps of
+// a pair share a shared-memory slice and the hand-off channel, synchronised
 // by a named barrier per pair.
 __device__ __forceinline__ void pair_sync(int pair) {
   asm volatile("bar.sync %0, 64;" ::"r"(pair + 1) : "memory");
