@@ -274,6 +274,15 @@ typedef struct sbs_window_batch {
   const int64_t* hit;
 } sbs_window_batch;
 int sbs_prefill_allocate(const sbs_window_batch* batch, void* stream);
+/* One window from HOST arrays, synchronous (the reference's one-call shape,
+ * allocate_batch prefill_alloc.h:59-62): rows = (id, prompt_len, wait_cycles)
+ * for the n_pending pending then n_new new requests; caps = c_avail per DP
+ * (updated in place); hits = Len_hit rows (NULL: Basic mode).  Outputs as in
+ * sbs_window_batch.  Small Basic windows need one launch and no copies. */
+int sbs_prefill_allocate_one(const int64_t* rows, int32_t n_pending, int32_t n_new,
+                             int64_t* caps, int32_t n_dp, int32_t n_limit,
+                             const int64_t* hits, int32_t* out_dp, int32_t* out_rank,
+                             int32_t* wait_out, uint8_t* flow);
 /* Asynchronous form: enqueue only.  `error_out` is a DEVICE int32 the caller
  * zeroes beforehand; the kernel sets it to SBS_ERR_OVERFLOW when a window
  * exceeds the kernel envelope (1024 requests, 1024 DP units). */

@@ -5,6 +5,7 @@ See DESIGN.md.  The compute path is libsbs_b200.so (CUDA, built in-tree by
 """
 from .api import (  # noqa: F401
     REFERENCE_AGG_KEYS, ConfigError, InvariantError, SbsError, Simulator, allocate_batch,
+    allocate_one,
     experiment_from_config, generate_workload, lib, library_path, run_experiment,
     select_decode_unit,
 )

@@ -200,6 +200,9 @@ def lib():
                                           C.POINTER(Aggregates), C.c_int32]
         L.sbs_prefill_allocate.argtypes = [C.POINTER(WindowBatch), C.c_void_p]
         L.sbs_decode_select.argtypes = [C.POINTER(DecodeBatch), C.c_void_p]
+        L.sbs_prefill_allocate_one.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
+                                               C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                               C.c_void_p, C.c_void_p, C.c_void_p]
         _lib = L
     return _lib
 
@@ -212,6 +215,7 @@ EXPORTED_SYMBOLS = [
     "sbs_prefill_allocate_async", "sbs_decode_select", "sbs_decode_select_async",
     "sbs_last_error", "sbs_version", "sbs_sim_profile_counters", "sbs_sim_des_ms",
     "sbs_sim_enable_trace_slots", "sbs_sim_upload_traces_slot", "sbs_sim_launch_slot",
+    "sbs_prefill_allocate_one",
 ]
 
 
@@ -578,6 +582,31 @@ def run_experiment(cfg: dict, per_request=False, logs=False, device=0):
 
 
 # ----------------------------------------------------------------- allocators
+def allocate_one(pending, new, caps, n_limit, hits=None):
+    """One allocate_batch call from host arrays (sbs_prefill_allocate_one):
+    pending/new rows (id, prompt_len, wait_cycles); returns the same dict as
+    allocate_batch's windows."""
+    p = np.asarray(pending, np.int64).reshape(-1, 3)
+    q = np.asarray(new, np.int64).reshape(-1, 3)
+    rows = np.ascontiguousarray(np.concatenate([p, q]) if len(p) + len(q) else np.zeros((0, 3), np.int64))
+    caps = np.array(caps, np.int64)
+    n, D = len(rows), len(caps)
+    h = None if hits is None else np.ascontiguousarray(np.asarray(hits, np.int64).reshape(n, D))
+    dp, rk, wo = (np.zeros(max(n, 1), np.int32) for _ in range(3))
+    flow = C.c_uint8(0)
+    _check(lib().sbs_prefill_allocate_one(rows.ctypes.data, len(p), len(q), caps.ctypes.data, D,
+                                          int(n_limit), h.ctypes.data if h is not None else None,
+                                          dp.ctypes.data, rk.ctypes.data, wo.ctypes.data,
+                                          C.byref(flow)))
+    placed = np.nonzero(dp[:n] >= 0)[0]
+    placed = placed[np.argsort(rk[placed], kind="stable")]
+    ids = rows[:, 0]
+    return {"mapping": np.stack([ids[placed], dp[placed]], 1) if len(placed) else np.zeros((0, 2), np.int64),
+            "deferred": np.stack([ids[dp[:n] == -1], wo[:n][dp[:n] == -1]], 1)
+            if (dp[:n] == -1).any() else np.zeros((0, 2), np.int64),
+            "throttled": ids[dp[:n] == -2], "caps": caps, "flow": bool(flow.value)}
+
+
 def allocate_batch(windows, device="cuda"):
     """Batched allocate_batch (prefill_alloc.cpp:61-88).
 

@@ -25,6 +25,7 @@ constexpr int kAllocWarps = 4;
 constexpr int kAllocMaxReq = 1024;  // per window (shared-memory sort)
 constexpr int kAllocMaxDp = 1024;
 constexpr int kIqrMaxUnits = 2048;
+constexpr int kOneMax = 32;  // pbaa_one_kernel: requests / DP units by value
 
 // Lexicographic ascending sort of (a, b) pairs in shared memory by a warp.
 __device__ void warp_sort_pairs(uint64_t* a, uint64_t* b, int* idx, int n) {
@@ -71,12 +72,10 @@ struct PbaaArgs {
   const int64_t* hit;
 };
 
-__global__ void __launch_bounds__(32 * kAllocWarps) pbaa_kernel(PbaaArgs A) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int warp = threadIdx.x >> 5, lane = lane_id();
-  const int w = blockIdx.x * kAllocWarps + warp;
-  if (w >= A.n_windows) return;
-  unsigned char* my = smem + warp * (kAllocMaxReq * 20 + kAllocMaxDp * 8);
+// One cluster-window by one warp; `my` is its shared-memory slice
+// (kAllocMaxReq * 20 + kAllocMaxDp * 8 bytes).
+__device__ void pbaa_window(const PbaaArgs& A, int w, unsigned char* my) {
+  const int lane = lane_id();
   uint64_t* ka = (uint64_t*)my;
   uint64_t* kb = ka + kAllocMaxReq;
   int* ki = (int*)(kb + kAllocMaxReq);
@@ -157,6 +156,62 @@ __global__ void __launch_bounds__(32 * kAllocWarps) pbaa_kernel(PbaaArgs A) {
   if (lane == 0) A.flow[w] = any_thr ? 1 : 0;
 }
 
+__global__ void __launch_bounds__(32 * kAllocWarps) pbaa_kernel(PbaaArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5;
+  const int w = blockIdx.x * kAllocWarps + warp;
+  if (w >= A.n_windows) return;
+  pbaa_window(A, w, smem + warp * (kAllocMaxReq * 20 + kAllocMaxDp * 8));
+}
+
+// A single small window passed by value in the kernel parameters (no input
+// copy), results written straight into mapped pinned host memory (no output
+// copy): one launch per call for the reference's one-window interface.
+struct PbaaOne {
+  int32_t n, n_pending, n_dp, n_limit;
+  int64_t req_id[kOneMax];
+  int64_t prompt_len[kOneMax];
+  int32_t wait_in[kOneMax];
+  int64_t caps[kOneMax];
+  int32_t* out;  // mapped host: dp[n], rank[n], wait[n], flow, error; then caps (int64, 8-aligned)
+};
+__global__ void __launch_bounds__(32) pbaa_one_kernel(PbaaOne P) {
+  __shared__ __align__(16) unsigned char slice[kAllocMaxReq * 20 + kAllocMaxDp * 8];
+  __shared__ int64_t s_id[kOneMax], s_len[kOneMax], s_caps[kOneMax], s_off[4];
+  __shared__ int32_t s_wait[kOneMax], s_dp[kOneMax], s_rank[kOneMax], s_wout[kOneMax], s_misc[4];
+  __shared__ uint8_t s_flow;
+  __shared__ int32_t s_err;
+  const int lane = lane_id();
+  for (int i = lane; i < P.n; i += 32) {
+    s_id[i] = P.req_id[i];
+    s_len[i] = P.prompt_len[i];
+    s_wait[i] = P.wait_in[i];
+  }
+  for (int d = lane; d < P.n_dp; d += 32) s_caps[d] = P.caps[d];
+  if (lane == 0) {
+    s_off[0] = 0; s_off[1] = P.n; s_off[2] = 0; s_off[3] = P.n_dp;
+    s_misc[0] = P.n_pending; s_misc[1] = P.n_limit;
+    s_err = 0;
+  }
+  __syncwarp();
+  PbaaArgs A{1, s_off, s_misc, s_off + 2, s_misc + 1, s_id, s_len, s_wait, s_caps,
+             s_dp, s_rank, s_wout, &s_flow, &s_err, nullptr, nullptr};
+  pbaa_window(A, 0, slice);
+  __syncwarp();
+  int32_t* o = P.out;
+  for (int i = lane; i < P.n; i += 32) {
+    o[i] = s_dp[i];
+    o[P.n + i] = s_rank[i];
+    o[2 * P.n + i] = s_wout[i];
+  }
+  int64_t* oc = (int64_t*)(o + ((3 * P.n + 2 + 1) & ~1));
+  for (int d = lane; d < P.n_dp; d += 32) oc[d] = s_caps[d];
+  if (lane == 0) {
+    o[3 * P.n] = s_flow;
+    o[3 * P.n + 1] = s_err;
+  }
+}
+
 struct IqrArgs {
   int32_t n_calls;
   const int64_t* unit_off;
@@ -228,6 +283,23 @@ __global__ void __launch_bounds__(32 * kAllocWarps) iqr_kernel(IqrArgs A) {
     if (A.fallback_out) A.fallback_out[c] = fallback ? 1 : 0;
     if (A.threshold_out) A.threshold_out[c] = th;
   }
+}
+
+cudaError_t launch_pbaa_one(const int64_t* rows, int n_pending, int n_new, const int64_t* caps,
+                            int n_dp, int n_limit, int32_t* mapped_out, cudaStream_t st) {
+  const int n = n_pending + n_new;
+  if (n > kOneMax || n_dp > kOneMax || n_dp < 1) return cudaErrorInvalidValue;
+  PbaaOne P;
+  P.n = n; P.n_pending = n_pending; P.n_dp = n_dp; P.n_limit = n_limit;
+  for (int i = 0; i < n; ++i) {
+    P.req_id[i] = rows[3 * i];
+    P.prompt_len[i] = rows[3 * i + 1];
+    P.wait_in[i] = (int32_t)rows[3 * i + 2];
+  }
+  for (int d = 0; d < n_dp; ++d) P.caps[d] = caps[d];
+  P.out = mapped_out;
+  pbaa_one_kernel<<<1, 32, 0, st>>>(P);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_pbaa(const PbaaArgs& a, cudaStream_t st) {

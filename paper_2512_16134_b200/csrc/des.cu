@@ -2094,7 +2094,7 @@ __device__ __forceinline__ void pair_sync(int pair) {
 
 // Warps [0, R) are the prefill warps and [R, 2R) the decode warps of R pairs,
 // so with R = 4 every scheduler partition (warp % 4) holds one decode warp.
-template <int KD>
+template <int KD, bool CA = false>
 __global__ void __launch_bounds__(256) des_split_kernel(const DevPoint* __restrict__ pts, int n_pts,
                                                         int* __restrict__ next_point,
                                                         DevResult* __restrict__ res,
@@ -2115,7 +2115,7 @@ __global__ void __launch_bounds__(256) des_split_kernel(const DevPoint* __restri
     if (role == 0 && lane == 0)
       for (int i = 0; i < 24; ++i) res[pi].prof[i] = 0;
     pair_sync(pair);
-    if (role == 0) run_replica<KD, false, 1, false>(pt, res[pi], my, my);
+    if (role == 0) run_replica<KD, false, 1, false, CA>(pt, res[pi], my, my);
     else run_replica<KD, false, 2, false>(pt, res[pi], my, my);
     pair_sync(pair);
     if (role == 0)
@@ -2132,7 +2132,7 @@ __global__ void __launch_bounds__(256) des_split_kernel(const DevPoint* __restri
 // the reader's own shared memory and written remotely (DSMEM) by the other
 // side.  Replicas go round-robin over clusters, rounds separated by a
 // cluster barrier.
-template <int KD>
+template <int KD, bool CA = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256)
     des_cluster_kernel(const DevPoint* __restrict__ pts, int n_pts, int* __restrict__ unused,
                        DevResult* __restrict__ res, int smem_per_rep) {
@@ -2158,7 +2158,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256)
       for (int i = 0; i < 24; ++i) res[pi].prof[i] = 0;
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     if (active) {
-      if (crank == 0) run_replica<KD, false, 1, true>(pts[pi], res[pi], my, peer);
+      if (crank == 0) run_replica<KD, false, 1, true, CA>(pts[pi], res[pi], my, peer);
       else run_replica<KD, false, 2, true>(pts[pi], res[pi], my, peer);
     }
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -2247,21 +2247,22 @@ __global__ void __launch_bounds__(256) finalize_kernel(const DevPoint* __restric
 namespace sbs {
 // variant: bit 0 = dp_degree > 32 (KD 4), bit 1 = run records, 4|5 = two-warp
 // replicas (smem_per_warp is then the per-pair slice, warps_per_block even),
-// 6..9 = 0..3 with the cache-aware dispatch compiled in
+// 6..9 = 0..3 and 10|11 = 4|5 with the cache-aware dispatch compiled in
 cudaError_t launch_des(int variant, const DevPoint* d_pts, int n_pts, int* d_counter,
                        DevResult* d_res, int smem_per_warp, int warps_per_block, int n_blocks,
                        int min_smem, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(d_counter, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
   // one-warp variants: a slice per warp; two-warp variants: a slice per pair
-  const bool pairs = variant == 4 || variant == 5;
+  const bool pairs = variant == 4 || variant == 5 || variant == 10 || variant == 11;
   size_t smem = (size_t)smem_per_warp * (pairs ? warps_per_block / 2 : warps_per_block);
   void (*k)(const DevPoint*, int, int*, DevResult*, int) =
       variant == 0 ? des_kernel<1, false> : variant == 1 ? des_kernel<4, false>
     : variant == 2 ? des_kernel<1, true> : variant == 3 ? des_kernel<4, true>
     : variant == 6 ? des_kernel<1, false, true> : variant == 7 ? des_kernel<4, false, true>
     : variant == 8 ? des_kernel<1, true, true> : variant == 9 ? des_kernel<4, true, true>
-    : variant == 4 ? des_split_kernel<1> : des_split_kernel<4>;
+    : variant == 4 ? des_split_kernel<1> : variant == 5 ? des_split_kernel<4>
+    : variant == 10 ? des_split_kernel<1, true> : des_split_kernel<4, true>;
   if (min_smem > 0 && smem < (size_t)min_smem) smem = (size_t)min_smem;  // CTAs per SM cap
   e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -2275,7 +2276,8 @@ cudaError_t launch_des(int variant, const DevPoint* d_pts, int n_pts, int* d_cou
 cudaError_t launch_des_cluster(int variant, const DevPoint* d_pts, int n_pts, DevResult* d_res,
                                int smem_per_rep, cudaStream_t st) {
   void (*k)(const DevPoint*, int, int*, DevResult*, int) =
-      variant == 4 ? des_cluster_kernel<1> : des_cluster_kernel<4>;
+      variant == 4 ? des_cluster_kernel<1> : variant == 5 ? des_cluster_kernel<4>
+    : variant == 10 ? des_cluster_kernel<1, true> : des_cluster_kernel<4, true>;
   constexpr int kMaxSmem = 227 * 1024, kOnePerSm = 120 * 1024;
   int wmax = 8;
   while (wmax > 1 && wmax * smem_per_rep > kMaxSmem) --wmax;

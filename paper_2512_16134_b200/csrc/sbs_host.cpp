@@ -74,6 +74,8 @@ struct IqrArgs {
   int32_t* error;
 };
 cudaError_t launch_pbaa(const PbaaArgs& a, cudaStream_t st);
+cudaError_t launch_pbaa_one(const int64_t* rows, int n_pending, int n_new, const int64_t* caps,
+                            int n_dp, int n_limit, int32_t* mapped_out, cudaStream_t st);
 cudaError_t launch_iqr(const IqrArgs& a, cudaStream_t st);
 }  // namespace sbs
 
@@ -374,7 +376,7 @@ struct sbs_sim {
   std::vector<PointHost> pts;
   std::vector<TraceDev> traces;
   std::vector<int> order;  // device slot -> point index (grouped by variant, cost-descending)
-  static constexpr int kVariants = 10;
+  static constexpr int kVariants = 12;
   int group_begin[kVariants + 1] = {};  // slots of kernel variant v: [group_begin[v], group_begin[v+1])
   sbs::DevPoint* d_pts = nullptr;
   sbs::DevResult* d_res = nullptr;
@@ -465,7 +467,8 @@ void build_point(sbs_sim& s, PointHost& p) {
     // (completion-ring entries carry times in 48 bits)
     // (cache-aware points run on the one-warp kernels that compile the cache in)
     const bool ca = x.prefill_mode == SBS_ALLOC_CACHE_AWARE && c.cache_enabled && t.pool != nullptr;
-    d.split = (allow && p.split && !ca && !(s.flags & SBS_FLAG_LOGS) && t.max_output > 1 &&
+    (void)ca;
+    d.split = (allow && p.split && !(s.flags & SBS_FLAG_LOGS) && t.max_output > 1 &&
                seconds_to_ns(x.workload.duration_s) < (int64_t(1) << 47)) ? 1 : 0;
   }
   d.c_chunk = c.c_chunk;
@@ -679,7 +682,7 @@ void grow_caps(PointHost& p) {
 }
 
 int variant_of(const PointHost& p) {
-  if (p.dp.split) return 4 | (p.dp.D > 32 ? 1 : 0);
+  if (p.dp.split) return (4 | (p.dp.D > 32 ? 1 : 0)) + (p.dp.cache_on ? 6 : 0);
   return (p.dp.D > 32 ? 1 : 0) + (p.dp.log != nullptr ? 2 : 0) + (p.dp.cache_on ? 6 : 0);
 }
 
@@ -696,6 +699,9 @@ void order_points(sbs_sim& s) {
   for (int i = 0; i < n; ++i) s.group_begin[variant_of(s.pts[s.order[i]]) + 1] += 1;
   for (int v = 1; v <= sbs_sim::kVariants; ++v) s.group_begin[v] += s.group_begin[v - 1];
 }
+
+// Kernel variants whose replicas are warp pairs (prefill warp + decode warp).
+bool is_pair_variant(int v) { return v == 4 || v == 5 || v == 10 || v == 11; }
 
 void launch_all(sbs_sim& s, cudaStream_t st) {
   s.n_launches = 0;
@@ -714,8 +720,8 @@ void launch_all(sbs_sim& s, cudaStream_t st) {
   int total_blocks = 0;
   for (int v = 0; v < sbs_sim::kVariants; ++v) {
     const int n = s.group_begin[v + 1] - s.group_begin[v];
-    if (n <= 0 || ((v == 4 || v == 5) && s.pair_mode == 2)) continue;
-    const int per = (v == 4 || v == 5) ? std::max(1, std::min(4, (n + s.sm_count - 1) / s.sm_count))
+    if (n <= 0 || (is_pair_variant(v) && s.pair_mode == 2)) continue;
+    const int per = is_pair_variant(v) ? std::max(1, std::min(4, (n + s.sm_count - 1) / s.sm_count))
                                        : s.warps_per_block;
     total_blocks += (n + per - 1) / per;
   }
@@ -730,10 +736,10 @@ void launch_all(sbs_sim& s, cudaStream_t st) {
     CUDA_OR_THROW(cudaStreamWaitEvent(vs, s.ev_des[0], 0));
     used[v] = 1;
     int wpb = s.warps_per_block, per_block = wpb;
-    if ((v == 4 || v == 5) && s.pair_mode == 2) {  // replica = a CTA pair of a 2-CTA cluster
+    if (is_pair_variant(v) && s.pair_mode == 2) {  // replica = a CTA pair of a 2-CTA cluster
       CUDA_OR_THROW(sbs::launch_des_cluster(v, dp + b, e - b, s.d_res + b, s.smem_per_warp, vs));
     } else {
-      if (v == 4 || v == 5) {  // two warps per replica; up to four replicas per block
+      if (is_pair_variant(v)) {  // two warps per replica; up to four replicas per block
         int rpb = std::max(1, std::min(4, (e - b + s.sm_count - 1) / s.sm_count));
         while (rpb > 1 && (size_t)rpb * s.smem_per_warp > 227 * 1024) --rpb;
         wpb = 2 * rpb;
@@ -1365,6 +1371,107 @@ int sbs_prefill_allocate(const sbs_window_batch* b, void* stream) {
     CUDA_OR_THROW(cudaMemcpyAsync(sc.h_err, sc.d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CUDA_OR_THROW(cudaStreamSynchronize(st));
     if (*sc.h_err) throw Error{*sc.h_err, "window exceeds the kernel's shared-memory envelope"};
+    return SBS_OK;
+  });
+}
+
+// One window from host arrays (the reference's allocate_batch call shape).
+// Small Basic-mode windows travel in the kernel parameters and come back
+// through mapped pinned memory: one launch and one synchronisation per call.
+// Larger or cache-aware windows use a per-thread device staging block.
+struct OneWindow {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  int32_t* mapped = nullptr;             // pinned, device-visible outputs
+  unsigned char* host = nullptr;         // staged path
+  unsigned char* dev = nullptr;
+  size_t cap = 0;
+};
+OneWindow& one_window() {
+  thread_local OneWindow w;
+  int dev = 0;
+  CUDA_OR_THROW(cudaGetDevice(&dev));
+  if (w.device != dev) {
+    CUDA_OR_THROW(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
+    CUDA_OR_THROW(cudaHostAlloc(&w.mapped, 4096, cudaHostAllocMapped));
+    w.device = dev;
+  }
+  return w;
+}
+
+int sbs_prefill_allocate_one(const int64_t* rows, int32_t n_pending, int32_t n_new, int64_t* caps,
+                             int32_t n_dp, int32_t n_limit, const int64_t* hits, int32_t* out_dp,
+                             int32_t* out_rank, int32_t* wait_out, uint8_t* flow) {
+  return guarded([&] {
+    const int n = n_pending + n_new;
+    if (n_dp < 1 || n_pending < 0 || n_new < 0) throw Error{SBS_ERR_CONFIG, "bad window shape"};
+    OneWindow& w = one_window();
+    if (hits == nullptr && n <= 32 && n_dp <= 32) {
+      int32_t* o = nullptr;
+      CUDA_OR_THROW(cudaHostGetDevicePointer((void**)&o, w.mapped, 0));
+      CUDA_OR_THROW(sbs::launch_pbaa_one(rows, n_pending, n_new, caps, n_dp, n_limit, o, w.stream));
+      CUDA_OR_THROW(cudaStreamSynchronize(w.stream));
+      const int32_t* m = w.mapped;
+      if (m[3 * n + 1]) throw Error{SBS_ERR_OVERFLOW, "window exceeds the kernel envelope"};
+      std::memcpy(out_dp, m, 4 * (size_t)n);
+      std::memcpy(out_rank, m + n, 4 * (size_t)n);
+      std::memcpy(wait_out, m + 2 * n, 4 * (size_t)n);
+      *flow = (uint8_t)m[3 * n];
+      std::memcpy(caps, (const int64_t*)(m + ((3 * n + 3) & ~1)), 8 * (size_t)n_dp);
+      return SBS_OK;
+    }
+    // staged: [req_off 2][n_pending][dp_off 2][n_limit][ids][lens][waits][caps][hit_off 2][hits]
+    //         [dp][rank][wait_out][flow][err]
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = (off + bytes + 7) & ~size_t(7); return o; };
+    const size_t o_roff = take(16), o_np = take(4), o_doff = take(16), o_nl = take(4),
+                 o_id = take(8 * (size_t)n), o_len = take(8 * (size_t)n), o_win = take(4 * (size_t)n),
+                 o_caps = take(8 * (size_t)n_dp), o_hoff = take(16),
+                 o_hit = take(hits ? 8 * (size_t)n * n_dp : 0), o_dp = take(4 * (size_t)n),
+                 o_rank = take(4 * (size_t)n), o_wout = take(4 * (size_t)n), o_flow = take(8),
+                 o_err = take(8);
+    if (off > w.cap) {
+      if (w.host) cudaFreeHost(w.host);
+      if (w.dev) cudaFree(w.dev);
+      w.cap = std::max(off, 2 * w.cap);
+      CUDA_OR_THROW(cudaMallocHost(&w.host, w.cap));
+      CUDA_OR_THROW(cudaMalloc(&w.dev, w.cap));
+    }
+    unsigned char* h = w.host;
+    const int64_t roff[2] = {0, n}, doff[2] = {0, n_dp}, hoff[2] = {0, (int64_t)n * n_dp};
+    std::memcpy(h + o_roff, roff, 16);
+    std::memcpy(h + o_np, &n_pending, 4);
+    std::memcpy(h + o_doff, doff, 16);
+    std::memcpy(h + o_nl, &n_limit, 4);
+    for (int i = 0; i < n; ++i) {
+      ((int64_t*)(h + o_id))[i] = rows[3 * i];
+      ((int64_t*)(h + o_len))[i] = rows[3 * i + 1];
+      ((int32_t*)(h + o_win))[i] = (int32_t)rows[3 * i + 2];
+    }
+    std::memcpy(h + o_caps, caps, 8 * (size_t)n_dp);
+    std::memcpy(h + o_hoff, hoff, 16);
+    if (hits) std::memcpy(h + o_hit, hits, 8 * (size_t)n * n_dp);
+    *(int32_t*)(h + o_err) = 0;
+    unsigned char* g = w.dev;
+    CUDA_OR_THROW(cudaMemcpyAsync(g, h, off, cudaMemcpyHostToDevice, w.stream));
+    sbs::PbaaArgs a{1, (const int64_t*)(g + o_roff), (const int32_t*)(g + o_np),
+                    (const int64_t*)(g + o_doff), (const int32_t*)(g + o_nl),
+                    (const int64_t*)(g + o_id), (const int64_t*)(g + o_len),
+                    (const int32_t*)(g + o_win), (int64_t*)(g + o_caps), (int32_t*)(g + o_dp),
+                    (int32_t*)(g + o_rank), (int32_t*)(g + o_wout), (uint8_t*)(g + o_flow),
+                    (int32_t*)(g + o_err), hits ? (const int64_t*)(g + o_hoff) : nullptr,
+                    hits ? (const int64_t*)(g + o_hit) : nullptr};
+    CUDA_OR_THROW(sbs::launch_pbaa(a, w.stream));
+    CUDA_OR_THROW(cudaMemcpyAsync(h + o_dp, g + o_dp, off - o_dp, cudaMemcpyDeviceToHost, w.stream));
+    CUDA_OR_THROW(cudaMemcpyAsync(h + o_caps, g + o_caps, 8 * (size_t)n_dp, cudaMemcpyDeviceToHost,
+                                  w.stream));
+    CUDA_OR_THROW(cudaStreamSynchronize(w.stream));
+    if (*(int32_t*)(h + o_err)) throw Error{SBS_ERR_OVERFLOW, "window exceeds the kernel envelope"};
+    std::memcpy(out_dp, h + o_dp, 4 * (size_t)n);
+    std::memcpy(out_rank, h + o_rank, 4 * (size_t)n);
+    std::memcpy(wait_out, h + o_wout, 4 * (size_t)n);
+    *flow = h[o_flow];
+    std::memcpy(caps, h + o_caps, 8 * (size_t)n_dp);
     return SBS_OK;
   });
 }

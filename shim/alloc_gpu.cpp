@@ -9,8 +9,9 @@
 // percentile / outlier_threshold / lex_less are the scalar helpers the
 // reference's metrics also use (metrics.cpp:151-152); they stay host math.
 //
-// Cache-aware PBAA (AllocMode::kCacheAware) is outside the GPU path's scope
-// and raises ConfigError, as any unsupported configuration does.
+// Cache-aware PBAA (AllocMode::kCacheAware): Len_hit(r, d) is resolved on the
+// host against the PrefixCache objects the caller's DpPlans borrow and shipped
+// with the window; the kernel does the argmax / guard / update.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -72,7 +73,8 @@ struct WindowOut {
   bool flow = false;
 };
 
-// One cluster-window through the batched PBAA kernel.
+// One cluster-window through the PBAA kernel (sbs_prefill_allocate_one: small
+// Basic windows travel in the kernel parameters, one launch per call).
 WindowOut run_window(std::span<sbsim::Request* const> pending,
                      std::span<sbsim::Request* const> fresh,
                      const std::vector<sbsim::DpPlan>& dps, int n_limit, sbsim::AllocMode mode) {
@@ -80,73 +82,30 @@ WindowOut run_window(std::span<sbsim::Request* const> pending,
   // cache-aware: Len_hit(r, d) resolved against the caller's caches (the
   // PrefixCache objects the DpPlans borrow, prefill_alloc.h:22)
   const bool ca = mode == sbsim::AllocMode::kCacheAware;
-  // layout in the staging block
-  size_t off = 0;
-  auto take = [&](size_t bytes) { size_t o = off; off = align8(off + bytes); return o; };
-  const size_t o_roff = take(16), o_np = take(4), o_doff = take(16), o_nl = take(4),
-               o_id = take(8 * n), o_len = take(8 * n), o_win = take(4 * n), o_caps = take(8 * D),
-               o_dp = take(4 * n), o_rank = take(4 * n), o_wout = take(4 * n),
-               o_flow = take(8), o_err = take(8), o_hoff = take(ca ? 16 : 0),
-               o_hit = take(ca ? 8 * n * D : 0);
-  g_st.ensure(off + 64);
-  unsigned char* h = g_st.host;
-  int64_t roff[2] = {0, (int64_t)n}, doff[2] = {0, (int64_t)D};
-  int32_t np = (int32_t)pending.size(), nl = n_limit;
-  std::memcpy(h + o_roff, roff, 16);
-  std::memcpy(h + o_np, &np, 4);
-  std::memcpy(h + o_doff, doff, 16);
-  std::memcpy(h + o_nl, &nl, 4);
+  thread_local std::vector<int64_t> rows, hits;
+  rows.resize(3 * n);
+  hits.resize(ca ? n * D : 0);
   size_t i = 0;
   for (auto* q : {&pending, &fresh})
     for (sbsim::Request* r : *q) {
-      ((int64_t*)(h + o_id))[i] = (int64_t)r->id;
-      ((int64_t*)(h + o_len))[i] = r->prompt_len;
-      ((int32_t*)(h + o_win))[i] = r->wait_cycles;
+      rows[3 * i] = (int64_t)r->id;
+      rows[3 * i + 1] = r->prompt_len;
+      rows[3 * i + 2] = r->wait_cycles;
+      if (ca)
+        for (size_t d = 0; d < D; ++d) hits[i * D + d] = sbsim::cache_hit_len(*r, dps[d]);
       ++i;
     }
-  for (size_t d = 0; d < D; ++d) ((int64_t*)(h + o_caps))[d] = dps[d].c_avail;
-  if (ca) {
-    int64_t hoff[2] = {0, (int64_t)(n * D)};
-    std::memcpy(h + o_hoff, hoff, 16);
-    size_t r = 0;
-    for (auto* q : {&pending, &fresh})
-      for (sbsim::Request* req : *q) {
-        for (size_t d = 0; d < D; ++d)
-          ((int64_t*)(h + o_hit))[r * D + d] = sbsim::cache_hit_len(*req, dps[d]);
-        ++r;
-      }
-  }
-  *(int32_t*)(h + o_err) = 0;
-  unsigned char* g = g_st.dev;
-  // one H2D of the whole block (inputs + zeroed error word), one kernel, one D2H
-  Staging::check(cudaMemcpyAsync(g, h, off, cudaMemcpyHostToDevice, g_st.stream));
-  sbs_window_batch b{};
-  b.n_windows = 1;
-  b.req_off = (const int64_t*)(g + o_roff);
-  b.n_pending = (const int32_t*)(g + o_np);
-  b.dp_off = (const int64_t*)(g + o_doff);
-  b.n_limit = (const int32_t*)(g + o_nl);
-  b.req_id = (const int64_t*)(g + o_id);
-  b.prompt_len = (const int64_t*)(g + o_len);
-  b.wait_in = (const int32_t*)(g + o_win);
-  b.caps = (int64_t*)(g + o_caps);
-  b.out_dp = (int32_t*)(g + o_dp);
-  b.out_rank = (int32_t*)(g + o_rank);
-  b.wait_out = (int32_t*)(g + o_wout);
-  b.flow = (uint8_t*)(g + o_flow);
-  b.hit_off = ca ? (const int64_t*)(g + o_hoff) : nullptr;
-  b.hit = ca ? (const int64_t*)(g + o_hit) : nullptr;
-  throw_rc(sbs_prefill_allocate_async(&b, (int32_t*)(g + o_err), g_st.stream));
-  Staging::check(cudaMemcpyAsync(h + o_caps, g + o_caps, o_err + 8 - o_caps, cudaMemcpyDeviceToHost,
-                                 g_st.stream));
-  Staging::check(cudaStreamSynchronize(g_st.stream));
-  if (*(int32_t*)(h + o_err)) throw_rc(SBS_ERR_OVERFLOW);
   WindowOut w;
-  w.dp.assign((int32_t*)(h + o_dp), (int32_t*)(h + o_dp) + n);
-  w.rank.assign((int32_t*)(h + o_rank), (int32_t*)(h + o_rank) + n);
-  w.wait.assign((int32_t*)(h + o_wout), (int32_t*)(h + o_wout) + n);
-  w.caps.assign((int64_t*)(h + o_caps), (int64_t*)(h + o_caps) + D);
-  w.flow = h[o_flow] != 0;
+  w.dp.resize(n);
+  w.rank.resize(n);
+  w.wait.resize(n);
+  w.caps.resize(D);
+  for (size_t d = 0; d < D; ++d) w.caps[d] = dps[d].c_avail;
+  uint8_t flow = 0;
+  throw_rc(sbs_prefill_allocate_one(rows.data(), (int32_t)pending.size(), (int32_t)fresh.size(),
+                                    w.caps.data(), (int32_t)D, n_limit, ca ? hits.data() : nullptr,
+                                    w.dp.data(), w.rank.data(), w.wait.data(), &flow));
+  w.flow = flow != 0;
   return w;
 }
 

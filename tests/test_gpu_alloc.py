@@ -122,3 +122,25 @@ def test_iqr_kats_and_random():
         for i, (B, K) in enumerate(calls):
             e = orc.select_decode_unit(B, K, k)
             assert (pos[i], fb[i], th[i]) == e
+
+
+def test_allocate_one_host_arrays():
+    """sbs_prefill_allocate_one (host arrays, one call per window): the small
+    by-value path and the staged path (> 32 requests, cache-aware hits) give
+    the reference's results on the recorded windows."""
+    wins = records_windows(np.load(GOLD / "windows_short_3k.npz")["records"])
+    for w in wins[:300]:
+        g = P.allocate_one(w["pending"], w["new"], w["caps"], w["n_limit"])
+        assert g["mapping"].tolist() == w["mapping"]
+        assert g["deferred"].tolist() == w["deferred"]
+        assert g["throttled"].tolist() == w["throttled"]
+        assert g["caps"].tolist() == w["caps_out"]
+        assert g["flow"] == w["flow"]
+    assert any(len(w["pending"]) + len(w["new"]) > 32 for w in wins[:300])
+    wins = records_windows_ca(np.load(GOLD / "windows_cache_aware.npz")["records"])
+    for w in wins[:100]:
+        g = P.allocate_one(w["pending"], w["new"], w["caps"], w["n_limit"], hits=w["hits"])
+        assert g["mapping"].tolist() == w["mapping"]
+        assert g["deferred"].tolist() == w["deferred"]
+        assert g["throttled"].tolist() == w["throttled"]
+        assert g["caps"].tolist() == w["caps_out"]

@@ -35,7 +35,7 @@ def _same(a, b, name):
 
 
 @pytest.mark.parametrize("mode", [1, 2])
-@pytest.mark.parametrize("name", ["decode_dp32", "cfg2_20s", "short_3k", "oracle_n8"])
+@pytest.mark.parametrize("name", ["decode_dp32", "cfg2_20s", "short_3k", "oracle_n8", "cache_pd", "cache_pd_dp33"])
 def test_split_equals_serial(name, mode, monkeypatch):
     _same(_run(CASES[name], mode, monkeypatch), _run(CASES[name], 0, monkeypatch), name)
 
