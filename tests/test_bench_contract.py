@@ -1,0 +1,40 @@
+"""CPU: bench.py's reference arm (the compiled reference on the host cores)
+prints the contract's JSON line; the workload slices are what DESIGN.md says."""
+import json
+import subprocess
+import sys
+from collections import Counter
+from pathlib import Path
+
+import pytest
+
+from oracle import ref
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+import bench  # noqa: E402
+
+
+def test_workload_slices():
+    d, c5 = bench.workload_points("cfg5", 0, 1)
+    assert len(c5) == 512 and c5[0]["workload"]["duration_s"] == 5000.0
+    seeds = {c["sim"]["seed"] for r in range(8) for c in bench.workload_points("cfg5", r, 8)[1]}
+    assert len(seeds) == 8 * 512  # the 4096-replica sweep, no seed twice
+    for r in range(8):  # cfg4: every rank gets every dp_degree
+        _, c4 = bench.workload_points("cfg4", r, 8)
+        assert Counter(c["cluster"]["dp_degree"] for c in c4) == {d: 16 for d in (1, 2, 4, 8, 16, 32, 64, 128)}
+
+
+@pytest.mark.skipif(not ref.available(), reason="compiled reference unavailable")
+def test_reference_arm_json_line():
+    p = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--workload", "cfg1",
+                        "--replicas", "4", "--steps", "1", "--warmup", "1"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "dtype", "data", "config", "cpu_baseline", "e2e"):
+        assert k in line, k
+    assert line["impl"] == "reference" and line["value"] > 0
+    assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
