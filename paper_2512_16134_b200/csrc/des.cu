@@ -1031,7 +1031,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       complete_lanes(done, id, now, false, arr, out, disp, ps, now);
       unsigned m = __ballot_sync(kFull, wait);
       if (ROLE == 1) {
-        // hand-off ring: wait for room (the decode warp consumes independently)
+        // hand-off ring: wait for room (the decode warp consumes independently);
+        // one EndForward's keys must fit the ring whole, else run on one warp
+        if (m && ndw + 32 > kChanKeys) { error = kErrSplitTie; break; }
         if (m) {
           for (;;) {
             const int kh = chL->khead;
