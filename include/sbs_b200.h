@@ -153,7 +153,9 @@ typedef struct sbs_aggregates {
   uint64_t alloc_calls;     /* allocate_batch invocations (cluster-windows) */
   uint64_t decode_selects;  /* decode placements */
   uint64_t events;          /* live events processed */
-  double tpot_mean_s;       /* (completion-first_token)/(output_len-1), output_len>1 */
+  double tpot_mean_s;       /* mean over completed requests with output_len > 1 of
+                               (completion_ns - first_token_ns) / (output_len - 1),
+                               one IEEE FP64 division per request, then / 1e9 */
   uint64_t tpot_count;
   int64_t ttft_sum_ns, sched_sum_ns, device_sum_ns; /* exact int64 sums */
   int32_t error;            /* per-replica SBS_* code */
@@ -162,7 +164,9 @@ typedef struct sbs_aggregates {
 
 #define SBS_HIST_BINS 64
 /* TTFT / TPOT log2-spaced histograms (bin b counts values in [2^b, 2^(b+1)) ns,
- * bin 0 also holds 0) summed over replicas; NCCL-reducible as int64. */
+ * bin 0 also holds 0) summed over replicas; NCCL-reducible as int64.
+ * ttft: first_token - arrival of the window requests (completed, arrival >=
+ * warmup: metrics.cpp:122-136); tpot: trunc of the per-request TPOT in ns. */
 typedef struct sbs_histograms {
   int64_t ttft[SBS_HIST_BINS];
   int64_t tpot[SBS_HIST_BINS];

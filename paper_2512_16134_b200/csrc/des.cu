@@ -577,8 +577,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         o_status[id] = kStCompleted;
       }
       if (decode) {
-        // TPOT (not in the reference): ns per output token after the first
-        const double per = __dmul_rn((double)(t_done - ftok), __drcp_rn((double)(out - 1)));
+        // TPOT (not in the reference): ns per output token after the first,
+        // one IEEE division (include/sbs_b200.h; pinned by test_gpu_north_star)
+        const double per = __ddiv_rn((double)(t_done - ftok), (double)(out - 1));
         tpot_sum = __dadd_rn(tpot_sum, per);
         tpot_n += 1;
         atomicAdd((unsigned long long*)&g_tpot_hist[hist_bin((int64_t)per)], 1ull);
