@@ -184,6 +184,42 @@ int sbs_generate_workload(const sbs_workload* spec, uint64_t seed,
                           uint64_t* digest);
 
 /* ----------------------------------------------------------------------- */
+/* Trace generation ON THE DEVICE: generate_workload + workload_digest      */
+/* (workload.cpp:67-162), one warp per trace, bit-identical to the host     */
+/* run on glibc 2.39 x86-64 (its FMA-path log/cos/exp are restated in       */
+/* csrc/glibc_libm.cuh).  Output arrays and `stats` are DEVICE pointers;     */
+/* a trace longer than `cap` sets stats->error = SBS_ERR_OVERFLOW (n = 0).   */
+typedef struct sbs_gen_stats {
+  int64_t n;            /* requests generated */
+  uint64_t digest;      /* workload_digest (when requested, else 0) */
+  int32_t max_prompt, max_output;
+  int32_t n_pools;      /* 1 + largest prefix pool id used (0: none) */
+  int32_t max_psize;    /* largest prefix size */
+  int32_t error;        /* SBS_OK / SBS_ERR_OVERFLOW / SBS_ERR_CONFIG (length > 2^30) */
+  int32_t _pad;
+  int64_t draws;        /* mt19937_64 outputs consumed */
+} sbs_gen_stats;
+typedef struct sbs_gen_job {
+  sbs_workload spec;
+  uint64_t seed;
+  int64_t cap;
+  int64_t* arrival_ns;
+  int32_t* prompt_len;
+  int32_t* output_len;
+  int32_t* prefix_pool_id; /* both NULL unless spec.shared_prefix_fraction > 0 */
+  int32_t* prefix_size;
+  sbs_gen_stats* stats;
+} sbs_gen_job;
+/* jobs: HOST array (copied); seeds: DEVICE array overriding jobs[i].seed, or
+ * NULL.  Enqueued on `stream`. */
+int sbs_generate_workload_device(const sbs_gen_job* jobs, int32_t n_jobs, const uint64_t* seeds,
+                                 int32_t want_digest, void* stream);
+/* An upper bound on the requests generate_workload can produce for `spec`
+ * with probability 1 - 1e-12 (Poisson: initial_burst + mean + 8 sd + 64),
+ * exact for the uniform processes. */
+int64_t sbs_workload_capacity(const sbs_workload* spec);
+
+/* ----------------------------------------------------------------------- */
 /* Persistent replica simulator (the DES hot path).                         */
 /* Replaces run_experiment (simulation.h:33 / simulation.cpp:537-541) for   */
 /* many independent replicas at once: one warp per replica.                 */

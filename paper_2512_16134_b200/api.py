@@ -155,6 +155,19 @@ class DecodeBatch(C.Structure):
                 ("threshold_out", C.c_void_p)]
 
 
+class GenStats(C.Structure):
+    _fields_ = [("n", C.c_int64), ("digest", C.c_uint64), ("max_prompt", C.c_int32),
+                ("max_output", C.c_int32), ("n_pools", C.c_int32), ("max_psize", C.c_int32),
+                ("error", C.c_int32), ("_pad", C.c_int32), ("draws", C.c_int64)]
+
+
+class GenJob(C.Structure):
+    _fields_ = [("spec", Workload), ("seed", C.c_uint64), ("cap", C.c_int64),
+                ("arrival_ns", C.c_void_p), ("prompt_len", C.c_void_p),
+                ("output_len", C.c_void_p), ("prefix_pool_id", C.c_void_p),
+                ("prefix_size", C.c_void_p), ("stats", C.c_void_p)]
+
+
 # ----------------------------------------------------------------- library
 _lib = None
 
@@ -176,6 +189,10 @@ def lib():
                                             C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                             C.c_int64, C.POINTER(C.c_int64),
                                             C.POINTER(C.c_uint64)]
+        L.sbs_generate_workload_device.argtypes = [C.POINTER(GenJob), C.c_int32, C.c_void_p,
+                                                   C.c_int32, C.c_void_p]
+        L.sbs_workload_capacity.argtypes = [C.POINTER(Workload)]
+        L.sbs_workload_capacity.restype = C.c_int64
         L.sbs_sim_create.argtypes = [C.POINTER(Experiment), C.c_int32, C.POINTER(Trace),
                                      C.c_int32, C.c_void_p, C.c_uint32, C.c_int32,
                                      C.POINTER(C.c_void_p)]
@@ -215,7 +232,7 @@ EXPORTED_SYMBOLS = [
     "sbs_prefill_allocate_async", "sbs_decode_select", "sbs_decode_select_async",
     "sbs_last_error", "sbs_version", "sbs_sim_profile_counters", "sbs_sim_des_ms",
     "sbs_sim_enable_trace_slots", "sbs_sim_upload_traces_slot", "sbs_sim_launch_slot",
-    "sbs_prefill_allocate_one",
+    "sbs_prefill_allocate_one", "sbs_generate_workload_device", "sbs_workload_capacity",
 ]
 
 
@@ -464,6 +481,78 @@ def generate_workload(point_or_cfg, pinned: bool = False) -> HostTrace:
     if pp is not None:
         pp, ps = pp[:k], ps[:k]
     return HostTrace(a[:k], p[:k], o[:k], dg.value, pp, ps)
+
+
+@dataclass
+class DeviceTrace:
+    """A trace generated on the GPU (torch tensors in HBM) and its stats."""
+    arrival_ns: object
+    prompt_len: object
+    output_len: object
+    prefix_pool_id: object
+    prefix_size: object
+    n: int
+    digest: int
+    stats: dict
+
+    def to_host(self) -> HostTrace:
+        k = self.n
+        pp = self.prefix_pool_id[:k].cpu().numpy() if self.prefix_pool_id is not None else None
+        ps = self.prefix_size[:k].cpu().numpy() if self.prefix_size is not None else None
+        return HostTrace(self.arrival_ns[:k].cpu().numpy(), self.prompt_len[:k].cpu().numpy(),
+                         self.output_len[:k].cpu().numpy(), self.digest, pp, ps)
+
+
+def workload_capacity(point_or_cfg) -> int:
+    pt = point_or_cfg if isinstance(point_or_cfg, Point) else experiment_from_config(point_or_cfg)
+    return int(lib().sbs_workload_capacity(C.byref(pt.exp.workload)))
+
+
+def generate_workload_device(points, digest: bool = True, device: int = 0, caps=None):
+    """generate_workload for each point's (workload, seed) ON THE GPU (one
+    warp per trace, sbs_generate_workload_device); bit-identical to the host
+    generator.  Returns DeviceTrace objects."""
+    import torch
+    L = lib()
+    pts = [p if isinstance(p, Point) else experiment_from_config(p) for p in points]
+    n = len(pts)
+    dev = torch.device("cuda", device)
+    jobs = (GenJob * n)()
+    stats = torch.zeros((n, C.sizeof(GenStats) // 8), dtype=torch.int64, device=dev)
+    keep = []
+    for i, p in enumerate(pts):
+        w = p.exp.workload
+        cap = int(caps[i]) if caps is not None else int(L.sbs_workload_capacity(C.byref(w)))
+        cap = max(cap, 1)
+        a = torch.empty(cap, dtype=torch.int64, device=dev)
+        pr = torch.empty(cap, dtype=torch.int32, device=dev)
+        o = torch.empty(cap, dtype=torch.int32, device=dev)
+        pp = ps = None
+        if w.shared_prefix_fraction > 0:
+            pp = torch.empty(cap, dtype=torch.int32, device=dev)
+            ps = torch.empty(cap, dtype=torch.int32, device=dev)
+        keep.append((a, pr, o, pp, ps))
+        jobs[i] = GenJob(spec=w, seed=p.exp.seed, cap=cap, arrival_ns=a.data_ptr(),
+                         prompt_len=pr.data_ptr(), output_len=o.data_ptr(),
+                         prefix_pool_id=pp.data_ptr() if pp is not None else None,
+                         prefix_size=ps.data_ptr() if ps is not None else None,
+                         stats=stats[i].data_ptr())
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream().cuda_stream
+        _check(L.sbs_generate_workload_device(jobs, n, None, 1 if digest else 0,
+                                              C.c_void_p(stream)))
+        torch.cuda.synchronize()
+    raw = stats.cpu().numpy()
+    out = []
+    for i in range(n):
+        g = GenStats.from_buffer_copy(raw[i].tobytes())
+        st = {f: getattr(g, f) for f, _ in GenStats._fields_ if not f.startswith("_")}
+        if g.error:
+            raise (ConfigError if g.error == ERR_CONFIG else SbsError)(
+                f"device trace generation failed for point {i}: error {g.error}")
+        a, pr, o, pp, ps = keep[i]
+        out.append(DeviceTrace(a, pr, o, pp, ps, int(g.n), int(g.digest), st))
+    return out
 
 
 # ----------------------------------------------------------------- simulator

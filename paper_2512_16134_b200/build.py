@@ -18,7 +18,7 @@ PROF = os.environ.get("SBS_PROF") == "1"   # development: clock64 region counter
 LIB = LIB_DIR / ("libsbs_b200_prof.so" if PROF else "libsbs_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["des.cu", "alloc.cu"]
+CU_SOURCES = ["des.cu", "alloc.cu", "gen.cu"]
 CPP_SOURCES = ["sbs_host.cpp"]
 
 

@@ -52,6 +52,7 @@
 #include <cstdint>
 
 #include "des_types.h"
+#include "mt19937.cuh"
 #include "warp.cuh"
 
 namespace sbs {
@@ -94,53 +95,7 @@ __device__ __forceinline__ int hist_bin(int64_t v) {
   return b < kHistBins ? b : kHistBins - 1;
 }
 
-// mt19937_64 (std::mersenne_twister_engine<uint64_t,64,312,156,31,...>).
-__device__ __forceinline__ void mt_twist(uint64_t* mt) {
-  const int lane = lane_id();
-  constexpr uint64_t UM = 0xFFFFFFFF80000000ull, LM = 0x7FFFFFFFull;
-  constexpr uint64_t MA = 0xB5026F5AA96619E9ull;
-  // phase 1: i in [0,156): reads old mt[i+1], old mt[i+156]
-  for (int base = 0; base < 156; base += 32) {
-    int i = base + lane;
-    uint64_t nv = 0;
-    if (i < 156) {
-      uint64_t x = (mt[i] & UM) | (mt[i + 1] & LM);
-      uint64_t xa = (x >> 1) ^ ((x & 1) ? MA : 0);
-      nv = mt[i + 156] ^ xa;
-    }
-    __syncwarp();
-    if (i < 156) mt[i] = nv;
-    __syncwarp();
-  }
-  // phase 2: i in [156,311): reads old mt[i+1], new mt[i-156]
-  for (int base = 156; base < 311; base += 32) {
-    int i = base + lane;
-    uint64_t nv = 0;
-    if (i < 311) {
-      uint64_t x = (mt[i] & UM) | (mt[i + 1] & LM);
-      uint64_t xa = (x >> 1) ^ ((x & 1) ? MA : 0);
-      nv = mt[i - 156] ^ xa;
-    }
-    __syncwarp();
-    if (i < 311) mt[i] = nv;
-    __syncwarp();
-  }
-  if (lane == 0) {
-    uint64_t x = (mt[311] & UM) | (mt[0] & LM);
-    uint64_t xa = (x >> 1) ^ ((x & 1) ? MA : 0);
-    mt[311] = mt[155] ^ xa;
-  }
-  __syncwarp();
-}
 __device__ __noinline__ void mt_twist_ool(uint64_t* mt) { mt_twist(mt); }
-
-__device__ __forceinline__ uint64_t mt_temper(uint64_t y) {
-  y ^= (y >> 29) & 0x5555555555555555ull;
-  y ^= (y << 17) & 0x71D67FFFEDA60000ull;
-  y ^= (y << 37) & 0xFFF7EEE000000000ull;
-  y ^= y >> 43;
-  return y;
-}
 
 }  // namespace
 
@@ -441,12 +396,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   // random decode policy: mt19937_64(seed ^ 0x9E3779B97F4A7C15) (simulation.cpp:42)
   if (dec_policy == kRandom) {
     if (lane == 0) {
-      uint64_t x = pt.rng_seed;
-      pt.mt[0] = x;
-      for (int i = 1; i < 312; ++i) {
-        x = 6364136223846793005ull * (x ^ (x >> 62)) + (uint64_t)i;
-        pt.mt[i] = x;
-      }
+      mt_seed_lane0(pt.mt, pt.rng_seed);
     }
     __syncwarp();
   }

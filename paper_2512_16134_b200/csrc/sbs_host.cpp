@@ -77,6 +77,8 @@ cudaError_t launch_pbaa(const PbaaArgs& a, cudaStream_t st);
 cudaError_t launch_pbaa_one(const int64_t* rows, int n_pending, int n_new, const int64_t* caps,
                             int n_dp, int n_limit, int32_t* mapped_out, cudaStream_t st);
 cudaError_t launch_iqr(const IqrArgs& a, cudaStream_t st);
+cudaError_t launch_gen(const sbs_gen_job* d_jobs, int n_jobs, const uint64_t* d_seeds, int want_digest,
+                       cudaStream_t st);
 }  // namespace sbs
 
 namespace {
@@ -243,7 +245,7 @@ void generate(const sbs_workload& spec, uint64_t seed, HostTrace& out) {
     if (prefixes && u01(rng) < spec.shared_prefix_fraction) {
       int pid = static_cast<int>(u01(rng) * static_cast<double>(spec.prefix_pool));
       pool_id = std::min(pid, spec.prefix_pool - 1);
-      plen = std::min<int64_t>(spec.prefix_len, p);
+      plen = std::max<int64_t>(0, std::min<int64_t>(spec.prefix_len, p));  // empty vector if <= 0
       out.pool[i] = plen > 0 ? pool_id : -1;
       out.psize[i] = static_cast<int32_t>(plen);
     }
@@ -1003,6 +1005,43 @@ int sbs_generate_workload(const sbs_workload* spec, uint64_t seed, int64_t* arri
       if (prefix_pool_id) prefix_pool_id[i] = t.pool.empty() ? -1 : t.pool[i];
       if (prefix_size) prefix_size[i] = t.psize.empty() ? 0 : t.psize[i];
     }
+    return SBS_OK;
+  });
+}
+
+int64_t sbs_workload_capacity(const sbs_workload* w) {
+  const double burst = w->initial_burst > 0 ? (double)w->initial_burst : 0.0;
+  const double slots = std::ceil(w->duration_s * w->rate_qps);
+  double cap;
+  if (w->process == SBS_ARRIVAL_POISSON)
+    cap = burst + slots + 8.0 * std::sqrt(slots) + 64.0;
+  else
+    cap = burst + slots + 2.0;
+  if (!(cap < 2147483647.0)) return (int64_t)1 << 31;
+  return (int64_t)cap;
+}
+
+int sbs_generate_workload_device(const sbs_gen_job* jobs, int32_t n_jobs, const uint64_t* seeds,
+                                 int32_t want_digest, void* stream) {
+  return guarded([&] {
+    if (n_jobs <= 0) return SBS_OK;
+    for (int i = 0; i < n_jobs; ++i) {
+      check_workload(jobs[i].spec);
+      const sbs_workload& w = jobs[i].spec;
+      if (w.process < 0 || w.process > SBS_ARRIVAL_UNIFORM_JITTER)
+        return fail(SBS_ERR_CONFIG, "workload.process must be poisson, uniform, or uniform_jitter");
+      if (w.shared_prefix_fraction > 0 && (!jobs[i].prefix_pool_id || !jobs[i].prefix_size))
+        return fail(SBS_ERR_CONFIG, "shared prefixes need prefix_pool_id / prefix_size arrays");
+      if (!jobs[i].arrival_ns || !jobs[i].prompt_len || !jobs[i].output_len || !jobs[i].stats)
+        return fail(SBS_ERR_CONFIG, "sbs_gen_job: NULL output array");
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    sbs_gen_job* d_jobs = nullptr;
+    const size_t bytes = sizeof(sbs_gen_job) * (size_t)n_jobs;
+    CUDA_OR_THROW(cudaMallocAsync((void**)&d_jobs, bytes, st));
+    CUDA_OR_THROW(cudaMemcpyAsync(d_jobs, jobs, bytes, cudaMemcpyHostToDevice, st));
+    CUDA_OR_THROW(sbs::launch_gen(d_jobs, n_jobs, seeds, want_digest, st));
+    CUDA_OR_THROW(cudaFreeAsync(d_jobs, st));
     return SBS_OK;
   });
 }

