@@ -234,7 +234,32 @@ int sbs_sim_create(const sbs_experiment* points, int32_t n_points,
                    const sbs_trace* traces, int32_t n_traces,
                    const int32_t* trace_of_point, uint32_t flags,
                    int32_t device, sbs_sim** out);
-/* Re-upload host traces (same shapes) on `stream` (16 B/request).  When every
+/* Traces generated ON THE DEVICE (sbs_generate_workload_device): trace t is
+ * generate_workload(points[i].workload, points[i].seed) of the first point i
+ * with trace_of_point[i] == t (all points sharing a trace must share both;
+ * trace_of_point NULL: one trace per point).  Arenas are sized from the
+ * workload spec (sbs_workload_capacity, length bounds), so any seed fits.
+ * Slot 0 is generated before this returns.  Replaces the reference's
+ * generate_workload call inside Runner::run (simulation.cpp:141). */
+int sbs_sim_create_generated(const sbs_experiment* points, int32_t n_points,
+                             const int32_t* trace_of_point, int32_t n_traces, uint32_t flags,
+                             int32_t device, sbs_sim** out);
+/* Regenerate every trace of a generated simulator into trace slot `slot` on
+ * `stream` with new seeds (HOST array, one per trace; NULL = the current
+ * seeds): 8 B per trace host->device, the rest is device work.  The next
+ * sbs_sim_launch_slot(slot) on the same stream reads them. */
+int sbs_sim_generate_slot(sbs_sim* sim, const uint64_t* seeds, int32_t slot, int32_t want_digest,
+                          void* stream);
+/* Generation stats of a trace in a slot (synchronises the device). */
+int sbs_sim_trace_stats(sbs_sim* sim, int32_t trace, int32_t slot, sbs_gen_stats* out);
+/* Copy a trace of a slot back to the host (synchronises); *n_out = length. */
+int sbs_sim_trace_arrays(sbs_sim* sim, int32_t trace, int32_t slot, int64_t* arrival_ns,
+                         int32_t* prompt_len, int32_t* output_len, int32_t* prefix_pool_id,
+                         int32_t* prefix_size, int64_t cap, int64_t* n_out);
+/* Re-upload host traces on `stream` (16 B/request).  Each must fit what the
+ * simulator was created with — same length, outputs no longer than the
+ * create-time maximum (decode completion ring), prefix pools/sizes within the
+ * create-time ones — else SBS_ERR_CONFIG (nothing is uploaded).  When every
  * array is pinned host memory the device gathers them in one launch (a copy
  * kernel over the mapped host pages); otherwise one copy per array. */
 int sbs_sim_upload_traces(sbs_sim* sim, const sbs_trace* traces, void* stream);

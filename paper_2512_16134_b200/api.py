@@ -196,6 +196,14 @@ def lib():
         L.sbs_sim_create.argtypes = [C.POINTER(Experiment), C.c_int32, C.POINTER(Trace),
                                      C.c_int32, C.c_void_p, C.c_uint32, C.c_int32,
                                      C.POINTER(C.c_void_p)]
+        L.sbs_sim_create_generated.argtypes = [C.POINTER(Experiment), C.c_int32, C.c_void_p,
+                                               C.c_int32, C.c_uint32, C.c_int32,
+                                               C.POINTER(C.c_void_p)]
+        L.sbs_sim_generate_slot.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+                                            C.c_void_p]
+        L.sbs_sim_trace_stats.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(GenStats)]
+        L.sbs_sim_trace_arrays.argtypes = [C.c_void_p, C.c_int32, C.c_int32] + [C.c_void_p] * 5 + \
+            [C.c_int64, C.POINTER(C.c_int64)]
         L.sbs_sim_upload_traces.argtypes = [C.c_void_p, C.POINTER(Trace), C.c_void_p]
         L.sbs_sim_launch.argtypes = [C.c_void_p, C.c_void_p]
         L.sbs_sim_enable_trace_slots.argtypes = [C.c_void_p, C.c_int32]
@@ -233,6 +241,8 @@ EXPORTED_SYMBOLS = [
     "sbs_last_error", "sbs_version", "sbs_sim_profile_counters", "sbs_sim_des_ms",
     "sbs_sim_enable_trace_slots", "sbs_sim_upload_traces_slot", "sbs_sim_launch_slot",
     "sbs_prefill_allocate_one", "sbs_generate_workload_device", "sbs_workload_capacity",
+    "sbs_sim_create_generated", "sbs_sim_generate_slot", "sbs_sim_trace_stats",
+    "sbs_sim_trace_arrays",
 ]
 
 
@@ -559,24 +569,70 @@ def generate_workload_device(points, digest: bool = True, device: int = 0, caps=
 class Simulator:
     """Many replicas, one warp each, resident on one GPU (sbs_sim_*)."""
 
-    def __init__(self, points, traces, trace_of_point=None, per_request=False, logs=False,
+    def __init__(self, points, traces=None, trace_of_point=None, per_request=False, logs=False,
                  device=0):
+        """traces: HostTrace list (uploaded), or None: every trace is
+        generated ON THE DEVICE from its points' (workload, seed)
+        (sbs_sim_create_generated) and regenerated by generate()."""
         L = lib()
         self.points = list(points)
-        self.traces = list(traces)
+        self.generated = traces is None
         n = len(self.points)
         self._exp = (Experiment * n)(*[p.exp for p in self.points])
-        self._tr = (Trace * len(self.traces))(*[t.as_c() for t in self.traces])
         self._map = None
         if trace_of_point is not None:
             self._map = (C.c_int32 * n)(*trace_of_point)
+        mp = C.cast(self._map, C.c_void_p) if self._map is not None else None
+        flags = (1 if per_request else 0) | (2 if logs else 0)
         h = C.c_void_p()
-        _check(L.sbs_sim_create(self._exp, n, self._tr, len(self.traces),
-                                C.cast(self._map, C.c_void_p) if self._map is not None else None,
-                                (1 if per_request else 0) | (2 if logs else 0), device,
-                                C.byref(h)))
+        if self.generated:
+            self.traces = None
+            self.n_traces = (max(trace_of_point) + 1) if trace_of_point is not None else n
+            _check(L.sbs_sim_create_generated(self._exp, n, mp, self.n_traces, flags, device,
+                                              C.byref(h)))
+        else:
+            self.traces = list(traces)
+            self.n_traces = len(self.traces)
+            self._tr = (Trace * len(self.traces))(*[t.as_c() for t in self.traces])
+            _check(L.sbs_sim_create(self._exp, n, self._tr, len(self.traces), mp, flags, device,
+                                    C.byref(h)))
         self.handle = h
         self.n = n
+        self._slot = 0
+
+    def generate(self, seeds=None, slot=0, stream=0, digest=False):
+        """Regenerate every trace on the device into `slot` (one seed per
+        trace; None = the current seeds).  Enqueued on `stream`."""
+        arr = None
+        if seeds is not None:
+            arr = (C.c_uint64 * self.n_traces)(*[int(x) for x in seeds])
+        _check(lib().sbs_sim_generate_slot(self.handle, arr, slot, 1 if digest else 0,
+                                           C.c_void_p(stream)))
+
+    def trace_stats(self, trace, slot=0):
+        st = GenStats()
+        _check(lib().sbs_sim_trace_stats(self.handle, trace, slot, C.byref(st)))
+        return {f: getattr(st, f) for f, _ in GenStats._fields_ if not f.startswith("_")}
+
+    def trace(self, trace, slot=0) -> HostTrace:
+        """A trace as the device holds it (copied back)."""
+        L = lib()
+        n = C.c_int64(0)
+        _check(L.sbs_sim_trace_arrays(self.handle, trace, slot, None, None, None, None, None, 0,
+                                      C.byref(n)))
+        k = max(n.value, 1)
+        a, p, o = np.empty(k, np.int64), np.empty(k, np.int32), np.empty(k, np.int32)
+        pp, ps = np.empty(k, np.int32), np.empty(k, np.int32)
+        _check(L.sbs_sim_trace_arrays(self.handle, trace, slot, a.ctypes.data, p.ctypes.data,
+                                      o.ctypes.data, pp.ctypes.data, ps.ctypes.data, k,
+                                      C.byref(n)))
+        k = n.value
+        dg = self.trace_stats(trace, slot)["digest"] if self.generated else self.traces[trace].digest
+        w = self.points[0].exp.workload
+        has_pfx = self.generated and any(pt.exp.workload.shared_prefix_fraction > 0
+                                         for pt in self.points)
+        return HostTrace(a[:k], p[:k], o[:k], dg, pp[:k] if has_pfx else None,
+                         ps[:k] if has_pfx else None)
 
     def upload_traces(self, traces=None, stream=0, slot=0):
         if traces is not None:
@@ -590,6 +646,7 @@ class Simulator:
 
     def launch(self, stream=0, slot=0):
         _check(lib().sbs_sim_launch_slot(self.handle, slot, C.c_void_p(stream)))
+        self._slot = slot
 
     def results(self, stream=0, histograms=False):
         out = (Aggregates * self.n)()
@@ -601,9 +658,14 @@ class Simulator:
         return (res, hist) if histograms else res
 
     def requests(self, point: int):
-        n = self.traces[0].n if self._map is None and len(self.traces) == 1 else None
-        tr = self.traces[self._map[point] if self._map is not None else point]
-        n = tr.n
+        t = self._map[point] if self._map is not None else point
+        if self.generated:
+            m = C.c_int64(0)
+            _check(lib().sbs_sim_trace_arrays(self.handle, t, self._slot, None, None, None, None,
+                                              None, 0, C.byref(m)))
+            n = m.value
+        else:
+            n = self.traces[t].n
         cols = [np.empty(max(n, 1), np.int64) for _ in range(4)]
         st = np.empty(max(n, 1), np.int8)
         _check(lib().sbs_sim_requests(self.handle, point, *[c.ctypes.data for c in cols],

@@ -240,7 +240,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   const bool sbs = pt.policy == kSbs;
   const int policy = pt.policy, dec_policy = pt.decode_policy;
   const int64_t c_chunk = pt.c_chunk;
-  const int64_t N = pt.N;
+  const int64_t N = pt.n_dev ? *pt.n_dev : pt.N;
   const int64_t horizon = pt.horizon, warmup = pt.warmup;
   const int F = pt.F, Fm = pt.F - 1, R = pt.R, BC = pt.BC;
   const int n_limit = pt.n_limit, cap_batch = pt.cap_batch, n_drops = pt.n_drops;
@@ -1995,7 +1995,7 @@ __device__ void combine_pair(const DevPoint& pt, DevResult& res, const Counters*
   const int lane = lane_id();
   // decode-warp TTFTs were written from the top of the buffer: move them
   // down behind the prefill warp's (the finalize select reads [0, n))
-  const int64_t na = a->n_ttft, nb = b->n_ttft, N = pt.N;
+  const int64_t na = a->n_ttft, nb = b->n_ttft, N = pt.n_dev ? *pt.n_dev : pt.N;
   for (int64_t base = 0; base < nb; base += 32) {
     const int64_t i = base + lane;
     const int64_t v = i < nb ? pt.ttft[N - nb + i] : 0;

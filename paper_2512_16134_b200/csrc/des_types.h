@@ -75,7 +75,8 @@ struct DevPoint {
   int64_t c_chunk, t_default, l_net, tps, horizon, warmup;
   double iqr_k, wd_mult, pf_base, pf_tok, dc_base, dc_req, dc_kv;
   uint64_t rng_seed;
-  int64_t N;
+  int64_t N;             // trace length, or its capacity when n_dev is set
+  const int64_t* n_dev;  // device-generated trace: its length (sbs_gen_stats::n), else NULL
   // ---- trace (SoA)
   const int64_t* arr;
   const int32_t* prompt;

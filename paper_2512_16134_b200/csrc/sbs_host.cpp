@@ -343,11 +343,19 @@ struct TraceDev {
   int32_t* output1 = nullptr;
   int32_t* pool1 = nullptr;
   int32_t* psize1 = nullptr;
-  int64_t n = 0;
+  int64_t n = 0;              // length (host traces) or capacity (generated traces)
   int32_t max_output = 0;
   int32_t n_pools = 0;       // 1 + max pool id
   int64_t max_psize = 0;
   uint64_t digest = 0;
+  // device-generated traces (sbs_sim_create_generated): the (workload, seed)
+  // they come from, per-slot generation stats on the device (n first: the
+  // DES kernels read the length from there) and their host copies
+  bool gen = false;
+  sbs_workload spec{};
+  uint64_t seed = 0;
+  sbs_gen_stats* d_stats = nullptr;  // [2]
+  sbs_gen_stats h_stats[2] = {};
 };
 
 struct PointHost {
@@ -400,6 +408,12 @@ struct sbs_sim {
   sbs::CopySeg* d_segs = nullptr;
   int seg_cap = 0;
   cudaEvent_t ev_segs = nullptr;  // the previous gather has consumed h_segs
+  bool generated = false;          // traces are generated on the device
+  sbs_gen_job* d_jobs[2] = {};     // per slot, one job per trace
+  uint64_t* d_seeds[2] = {};
+  uint64_t* h_seeds[2] = {};       // pinned staging for the next seeds
+  cudaEvent_t ev_seeds[2] = {};    // the staged seeds of a slot were consumed
+  int gen_slot_valid[2] = {};      // h_stats of the slot are current
   int n_slots = 1;                 // trace buffer sets
   int cur_slot = 0;                // the set the last launch read
   sbs::DevPoint* d_pts1 = nullptr; // point descriptors pointing at set 1
@@ -445,6 +459,34 @@ void layout_smem(sbs::DevPoint& d) {
   d.sm_bytes = (int32_t)off;
 }
 
+// Upper bounds of sample_length (workload.cpp:52-65) over a LengthSpec.
+int64_t length_bound(const sbs_length_spec& l, bool output) {
+  switch (l.dist) {
+    case SBS_LEN_CONSTANT:
+      return output ? std::max<int64_t>(0, l.value) : std::max<int64_t>(1, l.value);
+    case SBS_LEN_UNIFORM:
+      return std::max(std::max<int64_t>(1, l.min), l.max);
+    default:
+      return l.max;  // clamp(t, lo, max) = min(max(t, lo), max)
+  }
+}
+
+// Shape bounds of every trace generate_workload can produce for `w`: what the
+// arenas of a generated trace are sized by (a host trace uses its own maxima).
+void bound_trace_shape(TraceDev& t, const sbs_workload& w) {
+  t.max_output = (int32_t)std::min<int64_t>(std::max<int64_t>(0, length_bound(w.output, true)), 0x3fffffff);
+  if (w.shared_prefix_fraction > 0) {
+    t.n_pools = w.prefix_pool;
+    t.max_psize = std::max<int64_t>(0, std::min<int64_t>(w.prefix_len, length_bound(w.prompt, false)));
+  }
+}
+
+// Requests in the trace the point's last launch read.
+int64_t live_n(const sbs_sim& s, const PointHost& p) {
+  const TraceDev& t = s.traces[p.trace];
+  return t.gen ? t.h_stats[s.cur_slot].n : t.n;
+}
+
 void build_point(sbs_sim& s, PointHost& p) {
   const sbs_experiment& x = p.x;
   const sbs_cluster& c = x.cluster;
@@ -488,6 +530,7 @@ void build_point(sbs_sim& s, PointHost& p) {
   d.dc_kv = c.decode_per_kv_token_s;
   d.rng_seed = x.seed ^ 0x9E3779B97F4A7C15ULL;
   d.N = t.n;
+  d.n_dev = t.gen ? &t.d_stats[0].n : nullptr;
   d.arr = t.arr;
   d.prompt = t.prompt;
   d.output = t.output;
@@ -635,7 +678,8 @@ void build_point(sbs_sim& s, PointHost& p) {
   d.log = logs ? (int64_t*)(b + o_log) : nullptr;
   d.log_cap = logs ? p.LOG : 0;
   layout_smem(d);
-  p.cost = (double)t.n * (1.0 + (double)d.U / 64.0) * (1.0 + (double)(d.P * d.D) / 256.0);
+  const double n_exp = t.gen ? t.spec.rate_qps * t.spec.duration_s + t.spec.initial_burst : (double)t.n;
+  p.cost = n_exp * (1.0 + (double)d.U / 64.0) * (1.0 + (double)(d.P * d.D) / 256.0);
 }
 
 // Per-run reset of the parts of the arena the kernel reads before writing.
@@ -777,6 +821,7 @@ void upload_points(sbs_sim& s) {
       h[i].arr = t.arr1;
       h[i].prompt = t.prompt1;
       h[i].output = t.output1;
+      if (t.gen) h[i].n_dev = &t.d_stats[1].n;
       if (h[i].cache_on) {
         h[i].pfx_pool = t.pool1;
         h[i].pfx_size = t.psize1;
@@ -853,11 +898,55 @@ bool upload_traces_gather(sbs_sim& s, const sbs_trace* traces, int slot, cudaStr
   return true;
 }
 
-void do_upload_traces(sbs_sim& s, const sbs_trace* traces, cudaStream_t st, int slot = 0) {
-  for (size_t i = 0; i < s.traces.size(); ++i) {
-    if (traces[i].n != s.traces[i].n) throw Error{SBS_ERR_CONFIG, "trace shape changed"};
-    if ((traces[i].prefix_pool_id != nullptr) != (s.traces[i].pool != nullptr))
-      throw Error{SBS_ERR_CONFIG, "trace shape changed"};
+int parallel_threads();
+
+// A re-uploaded trace must fit what the points' arenas were sized for at
+// create time: its length, the completion ring (max output), the prefix-cache
+// key space (pool ids, prefix sizes).  Anything else is refused, never wrapped.
+void check_reupload(const TraceDev& t, const sbs_trace& tr) {
+  if (tr.n != t.n) throw Error{SBS_ERR_CONFIG, "trace shape changed (length)"};
+  if ((tr.prefix_pool_id != nullptr) != (t.pool != nullptr))
+    throw Error{SBS_ERR_CONFIG, "trace shape changed (shared prefixes)"};
+  int32_t mo = 0;
+  for (int64_t k = 0; k < tr.n; ++k) mo = std::max(mo, tr.output_len[k]);
+  if (mo > t.max_output)
+    throw Error{SBS_ERR_CONFIG, "re-uploaded trace has longer outputs than the one the simulator was "
+                                "created with (decode completion ring); create a new simulator"};
+  if (tr.prefix_pool_id != nullptr) {
+    for (int64_t k = 0; k < tr.n; ++k) {
+      const int32_t pid = tr.prefix_pool_id[k], ps = tr.prefix_size[k];
+      if (ps < 0 || (ps > 0 && pid < 0) || ps > tr.prompt_len[k])
+        throw Error{SBS_ERR_CONFIG, "trace prefix sizes out of range"};
+      if (ps > 0 && (pid >= t.n_pools || ps > t.max_psize))
+        throw Error{SBS_ERR_CONFIG, "re-uploaded trace uses prefix pools / sizes beyond the "
+                                    "create-time trace (prefix-cache key space)"};
+    }
+  }
+}
+
+void do_upload_traces(sbs_sim& s, const sbs_trace* traces, cudaStream_t st, int slot = 0,
+                      bool check = true) {
+  if (s.generated) throw Error{SBS_ERR_CONFIG, "traces of this simulator are generated on the device"};
+  if (check) {  // one O(n) scan per trace, traces spread over the host threads
+    const size_t nt = s.traces.size();
+    const int nth = (int)std::min<size_t>(nt, (size_t)parallel_threads());
+    std::vector<std::string> errs(nt);
+    std::atomic<size_t> next{0};
+    auto work = [&] {
+      for (size_t i; (i = next.fetch_add(1)) < nt;) {
+        try {
+          check_reupload(s.traces[i], traces[i]);
+        } catch (const Error& e) {
+          errs[i] = e.msg;
+        }
+      }
+    };
+    std::vector<std::thread> th;
+    for (int k = 1; k < nth; ++k) th.emplace_back(work);
+    work();
+    for (auto& t : th) t.join();
+    for (auto& e : errs)
+      if (!e.empty()) throw Error{SBS_ERR_CONFIG, e};
   }
   if (slot < 0 || slot >= s.n_slots) throw Error{SBS_ERR_CONFIG, "trace slot out of range"};
   if (s.traces.size() > 1 && upload_traces_gather(s, traces, slot, st)) return;
@@ -879,13 +968,13 @@ void do_upload_traces(sbs_sim& s, const sbs_trace* traces, cudaStream_t st, int 
   }
 }
 
-void finish_aggregates(const PointHost& p, const sbs::DevResult& r, sbs_aggregates& a) {
+void finish_aggregates(const PointHost& p, const sbs::DevResult& r, sbs_aggregates& a, int64_t N) {
   std::memset(&a, 0, sizeof(a));
   const sbs::DevPoint& d = p.dp;
-  a.generated = (uint64_t)d.N;
+  a.generated = (uint64_t)N;
   a.completed = (uint64_t)r.completed;
   a.throttled = (uint64_t)r.throttled;
-  a.in_flight = (uint64_t)(d.N - r.completed - r.throttled);
+  a.in_flight = (uint64_t)(N - r.completed - r.throttled);
   a.window_requests = (uint64_t)r.wr;
   a.warmup_cutoff_s = (double)d.warmup / 1e9;
   a.duration_s = (double)d.horizon / 1e9;
@@ -1046,26 +1135,118 @@ int sbs_generate_workload_device(const sbs_gen_job* jobs, int32_t n_jobs, const 
   });
 }
 
+}  // extern "C"
+
+namespace {
+
+void open_device(sbs_sim* s, const sbs_experiment* points, int32_t n_points, uint32_t flags,
+                 int32_t device) {
+  if (n_points < 1) throw Error{SBS_ERR_CONFIG, "no points"};
+  for (int i = 0; i < n_points; ++i) {
+    validate(points[i]);
+    check_workload(points[i].workload);
+  }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    throw Error{SBS_ERR_CUDA, "no CUDA device visible (the GPU path has no CPU fallback)"};
+  if (device < 0 || device >= ndev) throw Error{SBS_ERR_CONFIG, "device index out of range"};
+  s->device = device;
+  s->flags = flags;
+  CUDA_OR_THROW(cudaSetDevice(device));
+  CUDA_OR_THROW(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, device));
+  if (const char* e = std::getenv("SBS_SPLIT")) s->pair_mode = std::atoi(e) == 1 ? 1 : 2;
+}
+
+void alloc_trace(sbs_sim* s, TraceDev& t, bool prefixes) {
+  const size_t n = (size_t)std::max<int64_t>(t.n, 1);
+  CUDA_OR_THROW(cudaMalloc(&t.arr, 8 * n));
+  CUDA_OR_THROW(cudaMalloc(&t.prompt, 4 * n));
+  CUDA_OR_THROW(cudaMalloc(&t.output, 4 * n));
+  s->device_bytes += (int64_t)(16 * n);
+  if (prefixes) {
+    CUDA_OR_THROW(cudaMalloc(&t.pool, 4 * n));
+    CUDA_OR_THROW(cudaMalloc(&t.psize, 4 * n));
+    s->device_bytes += (int64_t)(8 * n);
+  }
+}
+
+void init_points(sbs_sim* s, const sbs_experiment* points, int32_t n_points,
+                 const int32_t* trace_of_point, int32_t n_traces) {
+  s->pts.resize(n_points);
+  for (int i = 0; i < n_points; ++i) {
+    PointHost& p = s->pts[i];
+    p.x = points[i];
+    p.drops.assign(points[i].drops, points[i].drops + points[i].n_drops);
+    p.deads.assign(points[i].deads, points[i].deads + points[i].n_deads);
+    p.topo.assign(points[i].topology, points[i].topology + points[i].n_topology);
+    if (p.x.cluster.cache_enabled)
+      p.probes.assign(points[i].cluster.cache_probe_lens,
+                      points[i].cluster.cache_probe_lens + points[i].cluster.cache_n_probes);
+    p.x.cluster.cache_probe_lens = p.probes.empty() ? nullptr : p.probes.data();
+    p.trace = trace_of_point ? trace_of_point[i] : i;
+    if (p.trace < 0 || p.trace >= n_traces) throw Error{SBS_ERR_CONFIG, "trace index out of range"};
+    initial_caps(p, s->traces[p.trace]);
+    build_point(*s, p);
+    s->device_bytes += (int64_t)p.arena_bytes;
+  }
+  order_points(*s);
+  CUDA_OR_THROW(cudaMalloc(&s->d_pts, sizeof(sbs::DevPoint) * n_points));
+  CUDA_OR_THROW(cudaMalloc(&s->d_res, sizeof(sbs::DevResult) * n_points));
+  CUDA_OR_THROW(cudaMalloc(&s->d_counter, sbs_sim::kVariants * sizeof(int)));
+  s->h_res.resize(n_points);
+  upload_points(*s);
+}
+
+// The generation jobs of one trace slot (device array, seeds from d_seeds).
+void upload_gen_jobs(sbs_sim* s, int slot) {
+  std::vector<sbs_gen_job> jobs(s->traces.size());
+  for (size_t i = 0; i < s->traces.size(); ++i) {
+    TraceDev& t = s->traces[i];
+    sbs_gen_job& j = jobs[i];
+    std::memset(&j, 0, sizeof(j));
+    j.spec = t.spec;
+    j.seed = t.seed;
+    j.cap = t.n;
+    j.arrival_ns = slot ? t.arr1 : t.arr;
+    j.prompt_len = slot ? t.prompt1 : t.prompt;
+    j.output_len = slot ? t.output1 : t.output;
+    j.prefix_pool_id = slot ? t.pool1 : t.pool;
+    j.prefix_size = slot ? t.psize1 : t.psize;
+    j.stats = &t.d_stats[slot];
+  }
+  if (s->d_jobs[slot] == nullptr) {
+    CUDA_OR_THROW(cudaMalloc(&s->d_jobs[slot], sizeof(sbs_gen_job) * jobs.size()));
+    CUDA_OR_THROW(cudaMalloc(&s->d_seeds[slot], sizeof(uint64_t) * jobs.size()));
+    CUDA_OR_THROW(cudaMallocHost(&s->h_seeds[slot], sizeof(uint64_t) * jobs.size()));
+    CUDA_OR_THROW(cudaEventCreateWithFlags(&s->ev_seeds[slot], cudaEventDisableTiming));
+    CUDA_OR_THROW(cudaEventRecord(s->ev_seeds[slot], 0));
+  }
+  CUDA_OR_THROW(cudaMemcpy(s->d_jobs[slot], jobs.data(), sizeof(sbs_gen_job) * jobs.size(),
+                           cudaMemcpyHostToDevice));
+}
+
+void generate_slot(sbs_sim* s, const uint64_t* seeds, int slot, int want_digest, cudaStream_t st) {
+  const size_t n = s->traces.size();
+  CUDA_OR_THROW(cudaEventSynchronize(s->ev_seeds[slot]));  // staging buffer free again
+  for (size_t i = 0; i < n; ++i) s->h_seeds[slot][i] = seeds ? seeds[i] : s->traces[i].seed;
+  CUDA_OR_THROW(cudaMemcpyAsync(s->d_seeds[slot], s->h_seeds[slot], sizeof(uint64_t) * n,
+                                cudaMemcpyHostToDevice, st));
+  CUDA_OR_THROW(cudaEventRecord(s->ev_seeds[slot], st));
+  CUDA_OR_THROW(sbs::launch_gen(s->d_jobs[slot], (int)n, s->d_seeds[slot], want_digest, st));
+  s->gen_slot_valid[slot] = 0;
+}
+
+}  // namespace
+
+extern "C" {
+
 int sbs_sim_create(const sbs_experiment* points, int32_t n_points, const sbs_trace* traces,
                    int32_t n_traces, const int32_t* trace_of_point, uint32_t flags,
                    int32_t device, sbs_sim** out) {
   *out = nullptr;
   sbs_sim* s = new sbs_sim();
   int rc = guarded([&] {
-    if (n_points < 1) throw Error{SBS_ERR_CONFIG, "no points"};
-    for (int i = 0; i < n_points; ++i) {
-      validate(points[i]);
-      check_workload(points[i].workload);
-    }
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
-      throw Error{SBS_ERR_CUDA, "no CUDA device visible (the GPU path has no CPU fallback)"};
-    s->device = device;
-    s->flags = flags;
-    CUDA_OR_THROW(cudaSetDevice(device));
-    CUDA_OR_THROW(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, device));
-    if (const char* e = std::getenv("SBS_SPLIT")) s->pair_mode = std::atoi(e) == 1 ? 1 : 2;
-    // traces
+    open_device(s, points, n_points, flags, device);
     s->traces.resize(n_traces);
     for (int i = 0; i < n_traces; ++i) {
       TraceDev& t = s->traces[i];
@@ -1073,12 +1254,8 @@ int sbs_sim_create(const sbs_experiment* points, int32_t n_points, const sbs_tra
       t.digest = traces[i].digest;
       if (t.n >= (int64_t)1 << 31) throw Error{SBS_ERR_CONFIG, "trace longer than 2^31 requests"};
       for (int64_t k = 0; k < t.n; ++k) t.max_output = std::max(t.max_output, traces[i].output_len[k]);
-      size_t n = (size_t)std::max<int64_t>(t.n, 1);
-      CUDA_OR_THROW(cudaMalloc(&t.arr, 8 * n));
-      CUDA_OR_THROW(cudaMalloc(&t.prompt, 4 * n));
-      CUDA_OR_THROW(cudaMalloc(&t.output, 4 * n));
-      s->device_bytes += (int64_t)(16 * n);
-      if (traces[i].prefix_pool_id != nullptr && traces[i].prefix_size != nullptr) {
+      const bool prefixes = traces[i].prefix_pool_id != nullptr && traces[i].prefix_size != nullptr;
+      if (prefixes) {
         for (int64_t k = 0; k < t.n; ++k) {
           const int32_t pid = traces[i].prefix_pool_id[k], ps = traces[i].prefix_size[k];
           if (ps < 0 || (ps > 0 && pid < 0) || ps > traces[i].prompt_len[k])
@@ -1088,39 +1265,12 @@ int sbs_sim_create(const sbs_experiment* points, int32_t n_points, const sbs_tra
             t.max_psize = std::max<int64_t>(t.max_psize, ps);
           }
         }
-        CUDA_OR_THROW(cudaMalloc(&t.pool, 4 * n));
-        CUDA_OR_THROW(cudaMalloc(&t.psize, 4 * n));
-        s->device_bytes += (int64_t)(8 * n);
       }
+      alloc_trace(s, t, prefixes);
     }
-    do_upload_traces(*s, traces, 0);
+    do_upload_traces(*s, traces, 0, 0, false);
     CUDA_OR_THROW(cudaDeviceSynchronize());
-    // points
-    s->pts.resize(n_points);
-    for (int i = 0; i < n_points; ++i) {
-      PointHost& p = s->pts[i];
-      p.x = points[i];
-      validate(p.x);
-      check_workload(p.x.workload);
-      p.drops.assign(points[i].drops, points[i].drops + points[i].n_drops);
-      p.deads.assign(points[i].deads, points[i].deads + points[i].n_deads);
-      p.topo.assign(points[i].topology, points[i].topology + points[i].n_topology);
-      if (p.x.cluster.cache_enabled)
-        p.probes.assign(points[i].cluster.cache_probe_lens,
-                        points[i].cluster.cache_probe_lens + points[i].cluster.cache_n_probes);
-      p.x.cluster.cache_probe_lens = p.probes.empty() ? nullptr : p.probes.data();
-      p.trace = trace_of_point ? trace_of_point[i] : i;
-      if (p.trace < 0 || p.trace >= n_traces) throw Error{SBS_ERR_CONFIG, "trace index out of range"};
-      initial_caps(p, s->traces[p.trace]);
-      build_point(*s, p);
-      s->device_bytes += (int64_t)p.arena_bytes;
-    }
-    order_points(*s);
-    CUDA_OR_THROW(cudaMalloc(&s->d_pts, sizeof(sbs::DevPoint) * n_points));
-    CUDA_OR_THROW(cudaMalloc(&s->d_res, sizeof(sbs::DevResult) * n_points));
-    CUDA_OR_THROW(cudaMalloc(&s->d_counter, sbs_sim::kVariants * sizeof(int)));
-    s->h_res.resize(n_points);
-    upload_points(*s);
+    init_points(s, points, n_points, trace_of_point, n_traces);
     return SBS_OK;
   });
   if (rc != SBS_OK) {
@@ -1129,6 +1279,108 @@ int sbs_sim_create(const sbs_experiment* points, int32_t n_points, const sbs_tra
   }
   *out = s;
   return SBS_OK;
+}
+
+int sbs_sim_create_generated(const sbs_experiment* points, int32_t n_points,
+                             const int32_t* trace_of_point, int32_t n_traces, uint32_t flags,
+                             int32_t device, sbs_sim** out) {
+  *out = nullptr;
+  sbs_sim* s = new sbs_sim();
+  int rc = guarded([&] {
+    open_device(s, points, n_points, flags, device);
+    if (trace_of_point == nullptr) n_traces = n_points;
+    if (n_traces < 1) throw Error{SBS_ERR_CONFIG, "no traces"};
+    s->generated = true;
+    s->traces.resize(n_traces);
+    std::vector<int> first(n_traces, -1);
+    for (int i = 0; i < n_points; ++i) {
+      const int t = trace_of_point ? trace_of_point[i] : i;
+      if (t < 0 || t >= n_traces) throw Error{SBS_ERR_CONFIG, "trace index out of range"};
+      if (first[t] < 0) first[t] = i;
+      else if (std::memcmp(&points[i].workload, &points[first[t]].workload, sizeof(sbs_workload)) != 0 ||
+               points[i].seed != points[first[t]].seed)
+        throw Error{SBS_ERR_CONFIG, "points sharing a trace must share workload and seed"};
+    }
+    for (int i = 0; i < n_traces; ++i) {
+      if (first[i] < 0) throw Error{SBS_ERR_CONFIG, "a trace no point uses"};
+      TraceDev& t = s->traces[i];
+      t.gen = true;
+      t.spec = points[first[i]].workload;
+      t.seed = points[first[i]].seed;
+      t.n = sbs_workload_capacity(&t.spec);
+      if (t.n >= (int64_t)1 << 31) throw Error{SBS_ERR_CONFIG, "trace longer than 2^31 requests"};
+      bound_trace_shape(t, t.spec);
+      alloc_trace(s, t, t.spec.shared_prefix_fraction > 0);
+      CUDA_OR_THROW(cudaMalloc(&t.d_stats, 2 * sizeof(sbs_gen_stats)));
+      CUDA_OR_THROW(cudaMemset(t.d_stats, 0, 2 * sizeof(sbs_gen_stats)));
+    }
+    upload_gen_jobs(s, 0);
+    init_points(s, points, n_points, trace_of_point, n_traces);
+    generate_slot(s, nullptr, 0, 0, 0);
+    CUDA_OR_THROW(cudaDeviceSynchronize());
+    return SBS_OK;
+  });
+  if (rc != SBS_OK) {
+    sbs_sim_destroy(s);
+    return rc;
+  }
+  *out = s;
+  return SBS_OK;
+}
+
+int sbs_sim_generate_slot(sbs_sim* s, const uint64_t* seeds, int32_t slot, int32_t want_digest,
+                          void* stream) {
+  return guarded([&] {
+    if (!s->generated) throw Error{SBS_ERR_CONFIG, "simulator traces are host-uploaded"};
+    if (slot < 0 || slot >= s->n_slots) throw Error{SBS_ERR_CONFIG, "trace slot out of range"};
+    CUDA_OR_THROW(cudaSetDevice(s->device));
+    if (seeds)
+      for (size_t i = 0; i < s->traces.size(); ++i) s->traces[i].seed = seeds[i];
+    generate_slot(s, seeds, slot, want_digest, (cudaStream_t)stream);
+    return SBS_OK;
+  });
+}
+
+int sbs_sim_trace_stats(sbs_sim* s, int32_t trace, int32_t slot, sbs_gen_stats* out) {
+  return guarded([&] {
+    if (trace < 0 || trace >= (int)s->traces.size()) throw Error{SBS_ERR_CONFIG, "trace out of range"};
+    if (slot < 0 || slot >= s->n_slots) throw Error{SBS_ERR_CONFIG, "trace slot out of range"};
+    TraceDev& t = s->traces[trace];
+    if (!t.gen) throw Error{SBS_ERR_CONFIG, "trace was uploaded from the host"};
+    CUDA_OR_THROW(cudaSetDevice(s->device));
+    CUDA_OR_THROW(cudaDeviceSynchronize());
+    CUDA_OR_THROW(cudaMemcpy(out, &t.d_stats[slot], sizeof(sbs_gen_stats), cudaMemcpyDeviceToHost));
+    return SBS_OK;
+  });
+}
+
+int sbs_sim_trace_arrays(sbs_sim* s, int32_t trace, int32_t slot, int64_t* arrival_ns,
+                         int32_t* prompt_len, int32_t* output_len, int32_t* prefix_pool_id,
+                         int32_t* prefix_size, int64_t cap, int64_t* n_out) {
+  return guarded([&] {
+    if (trace < 0 || trace >= (int)s->traces.size()) throw Error{SBS_ERR_CONFIG, "trace out of range"};
+    if (slot < 0 || slot >= s->n_slots) throw Error{SBS_ERR_CONFIG, "trace slot out of range"};
+    CUDA_OR_THROW(cudaSetDevice(s->device));
+    CUDA_OR_THROW(cudaDeviceSynchronize());
+    TraceDev& t = s->traces[trace];
+    int64_t n = t.n;
+    if (t.gen) {
+      sbs_gen_stats st{};
+      CUDA_OR_THROW(cudaMemcpy(&st, &t.d_stats[slot], sizeof(st), cudaMemcpyDeviceToHost));
+      n = st.n;
+    }
+    if (n_out) *n_out = n;
+    if (arrival_ns == nullptr || n == 0) return SBS_OK;
+    if (n > cap) return fail(SBS_ERR_OVERFLOW, "trace buffer too small");
+    CUDA_OR_THROW(cudaMemcpy(arrival_ns, slot ? t.arr1 : t.arr, 8 * n, cudaMemcpyDeviceToHost));
+    CUDA_OR_THROW(cudaMemcpy(prompt_len, slot ? t.prompt1 : t.prompt, 4 * n, cudaMemcpyDeviceToHost));
+    CUDA_OR_THROW(cudaMemcpy(output_len, slot ? t.output1 : t.output, 4 * n, cudaMemcpyDeviceToHost));
+    if (prefix_pool_id && t.pool)
+      CUDA_OR_THROW(cudaMemcpy(prefix_pool_id, slot ? t.pool1 : t.pool, 4 * n, cudaMemcpyDeviceToHost));
+    if (prefix_size && t.psize)
+      CUDA_OR_THROW(cudaMemcpy(prefix_size, slot ? t.psize1 : t.psize, 4 * n, cudaMemcpyDeviceToHost));
+    return SBS_OK;
+  });
 }
 
 int sbs_sim_upload_traces(sbs_sim* s, const sbs_trace* traces, void* stream) {
@@ -1181,6 +1433,7 @@ int sbs_sim_enable_trace_slots(sbs_sim* s, int32_t n) {
       CUDA_OR_THROW(cudaMalloc(&s->d_pts1, sizeof(sbs::DevPoint) * s->pts.size()));
       s->n_slots = 2;
       upload_points(*s);
+      if (s->generated) upload_gen_jobs(s, 1);
     }
     return SBS_OK;
   });
@@ -1216,6 +1469,12 @@ int sbs_sim_results(sbs_sim* s, sbs_aggregates* out, sbs_histograms* hist, void*
       CUDA_OR_THROW(cudaMemcpyAsync(s->h_res.data(), s->d_res, sizeof(sbs::DevResult) * n,
                                     cudaMemcpyDeviceToHost, st));
       CUDA_OR_THROW(cudaStreamSynchronize(st));
+      if (s->generated && !s->gen_slot_valid[s->cur_slot]) {
+        for (auto& t : s->traces)
+          CUDA_OR_THROW(cudaMemcpy(&t.h_stats[s->cur_slot], &t.d_stats[s->cur_slot],
+                                   sizeof(sbs_gen_stats), cudaMemcpyDeviceToHost));
+        s->gen_slot_valid[s->cur_slot] = 1;
+      }
       bool overflow = false;
       for (int i = 0; i < n; ++i) {
         const int err = s->h_res[i].error;
@@ -1249,7 +1508,13 @@ int sbs_sim_results(sbs_sim* s, sbs_aggregates* out, sbs_histograms* hist, void*
     std::vector<int64_t> th(sbs::kHistBins);
     for (int i = 0; i < n; ++i) {
       const PointHost& p = s->pts[s->order[i]];
-      finish_aggregates(p, s->h_res[i], out[s->order[i]]);
+      const TraceDev& t = s->traces[p.trace];
+      if (t.gen && t.h_stats[s->cur_slot].error != 0) {
+        rc = t.h_stats[s->cur_slot].error;
+        g_err = "device trace generation failed for trace " + std::to_string(p.trace) + " (code " +
+                std::to_string(rc) + ")";
+      }
+      finish_aggregates(p, s->h_res[i], out[s->order[i]], live_n(*s, p));
       if (s->h_res[i].error != 0) {
         rc = s->h_res[i].error;
         g_err = "replica " + std::to_string(s->order[i]) + " failed with code " + std::to_string(rc);
@@ -1274,7 +1539,7 @@ int sbs_sim_requests(sbs_sim* s, int32_t point, int64_t* dispatch_ns, int64_t* p
     if (point < 0 || point >= (int)s->pts.size()) throw Error{SBS_ERR_CONFIG, "point out of range"};
     CUDA_OR_THROW(cudaSetDevice(s->device));
     const sbs::DevPoint& d = s->pts[point].dp;
-    size_t n = (size_t)d.N;
+    size_t n = (size_t)live_n(*s, s->pts[point]);
     if (n == 0) return SBS_OK;
     if (dispatch_ns) CUDA_OR_THROW(cudaMemcpy(dispatch_ns, d.o_dispatch, 8 * n, cudaMemcpyDeviceToHost));
     if (prefill_start_ns) CUDA_OR_THROW(cudaMemcpy(prefill_start_ns, d.o_pstart, 8 * n, cudaMemcpyDeviceToHost));
@@ -1322,6 +1587,13 @@ void sbs_sim_destroy(sbs_sim* s) {
     if (t.psize) cudaFree(t.psize);
     for (void* q : {(void*)t.arr1, (void*)t.prompt1, (void*)t.output1, (void*)t.pool1, (void*)t.psize1})
       if (q) cudaFree(q);
+    if (t.d_stats) cudaFree(t.d_stats);
+  }
+  for (int k = 0; k < 2; ++k) {
+    if (s->d_jobs[k]) cudaFree(s->d_jobs[k]);
+    if (s->d_seeds[k]) cudaFree(s->d_seeds[k]);
+    if (s->h_seeds[k]) cudaFreeHost(s->h_seeds[k]);
+    if (s->ev_seeds[k]) cudaEventDestroy(s->ev_seeds[k]);
   }
   if (s->d_pts) cudaFree(s->d_pts);
   if (s->d_pts1) cudaFree(s->d_pts1);

@@ -100,3 +100,96 @@ def test_capacity_overflow_is_reported():
     c = copy.deepcopy(CASES["short_3k"])
     with pytest.raises(P.SbsError):
         api.generate_workload_device([c], caps=[10])
+
+
+# ---------------------------------------------------------------- simulator on device traces
+def _run_host(cfgs):
+    pts = [P.experiment_from_config(c) for c in cfgs]
+    sim = P.Simulator(pts, [P.generate_workload(p) for p in pts], per_request=True)
+    try:
+        sim.launch()
+        return sim.results(), [sim.requests(i) for i in range(len(cfgs))]
+    finally:
+        sim.close()
+
+
+def _same_results(a, b, ra, rb, name):
+    for k in P.REFERENCE_AGG_KEYS + ["alloc_calls", "decode_selects", "tpot_count", "tpot_mean_s"]:
+        assert a[k] == b[k], f"{name}: {k} {a[k]} vs {b[k]}"
+    for col in ("dispatch", "prefill_start", "first_token", "completion", "status"):
+        assert np.array_equal(ra[col], rb[col]), f"{name}: {col}"
+
+
+def test_generated_simulator_matches_golden():
+    """Simulator whose traces never leave the device: every golden case per
+    request against the reference's columns."""
+    names = sorted(CASES)
+    pts = [P.experiment_from_config(CASES[n]) for n in names]
+    sim = P.Simulator(pts, None, per_request=True)
+    try:
+        sim.generate(digest=True)
+        sim.launch()
+        aggs = sim.results()
+        for i, name in enumerate(names):
+            want = load_case(name)
+            assert sim.trace_stats(i)["digest"] == int(want["digest"]), name
+            r = sim.requests(i)
+            for col in ("dispatch", "prefill_start", "first_token", "completion"):
+                assert np.array_equal(r[col], want[col]), f"{name}: {col}"
+            assert aggs[i]["generated"] == len(want["arrival"])
+    finally:
+        sim.close()
+
+
+def test_generated_slots_new_seeds_match_fresh_host_runs():
+    """Regenerate into the second slot with new seeds (the bench's step loop)
+    and compare with host-generated simulators of those seeds."""
+    base = ["cfg2_20s", "decode_dp32", "short_3k", "cache_pd", "faults_decode_capped_tps3"]
+    cfgs = [copy.deepcopy(CASES[n]) for n in base]
+    pts = [P.experiment_from_config(c) for c in cfgs]
+    sim = P.Simulator(pts, None, per_request=True)
+    try:
+        sim.enable_trace_slots(2)
+        for step, slot in ((1, 1), (2, 0), (3, 1)):
+            seeds = [1000 * step + i for i in range(len(cfgs))]
+            sim.generate(seeds, slot=slot)
+            sim.launch(slot=slot)
+            aggs = sim.results()
+            got = [sim.requests(i) for i in range(len(cfgs))]
+            for c, s_ in zip(cfgs, seeds):
+                c["sim"]["seed"] = s_
+            want_aggs, want_req = _run_host(cfgs)
+            for i in range(len(cfgs)):
+                _same_results(aggs[i], want_aggs[i], got[i], want_req[i], f"{base[i]} step {step}")
+    finally:
+        sim.close()
+
+
+def test_reupload_checks_shape_bounds():
+    """a re-uploaded trace whose outputs exceed the
+    create-time completion ring is refused; one that fits gives the same
+    results as a fresh simulator."""
+    c = copy.deepcopy(CASES["decode_dp32"])
+    pt = P.experiment_from_config(c)
+    tr = P.generate_workload(pt)
+    sim = P.Simulator([pt], [tr], per_request=True)
+    try:
+        longer = copy.deepcopy(tr)
+        longer.output_len = tr.output_len.copy()
+        longer.output_len[0] = int(tr.output_len.max()) * 4 + 64
+        with pytest.raises(P.ConfigError):
+            sim.upload_traces([longer])
+        shorter = copy.deepcopy(tr)
+        shorter.output_len = np.maximum(tr.output_len // 2, 1).astype(np.int32)
+        sim.upload_traces([shorter])
+        sim.launch()
+        a = sim.results()
+        ra = sim.requests(0)
+    finally:
+        sim.close()
+    sim2 = P.Simulator([pt], [shorter], per_request=True)
+    try:
+        sim2.launch()
+        _same_results(a[0], sim2.results()[0], ra, sim2.requests(0), "reupload")
+    finally:
+        sim2.close()
