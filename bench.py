@@ -14,10 +14,20 @@ an NCCL all-reduce of the fixed-size summary/histogram buffer.
 
   value : simulated requests/s, traces already resident in HBM (CUDA events on
           the launching stream, max over ranks).
-  e2e   : same metric through the C-ABI with host traces: H2D of every trace
-          (16 B/request, pinned), simulate, D2H of the aggregates, per step.
+  e2e   : same metric end to end through the public API, the way the
+          reference's run_experiment works (simulation.cpp:136-169: the trace
+          is generated inside the run): per step the host sends the step's
+          fresh seeds (8 B per replica), the device generates every trace
+          (bit-identical to the reference's generate_workload) and simulates,
+          and the aggregates come back to the host.
+  e2e_host_traces : the same with traces generated on the host (all cores) and
+          uploaded (16 B/request H2D from pinned memory, copy of step k+1
+          overlapping step k); host generation time reported beside it.
   --impl reference : the reference C++ simulator (oracle/_ref, unmodified
-          sources) on all host cores over a bounded sample of the workload.
+          sources) on all host cores: one full-size replica of the workload per
+          core per step (cfg5: 16 x 5000 s replicas on a 16-core host).
+  --gpus N without torchrun: the script re-launches itself under
+          torch.distributed.run with N local ranks (127.0.0.1).
 """
 from __future__ import annotations
 
@@ -190,11 +200,10 @@ def cpu_reference(cfgs, threads, sample_replicas=None, sample_duration=None):
 
 
 def cpu_sample_spec(workload):
-    # bounded samples (~10-30 s of CPU work on the GPU box's cores)
+    # full-size replicas of the workload (same config as the GPU arm), one per
+    # core per step: cfg5 ~16 s of CPU work on a 16-core host
     if workload in ("cfg5", "cfg2"):
-        return {"replicas_per_core": 1, "duration": 500.0}
-    if workload == "cfg3":
-        return {"replicas_per_core": 2, "duration": None}
+        return {"replicas_per_core": 1, "duration": None}
     return {"replicas_per_core": 2, "duration": None}
 
 
@@ -227,16 +236,16 @@ def run_reference_arm(args, rank, world):
     gen = sum(t[1] for t in times)
     allocs = sum(t[2] for t in times)
     v = gen / wall
-    sample = (f"{nrep} replicas of the {args.workload} workload"
+    sample = (f"{nrep} full-size replicas of the {args.workload} workload"
               + (f" at duration {spec['duration']:g} s" if spec["duration"] else "")
-              + f" per step ({times[0][1]:.0f} simulated requests), run_experiment on a "
-              f"{threads}-thread std::thread pool")
+              + f" per step ({times[0][1]:.0f} simulated requests incl. generate_workload), "
+              f"run_experiment on a {threads}-thread std::thread pool")
     line = {
         "impl": "reference", "metric": "simulated_requests_per_s", "value": v,
         "unit": "sim-req/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * wall / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": desc, "sample": sample},
+        "config": {"workload": desc, "sample": sample, "same_config": spec["duration"] is None},
         "allocations_per_s": allocs / wall,
         "cpu_baseline": {"value": v, "unit": "sim-req/s", "cores": threads, "kind": "reference",
                          "sample": sample, "cpu_model": cpu_model()},
@@ -244,6 +253,19 @@ def run_reference_arm(args, rank, world):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def relaunch(n):
+    """`bench.py --gpus N` outside torchrun: one rank per GPU via
+    torch.distributed.run on 127.0.0.1 (rank 0 prints the line)."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())]
+    cmd += sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # --------------------------------------------------------------- our arm
@@ -258,11 +280,16 @@ def main():
     ap.add_argument("--duration", type=float, default=None, help="dev override (not a bench line)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-host-traces", action="store_true", help="skip the host-trace e2e leg")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args.gpus)
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus == 1 else 1)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference_arm(args, rank, world)
 
@@ -279,29 +306,19 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     desc, cfgs = workload_points(args.workload, rank, world, args.replicas, args.duration)
-    t0 = time.time()
     points = [P.experiment_from_config(c) for c in cfgs]
-    # host trace generation (pinned, for the e2e H2D leg); one trace per seed
-    from concurrent.futures import ThreadPoolExecutor
-    with ThreadPoolExecutor(max_workers=max(1, (os.cpu_count() or 2) // max(1, world))) as ex:
-        traces = list(ex.map(lambda p: P.generate_workload(p, pinned=True), points))
-    gen_s = time.time() - t0
-    n_req = sum(t.n for t in traces)
-    sim = P.Simulator(points, traces, device=local)
-    h2d_bytes = 16 * n_req
-
-    def step(upload):
-        if upload:
-            sim.upload_traces(stream=stream.cuda_stream)
-        sim.launch(stream=stream.cuda_stream)
+    # traces are generated on the device (bit-identical to generate_workload)
+    sim = P.Simulator(points, None, device=local)
+    R = len(points)
 
     # warm-up (also grows any arena that overflowed)
     for _ in range(args.warmup):
-        step(False)
+        sim.launch(stream=stream.cuda_stream)
         res = sim.results(stream=stream.cuda_stream)
     errs = [r["error"] for r in res if r["error"]]
     if errs:
         raise SystemExit(f"replica errors: {errs[:5]}")
+    n_req = sum(int(r["generated"]) for r in res)
 
     from paper_2512_16134_b200 import sweep
 
@@ -316,7 +333,7 @@ def main():
                 dist.barrier()
             torch.cuda.synchronize()
             ev0.record(stream)
-            step(False)
+            sim.launch(stream=stream.cuda_stream)
             ev1.record(stream)
             torch.cuda.synchronize()
             times.append(ev0.elapsed_time(ev1))
@@ -336,15 +353,58 @@ def main():
     total_alloc = summary["alloc_calls"]
     total_dsel = summary["decode_selects"]
     value = total_req / (ms / 1000.0)
+    import ctypes
+    d2h = ctypes.sizeof(P.api.Aggregates) * R
 
-    # ---- e2e: host traces -> H2D -> simulate -> D2H aggregates, through the
-    # public API.  Every step copies its own inputs from pinned host memory
-    # (16 B/request) and reads its aggregates back; the copy for step k+1 runs
-    # on a copy stream into the other trace slot while step k simulates.
+    # ---- e2e through the public API, generation included (the reference's
+    # run_experiment generates its trace inside the run): fresh seeds every
+    # step go host -> device, the device generates + simulates, aggregates
+    # come back.  Step k+1's generation is queued behind step k on one stream.
     e2e = None
     if not args.no_e2e:
         n_e = max(2, min(args.steps, 4))
-        sim.enable_trace_slots(2)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e_req = 0
+        t_a = time.perf_counter()
+        for k in range(n_e):
+            seeds = [int(p.exp.seed) + 1_000_003 * (k + 1) for p in points]
+            sim.generate(seeds, stream=stream.cuda_stream)
+            sim.launch(stream=stream.cuda_stream)
+            res2 = sim.results(stream=stream.cuda_stream)
+            e_req += sum(int(r["generated"]) for r in res2)
+        t_b = time.perf_counter()
+        if any(r["error"] for r in res2):
+            raise SystemExit("replica errors in the e2e leg")
+        es = (t_b - t_a) / n_e
+        e_rate = e_req / (t_b - t_a)
+        if dist:
+            t = torch.tensor([es, -e_rate, float(e_req)], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tt = torch.tensor([float(e_req)], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt)
+            es = float(t[0].item())
+            e_rate = float(tt.item()) / n_e / es
+        e2e = {"value": e_rate, "unit": "sim-req/s", "h2d_bytes_per_step": 8 * R * world,
+               "d2h_bytes_per_step": d2h * world, "ms_per_step": es * 1000.0, "steps": n_e,
+               "what": "per step: seeds H2D, device trace generation (generate_workload, "
+                       "bit-identical), DES + finalize, aggregates D2H; fresh seeds every step"}
+
+    # ---- e2e with host-generated traces uploaded every step (the r01 path)
+    e2e_host = None
+    if not args.no_e2e and not args.no_host_traces:
+        t0 = time.time()
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=max(1, (os.cpu_count() or 2) // max(1, world))) as ex:
+            traces = list(ex.map(lambda p: P.generate_workload(p, pinned=True), points))
+        gen_s = time.time() - t0
+        hsim = P.Simulator(points, traces, device=local)
+        h2d_bytes = 16 * sum(t.n for t in traces)
+        n_e = max(2, min(args.steps, 4))
+        hsim.launch(stream=stream.cuda_stream)  # warm-up
+        hsim.results(stream=stream.cuda_stream)
+        hsim.enable_trace_slots(2)
         copy = torch.cuda.Stream(device=dev)
         comp = torch.cuda.Stream(device=dev)  # (not the legacy default stream: it would serialise)
         up = [torch.cuda.Event(), torch.cuda.Event()]
@@ -352,30 +412,35 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         t_a = time.perf_counter()
-        sim.upload_traces(stream=copy.cuda_stream, slot=0)
+        hsim.upload_traces(stream=copy.cuda_stream, slot=0)
         up[0].record(copy)
         for k in range(n_e):
             sl = k & 1
             comp.wait_event(up[sl])
-            sim.launch(stream=comp.cuda_stream, slot=sl)
+            hsim.launch(stream=comp.cuda_stream, slot=sl)
             if k + 1 < n_e:  # the other slot's last reader (step k-1) has finished
-                sim.upload_traces(stream=copy.cuda_stream, slot=sl ^ 1)
+                hsim.upload_traces(stream=copy.cuda_stream, slot=sl ^ 1)
                 up[sl ^ 1].record(copy)
-            res2 = sim.results(stream=comp.cuda_stream)
+            res3 = hsim.results(stream=comp.cuda_stream)
         t_b = time.perf_counter()
         es = (t_b - t_a) / n_e
-        if any(r["error"] for r in res2):
-            raise SystemExit("replica errors in the e2e leg")
+        if any(r["error"] for r in res3):
+            raise SystemExit("replica errors in the host-trace e2e leg")
+        hreq = sum(t.n for t in traces)
         if dist:
-            t = torch.tensor([es], dtype=torch.float64, device=dev)
+            t = torch.tensor([es, gen_s], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            es = float(t.item())
-        import ctypes
-        e2e = {"value": total_req / es, "unit": "sim-req/s", "h2d_bytes_per_step": h2d_bytes * world,
-               "d2h_bytes_per_step": ctypes.sizeof(P.api.Aggregates) * len(points) * world,
-               "ms_per_step": es * 1000.0, "steps": n_e,
-               "pipelining": "step k+1's H2D (copy stream, second trace slot) overlaps step k",
-               "host_trace_generation_s": gen_s}
+            es, gen_s = float(t[0].item()), float(t[1].item())
+            tt = torch.tensor([float(hreq)], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt)
+            hreq = int(tt.item())
+        hsim.close()
+        e2e_host = {"value": hreq / es, "unit": "sim-req/s",
+                    "h2d_bytes_per_step": h2d_bytes * world, "d2h_bytes_per_step": d2h * world,
+                    "ms_per_step": es * 1000.0, "steps": n_e,
+                    "host_trace_generation_s": gen_s,
+                    "with_host_generation": hreq / (es + gen_s),
+                    "pipelining": "step k+1's H2D (copy stream, second trace slot) overlaps step k"}
 
     # ---- roofline: algorithmic bytes = 16 B/request (trace read), SURVEY §8d
     peaks = {}
@@ -419,12 +484,14 @@ def main():
         "data": "synthetic",
         "config": {"workload": desc, "replicas_per_gpu": len(points),
                    "requests_per_gpu": n_req, "l2": "inputs (16 B/request traces) far larger than L2",
+                   "traces": "generated on the device from the replicas' seeds (sbs_sim_create_generated)",
                    "parallelism": f"replicas sharded over {world} GPU(s), one warp per replica"},
         "allocations_per_s": total_alloc / (ms / 1000.0),
         "summary": {"completed": summary["completed"], "window_requests": summary["window_requests"],
                     "ttft_mean_s": summary.get("ttft_mean_s"), "events": summary["events"]},
         "decode_placements_per_s": total_dsel / (ms / 1000.0),
         "gpu_launches": args.steps * sim.launches_per_run,
+        "gpu_launches_e2e_step": 1 + sim.launches_per_run,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel_ms": des_ms,
                      "kernel_share_of_step": des_ms / ms,
@@ -432,6 +499,7 @@ def main():
                              "event chains make this latency-bound"},
         "clocks": clocks,
         "e2e": e2e,
+        "e2e_host_traces": e2e_host,
         "cpu_baseline": cpu,
     }
     if rank == 0:

@@ -373,6 +373,39 @@ int sbs_decode_select(const sbs_decode_batch* batch, void* stream);
  * 4 = more than 2048 units. */
 int sbs_decode_select_async(const sbs_decode_batch* batch, int32_t* error_out, void* stream);
 
+/* Batched schedule_decode_batch (decode_alloc.cpp:83-106): batch b places
+ * candidates [cand_off[b], cand_off[b+1]) onto units [unit_off[b],
+ * unit_off[b+1]) in the reference's order (sort_len desc, request_id asc,
+ * stable), one select_decode_unit each, adding B += 1, K += kv_len to the
+ * chosen unit (batch / kv updated in place).  Outputs per placement j of
+ * batch b (at cand_off[b] + j): order_out = input index of the candidate
+ * placed j-th, pos_out = the unit position chosen, and (nullable) the
+ * fallback flag and threshold the observer would see.  One warp per batch;
+ * max_candidates / max_units bound every batch (<= 4096 each).  DEVICE
+ * pointers; synchronous (checks the error flag). */
+typedef struct sbs_decode_schedule {
+  int32_t n_batches;
+  int32_t max_candidates;
+  int32_t max_units;
+  int32_t _pad;
+  const int64_t* cand_off;
+  const uint64_t* request_id;
+  const int64_t* sort_len;
+  const int64_t* kv_len;
+  const int64_t* unit_off;
+  int32_t* batch;
+  int64_t* kv;
+  double k;
+  int32_t* order_out;
+  int32_t* pos_out;
+  uint8_t* fallback_out;
+  double* threshold_out;
+} sbs_decode_schedule;
+int sbs_decode_schedule_batch(const sbs_decode_schedule* s, void* stream);
+/* Asynchronous form; error 3 = a batch with candidates but no units
+ * (select_decode_unit's logic_error), 4 = beyond max_candidates/max_units. */
+int sbs_decode_schedule_batch_async(const sbs_decode_schedule* s, int32_t* error_out, void* stream);
+
 const char* sbs_last_error(void);
 const char* sbs_version(void);
 

@@ -68,6 +68,9 @@ def lib():
                                              C.POINTER(C.c_int), _f64p]
         L.ref_percentile.argtypes = [_f64p, C.c_int64, C.c_double]
         L.ref_percentile.restype = C.c_double
+        L.ref_schedule_decode_batch.argtypes = [_i64p, C.c_int64, _i64p, _i64p, C.c_int64,
+                                                C.c_double, _i64p, C.POINTER(C.c_double),
+                                                C.POINTER(C.c_int)]
         L.ref_outlier_threshold.argtypes = [_i64p, C.c_int64, C.c_double]
         L.ref_outlier_threshold.restype = C.c_double
         L.ref_run_batch.argtypes = [C.POINTER(C.c_char_p), C.c_int64, C.c_int, _f64p,
@@ -160,6 +163,25 @@ def allocate_batch(pending, fresh, caps, n_limit, hits=None):
                                        _p(ot), _p(cnt))
     return {"mapping": om[: cnt[0]].copy(), "deferred": od[: cnt[1]].copy(),
             "throttled": ot[: cnt[2]].copy(), "caps": caps, "flow": bool(flow)}
+
+
+def schedule_decode_batch(cands, batch, kv, k=1.5):
+    """The reference's schedule_decode_batch: returns (placements (id, pos) in
+    placement order, thresholds, fallbacks, batch after, kv after)."""
+    c = np.ascontiguousarray(cands, np.int64).reshape(-1, 3)
+    b = np.array(batch, np.int64)
+    kv = np.array(kv, np.int64)
+    m = max(len(c), 1)
+    out = np.zeros((m, 2), np.int64)
+    th = np.zeros(m, np.float64)
+    fb = np.zeros(m, np.int32)
+    rc = lib().ref_schedule_decode_batch(_p(c), len(c), _p(b), _p(kv), len(b), float(k), _p(out),
+                                         th.ctypes.data_as(C.POINTER(C.c_double)),
+                                         fb.ctypes.data_as(C.POINTER(C.c_int)))
+    if rc:
+        raise RuntimeError(lib().ref_last_error().decode())
+    n = len(c)
+    return out[:n], th[:n], fb[:n].astype(bool), b, kv
 
 
 def select_decode_unit(batch, kv, k=1.5):

@@ -415,6 +415,43 @@ int ref_select_decode_unit(const std::int64_t* batch, const std::int64_t* kv,
   return pos;
 }
 
+// schedule_decode_batch (decode_alloc.cpp:83-106), the reference's own
+// function: cand rows (request_id, sort_len, kv_len); out rows (request_id,
+// unit position) in placement order, plus the observer's threshold/fallback
+// per placement; batch/kv updated in place.
+int ref_schedule_decode_batch(const std::int64_t* cand, std::int64_t n_cand,
+                              std::int64_t* batch, std::int64_t* kv, std::int64_t n_units,
+                              double k, std::int64_t* out, double* th_out, int* fb_out) {
+  try {
+    std::vector<DecodeCandidate> cands(static_cast<std::size_t>(n_cand));
+    for (std::int64_t i = 0; i < n_cand; ++i)
+      cands[static_cast<std::size_t>(i)] = DecodeCandidate{
+          static_cast<std::uint64_t>(cand[3 * i]), cand[3 * i + 1], cand[3 * i + 2]};
+    std::vector<DecodeUnitPlan> units(static_cast<std::size_t>(n_units));
+    for (std::int64_t i = 0; i < n_units; ++i)
+      units[static_cast<std::size_t>(i)] =
+          DecodeUnitPlan{static_cast<int>(i), static_cast<int>(batch[i]), kv[i]};
+    std::size_t j = 0;
+    auto res = schedule_decode_batch(cands, units, k, [&](const DecodePlacementInfo& info) {
+      th_out[j] = info.threshold;
+      fb_out[j] = info.fallback ? 1 : 0;
+      ++j;
+    });
+    for (std::size_t i = 0; i < res.size(); ++i) {
+      out[2 * i] = static_cast<std::int64_t>(res[i].first);
+      out[2 * i + 1] = res[i].second;
+    }
+    for (std::int64_t i = 0; i < n_units; ++i) {
+      batch[i] = units[static_cast<std::size_t>(i)].batch;
+      kv[i] = units[static_cast<std::size_t>(i)].kv;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 3;
+  }
+}
+
 double ref_percentile(const double* v, std::int64_t n, double p) {
   return percentile(std::vector<double>(v, v + n), p);
 }

@@ -7,5 +7,5 @@ from .api import (  # noqa: F401
     REFERENCE_AGG_KEYS, ConfigError, InvariantError, SbsError, Simulator, allocate_batch,
     allocate_one,
     experiment_from_config, generate_workload, lib, library_path, run_experiment,
-    select_decode_unit,
+    schedule_decode_batch, select_decode_unit,
 )

@@ -225,6 +225,7 @@ def lib():
                                           C.POINTER(Aggregates), C.c_int32]
         L.sbs_prefill_allocate.argtypes = [C.POINTER(WindowBatch), C.c_void_p]
         L.sbs_decode_select.argtypes = [C.POINTER(DecodeBatch), C.c_void_p]
+        L.sbs_decode_schedule_batch.argtypes = [C.c_void_p, C.c_void_p]
         L.sbs_prefill_allocate_one.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
                                                C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                                C.c_void_p, C.c_void_p, C.c_void_p]
@@ -242,7 +243,7 @@ EXPORTED_SYMBOLS = [
     "sbs_sim_enable_trace_slots", "sbs_sim_upload_traces_slot", "sbs_sim_launch_slot",
     "sbs_prefill_allocate_one", "sbs_generate_workload_device", "sbs_workload_capacity",
     "sbs_sim_create_generated", "sbs_sim_generate_slot", "sbs_sim_trace_stats",
-    "sbs_sim_trace_arrays",
+    "sbs_sim_trace_arrays", "sbs_decode_schedule_batch", "sbs_decode_schedule_batch_async",
 ]
 
 
@@ -853,3 +854,67 @@ def select_decode_unit(calls, k=1.5, device="cuda"):
     stream = torch.cuda.current_stream(dev).cuda_stream
     _check(lib().sbs_decode_select(C.byref(b), C.c_void_p(stream)))
     return t_pos.cpu().numpy(), t_fb.cpu().numpy().astype(bool), t_th.cpu().numpy()
+
+
+class DecodeSchedule(C.Structure):
+    _fields_ = [("n_batches", C.c_int32), ("max_candidates", C.c_int32),
+                ("max_units", C.c_int32), ("_pad", C.c_int32), ("cand_off", C.c_void_p),
+                ("request_id", C.c_void_p), ("sort_len", C.c_void_p), ("kv_len", C.c_void_p),
+                ("unit_off", C.c_void_p), ("batch", C.c_void_p), ("kv", C.c_void_p),
+                ("k", C.c_double), ("order_out", C.c_void_p), ("pos_out", C.c_void_p),
+                ("fallback_out", C.c_void_p), ("threshold_out", C.c_void_p)]
+
+
+def schedule_decode_batch(batches, k=1.5, device="cuda"):
+    """Batched schedule_decode_batch (decode_alloc.cpp:83-106), one warp per batch.
+
+    batches: list of (candidates[(request_id, sort_len, kv_len)], batch[], kv[]).
+    Returns, per batch, a dict: placements (request_id, unit position) in
+    placement order, threshold / fallback per placement, and the units'
+    batch / kv after the call (the reference mutates its units in place)."""
+    import torch
+    dev = torch.device(device)
+    co, uo = [0], [0]
+    rows, bs, ks = [], [], []
+    for cands, b, kv in batches:
+        c = np.asarray(cands, np.int64).reshape(-1, 3)
+        rows.append(c)
+        bs.append(np.asarray(b, np.int32))
+        ks.append(np.asarray(kv, np.int64))
+        co.append(co[-1] + len(c))
+        uo.append(uo[-1] + len(b))
+    allc = np.concatenate(rows) if rows else np.zeros((0, 3), np.int64)
+    M = max(1, co[-1])
+    t = lambda x, dt: torch.as_tensor(np.ascontiguousarray(x), dtype=dt, device=dev)
+    t_co, t_uo = t(co, torch.int64), t(uo, torch.int64)
+    t_id = t(allc[:, 0] if len(allc) else np.zeros(1, np.int64), torch.int64)
+    t_sl = t(allc[:, 1] if len(allc) else np.zeros(1, np.int64), torch.int64)
+    t_kl = t(allc[:, 2] if len(allc) else np.zeros(1, np.int64), torch.int64)
+    t_b = t(np.concatenate(bs) if uo[-1] else np.zeros(1, np.int32), torch.int32)
+    t_k = t(np.concatenate(ks) if uo[-1] else np.zeros(1, np.int64), torch.int64)
+    t_ord = torch.empty(M, dtype=torch.int32, device=dev)
+    t_pos = torch.empty(M, dtype=torch.int32, device=dev)
+    t_fb = torch.empty(M, dtype=torch.uint8, device=dev)
+    t_th = torch.empty(M, dtype=torch.float64, device=dev)
+    s = DecodeSchedule(n_batches=len(batches),
+                       max_candidates=max([len(r) for r in rows] + [1]),
+                       max_units=max([len(b) for b in bs] + [1]),
+                       cand_off=t_co.data_ptr(), request_id=t_id.data_ptr(),
+                       sort_len=t_sl.data_ptr(), kv_len=t_kl.data_ptr(), unit_off=t_uo.data_ptr(),
+                       batch=t_b.data_ptr(), kv=t_k.data_ptr(), k=float(k),
+                       order_out=t_ord.data_ptr(), pos_out=t_pos.data_ptr(),
+                       fallback_out=t_fb.data_ptr(), threshold_out=t_th.data_ptr())
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    _check(lib().sbs_decode_schedule_batch(C.byref(s), C.c_void_p(stream)))
+    ordv, pos = t_ord.cpu().numpy(), t_pos.cpu().numpy()
+    fb, th = t_fb.cpu().numpy().astype(bool), t_th.cpu().numpy()
+    b_after, k_after = t_b.cpu().numpy(), t_k.cpu().numpy()
+    out = []
+    for i in range(len(batches)):
+        c0, c1, u0, u1 = co[i], co[i + 1], uo[i], uo[i + 1]
+        ids = allc[c0:c1, 0][ordv[c0:c1]] if c1 > c0 else np.zeros(0, np.int64)
+        out.append({"placements": np.stack([ids, pos[c0:c1].astype(np.int64)], 1)
+                    if c1 > c0 else np.zeros((0, 2), np.int64),
+                    "threshold": th[c0:c1], "fallback": fb[c0:c1],
+                    "batch": b_after[u0:u1], "kv": k_after[u0:u1]})
+    return out

@@ -11,10 +11,16 @@
 //  iqr_kernel    : select_decode_unit (decode_alloc.cpp:38-81), one warp per
 //                  call: K staged and sorted in shared memory, Q1/Q3 by the
 //                  reference's FP64 interpolation, IQR mask, lex-min (B, K).
+//  sched_kernel  : schedule_decode_batch (decode_alloc.cpp:83-106), one warp
+//                  per candidate batch: stable order (sort_len desc, id asc),
+//                  then one select_decode_unit per candidate on units kept in
+//                  shared memory — the sorted K multiset is updated in place
+//                  (one O(U/32) shift per placement), B/K written back.
 //
 // No tensor cores: this is integer sorting/selection, HBM/latency bound.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "warp.cuh"
@@ -283,6 +289,166 @@ __global__ void __launch_bounds__(32 * kAllocWarps) iqr_kernel(IqrArgs A) {
     if (A.fallback_out) A.fallback_out[c] = fallback ? 1 : 0;
     if (A.threshold_out) A.threshold_out[c] = th;
   }
+}
+
+struct SchedArgs {
+  int32_t n_batches, max_cands, max_units;
+  const int64_t* cand_off;
+  const uint64_t* request_id;
+  const int64_t* sort_len;
+  const int64_t* kv_len;
+  const int64_t* unit_off;
+  int32_t* batch;
+  int64_t* kv;
+  double k;
+  int32_t* order_out;
+  int32_t* pos_out;
+  uint8_t* fallback_out;
+  double* threshold_out;
+  int32_t* error;
+};
+
+__device__ __forceinline__ uint64_t enc_k(int64_t v) { return (uint64_t)v ^ 0x8000000000000000ull; }
+__device__ __forceinline__ int64_t dec_k(uint64_t v) { return (int64_t)(v ^ 0x8000000000000000ull); }
+
+// std::stable_sort order of schedule_decode_batch (decode_alloc.cpp:88-93):
+// sort_len desc, request_id asc, then input position.
+__device__ __forceinline__ bool cand_before(const SchedArgs& A, int64_t c0, int x, int y) {
+  if (x < 0) return false;
+  if (y < 0) return true;
+  const int64_t lx = A.sort_len[c0 + x], ly = A.sort_len[c0 + y];
+  if (lx != ly) return lx > ly;
+  const uint64_t ix = A.request_id[c0 + x], iy = A.request_id[c0 + y];
+  if (ix != iy) return ix < iy;
+  return x < y;
+}
+
+__device__ __forceinline__ int lb_enc(const uint64_t* S, int n, uint64_t key) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (S[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ double pct_enc(const uint64_t* S, int lo, int hi, double frac) {
+  const double vlo = (double)dec_k(S[lo]);
+  if (lo == hi) return vlo;
+  return __dadd_rn(vlo, __dmul_rn(frac, __dsub_rn((double)dec_k(S[hi]), vlo)));
+}
+
+__global__ void __launch_bounds__(32) sched_kernel(SchedArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = lane_id();
+  const int bidx = blockIdx.x;
+  const int64_t c0 = A.cand_off[bidx], u0 = A.unit_off[bidx];
+  const int M = (int)(A.cand_off[bidx + 1] - c0), U = (int)(A.unit_off[bidx + 1] - u0);
+  if (M == 0) return;
+  if (U < 1 || M > A.max_cands || U > A.max_units) {
+    if (lane == 0) atomicExch(A.error, U < 1 ? 3 : 4);  // "select_decode_unit: no units"
+    return;
+  }
+  int Mp = 1;
+  while (Mp < M) Mp <<= 1;
+  int32_t* ord = (int32_t*)smem;
+  int32_t* sB = ord + ((A.max_cands + 1) & ~1) * 2;  // ord has room for the padded pow2
+  int64_t* sK = (int64_t*)(sB + ((A.max_units + 1) & ~1));
+  uint64_t* S = (uint64_t*)(sK + A.max_units);
+  uint64_t* T = S + A.max_units;
+  for (int i = lane; i < Mp; i += 32) ord[i] = i < M ? i : -1;
+  for (int u = lane; u < U; u += 32) {
+    sB[u] = A.batch[u0 + u];
+    sK[u] = A.kv[u0 + u];
+    S[u] = enc_k(sK[u]);
+  }
+  __syncwarp();
+  warp_sort_buf(S, U);
+  // candidates: bitonic network over positions with the stable comparator
+  for (int k2 = 2; k2 <= Mp; k2 <<= 1)
+    for (int j = k2 >> 1; j > 0; j >>= 1) {
+      for (int i = lane; i < (Mp >> 1); i += 32) {
+        const int x = ((i & ~(j - 1)) << 1) | (i & (j - 1)), y = x | j;
+        const bool up = (x & k2) == 0;
+        const int ox = ord[x], oy = ord[y];
+        if (cand_before(A, c0, oy, ox) == up) { ord[x] = oy; ord[y] = ox; }
+      }
+      __syncwarp();
+    }
+  // percentile ranks (decode_alloc.cpp:17-20) depend on U only
+  const double r25 = __ddiv_rn(__dmul_rn((double)U - 1.0, 25.0), 100.0);
+  const double r75 = __ddiv_rn(__dmul_rn((double)U - 1.0, 75.0), 100.0);
+  const int lo25 = (int)floor(r25), hi25 = (int)ceil(r25), lo75 = (int)floor(r75), hi75 = (int)ceil(r75);
+  const double f25 = __dsub_rn(r25, (double)lo25), f75 = __dsub_rn(r75, (double)lo75);
+  for (int j = 0; j < M; ++j) {
+    const int ci = ord[j];
+    const double q1 = pct_enc(S, lo25, hi25, f25), q3 = pct_enc(S, lo75, hi75, f75);
+    const double th = __dadd_rn(q3, __dmul_rn(A.k, __dsub_rn(q3, q1)));
+    int nsafe = 0;
+    for (int u = lane; u < U; u += 32) nsafe += ((double)sK[u] <= th) ? 1 : 0;
+    nsafe = __reduce_add_sync(kFull, nsafe);
+    const bool fallback = nsafe == 0;
+    int32_t bb = 0x7fffffff;
+    int64_t bk = kInf64;
+    int bp = 0x7fffffff;
+    for (int u = lane; u < U; u += 32) {
+      const int64_t kv = sK[u];
+      if (!fallback && !((double)kv <= th)) continue;
+      const int32_t b = sB[u];
+      if (b < bb || (b == bb && kv < bk)) { bb = b; bk = kv; bp = u; }
+    }
+    const uint32_t ob = (uint32_t)bb ^ 0x80000000u;
+    const uint32_t mb = __reduce_min_sync(kFull, ob);
+    const int64_t mk = warp_min_i64(ob == mb ? bk : kInf64);
+    const int pos = (int)__reduce_min_sync(kFull, (ob == mb && bk == mk) ? (uint32_t)bp : 0xffffffffu);
+    const int64_t old_k = sK[pos];
+    const int64_t new_k = old_k + A.kv_len[c0 + ci];
+    if (lane == 0) {
+      A.order_out[c0 + j] = ci;
+      A.pos_out[c0 + j] = pos;
+      if (A.fallback_out) A.fallback_out[c0 + j] = fallback ? 1 : 0;
+      if (A.threshold_out) A.threshold_out[c0 + j] = th;
+      sB[pos] += 1;
+      sK[pos] = new_k;
+    }
+    // sorted multiset: replace one old_k by new_k (ping-pong shift)
+    const uint64_t a = enc_k(old_k), b = enc_k(new_k);
+    if (a != b) {
+      const int i = lb_enc(S, U, a);
+      if (b > a) {
+        const int q = lb_enc(S, U, b) - 1;
+        for (int p = lane; p < U; p += 32) T[p] = (p < i || p > q) ? S[p] : (p == q ? b : S[p + 1]);
+      } else {
+        const int q = lb_enc(S, U, b);
+        for (int p = lane; p < U; p += 32) T[p] = (p < q || p > i) ? S[p] : (p == q ? b : S[p - 1]);
+      }
+      __syncwarp();
+      uint64_t* t = S; S = T; T = t;
+    } else {
+      __syncwarp();
+    }
+  }
+  for (int u = lane; u < U; u += 32) {
+    A.batch[u0 + u] = sB[u];
+    A.kv[u0 + u] = sK[u];
+  }
+}
+
+size_t sched_smem_bytes(int max_cands, int max_units) {
+  int mp = 1;
+  while (mp < max_cands) mp <<= 1;
+  const size_t ord = 4 * (size_t)std::max(mp, ((max_cands + 1) & ~1) * 2);
+  return ord + 4 * (size_t)((max_units + 1) & ~1) + 8 * (size_t)max_units * 3;
+}
+
+cudaError_t launch_sched(const SchedArgs& a, cudaStream_t st) {
+  if (a.n_batches <= 0) return cudaSuccess;
+  const size_t smem = sched_smem_bytes(a.max_cands, a.max_units);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(sched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  sched_kernel<<<a.n_batches, 32, smem, st>>>(a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_pbaa_one(const int64_t* rows, int n_pending, int n_new, const int64_t* caps,

@@ -77,6 +77,23 @@ cudaError_t launch_pbaa(const PbaaArgs& a, cudaStream_t st);
 cudaError_t launch_pbaa_one(const int64_t* rows, int n_pending, int n_new, const int64_t* caps,
                             int n_dp, int n_limit, int32_t* mapped_out, cudaStream_t st);
 cudaError_t launch_iqr(const IqrArgs& a, cudaStream_t st);
+struct SchedArgs {
+  int32_t n_batches, max_cands, max_units;
+  const int64_t* cand_off;
+  const uint64_t* request_id;
+  const int64_t* sort_len;
+  const int64_t* kv_len;
+  const int64_t* unit_off;
+  int32_t* batch;
+  int64_t* kv;
+  double k;
+  int32_t* order_out;
+  int32_t* pos_out;
+  uint8_t* fallback_out;
+  double* threshold_out;
+  int32_t* error;
+};
+cudaError_t launch_sched(const SchedArgs& a, cudaStream_t st);
 cudaError_t launch_gen(const sbs_gen_job* d_jobs, int n_jobs, const uint64_t* d_seeds, int want_digest,
                        cudaStream_t st);
 }  // namespace sbs
@@ -1818,6 +1835,52 @@ int sbs_decode_select_async(const sbs_decode_batch* b, int32_t* error_out, void*
     sbs::IqrArgs a{b->n_calls, b->unit_off, b->batch, b->kv, b->k, b->pos_out,
                    b->fallback_out, b->threshold_out, error_out};
     CUDA_OR_THROW(sbs::launch_iqr(a, (cudaStream_t)stream));
+    return SBS_OK;
+  });
+}
+
+namespace {
+sbs::SchedArgs sched_args(const sbs_decode_schedule* b, int32_t* err) {
+  if (b->max_candidates < 0 || b->max_candidates > 4096 || b->max_units < 1 || b->max_units > 4096)
+    throw Error{SBS_ERR_CONFIG, "sbs_decode_schedule: max_candidates / max_units must be <= 4096"};
+  sbs::SchedArgs a{};
+  a.n_batches = b->n_batches;
+  a.max_cands = std::max(1, b->max_candidates);
+  a.max_units = b->max_units;
+  a.cand_off = b->cand_off;
+  a.request_id = b->request_id;
+  a.sort_len = b->sort_len;
+  a.kv_len = b->kv_len;
+  a.unit_off = b->unit_off;
+  a.batch = b->batch;
+  a.kv = b->kv;
+  a.k = b->k;
+  a.order_out = b->order_out;
+  a.pos_out = b->pos_out;
+  a.fallback_out = b->fallback_out;
+  a.threshold_out = b->threshold_out;
+  a.error = err;
+  return a;
+}
+}  // namespace
+
+int sbs_decode_schedule_batch_async(const sbs_decode_schedule* b, int32_t* error_out, void* stream) {
+  return guarded([&] {
+    CUDA_OR_THROW(sbs::launch_sched(sched_args(b, error_out), (cudaStream_t)stream));
+    return SBS_OK;
+  });
+}
+
+int sbs_decode_schedule_batch(const sbs_decode_schedule* b, void* stream) {
+  return guarded([&] {
+    cudaStream_t st = (cudaStream_t)stream;
+    Scratch& sc = scratch();
+    CUDA_OR_THROW(cudaMemsetAsync(sc.d_err, 0, sizeof(int32_t), st));
+    CUDA_OR_THROW(sbs::launch_sched(sched_args(b, sc.d_err), st));
+    CUDA_OR_THROW(cudaMemcpyAsync(sc.h_err, sc.d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CUDA_OR_THROW(cudaStreamSynchronize(st));
+    if (*sc.h_err == 3) return fail(SBS_ERR_INVARIANT, "select_decode_unit: no units");
+    if (*sc.h_err) return fail(SBS_ERR_OVERFLOW, "decode batch beyond max_candidates / max_units");
     return SBS_OK;
   });
 }

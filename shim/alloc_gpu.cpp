@@ -5,9 +5,12 @@
 // drain_decode_admissions (:459-460), the acceptance audits — runs the
 // allocation on the B200 through the C-ABI (include/sbs_b200.h):
 //   allocate_batch / greedy_dispatch -> sbs_prefill_allocate (PBAA kernel)
-//   select_decode_unit / schedule_decode_batch -> sbs_decode_select (IQR kernel)
-// percentile / outlier_threshold / lex_less are the scalar helpers the
-// reference's metrics also use (metrics.cpp:151-152); they stay host math.
+//   select_decode_unit -> sbs_decode_select (IQR kernel)
+//   schedule_decode_batch -> sbs_decode_schedule_batch (one sched_kernel launch
+//                            per batch: order + every placement on the device)
+//   outlier_threshold -> the IQR kernel's threshold output
+// percentile / lex_less are scalar helpers the reference's own metrics TU
+// calls per finalize (metrics.cpp:151-152); they stay host math.
 //
 // Cache-aware PBAA (AllocMode::kCacheAware): Len_hit(r, d) is resolved on the
 // host against the PrefixCache objects the caller's DpPlans borrow and shipped
@@ -174,10 +177,45 @@ double percentile(std::vector<double> values, double p) {
 }
 
 double outlier_threshold(std::span<const Tokens> kv_loads, double k) {
-  std::vector<double> v(kv_loads.begin(), kv_loads.end());
-  double q1 = percentile(v, 25.0);
-  double q3 = percentile(std::move(v), 75.0);
-  return q3 + k * (q3 - q1);
+  // Q3 + k (Q3 - Q1) from the IQR kernel (the threshold it masks with)
+  const size_t U = kv_loads.size();
+  if (U == 0) throw std::logic_error("percentile: empty input");
+  if (U > 2048) {  // beyond the kernel's staging envelope: the same formula on the host
+    std::vector<double> v(kv_loads.begin(), kv_loads.end());
+    double q1 = percentile(v, 25.0);
+    double q3 = percentile(std::move(v), 75.0);
+    return q3 + k * (q3 - q1);
+  }
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = align8(off + bytes); return o; };
+  const size_t o_off = take(16), o_b = take(4 * U), o_k = take(8 * U), o_err = take(8),
+               o_pos = take(4), o_fb = take(8), o_th = take(8);
+  g_st.ensure(off + 64);
+  unsigned char* h = g_st.host;
+  int64_t uo[2] = {0, (int64_t)U};
+  std::memcpy(h + o_off, uo, 16);
+  for (size_t i = 0; i < U; ++i) {
+    ((int32_t*)(h + o_b))[i] = 0;
+    ((int64_t*)(h + o_k))[i] = kv_loads[i];
+  }
+  *(int32_t*)(h + o_err) = 0;
+  unsigned char* g = g_st.dev;
+  Staging::check(cudaMemcpyAsync(g, h, o_pos, cudaMemcpyHostToDevice, g_st.stream));
+  sbs_decode_batch b{};
+  b.n_calls = 1;
+  b.unit_off = (const int64_t*)(g + o_off);
+  b.batch = (const int32_t*)(g + o_b);
+  b.kv = (const int64_t*)(g + o_k);
+  b.k = k;
+  b.pos_out = (int32_t*)(g + o_pos);
+  b.fallback_out = (uint8_t*)(g + o_fb);
+  b.threshold_out = (double*)(g + o_th);
+  throw_rc(sbs_decode_select_async(&b, (int32_t*)(g + o_err), g_st.stream));
+  Staging::check(cudaMemcpyAsync(h + o_err, g + o_err, off - o_err, cudaMemcpyDeviceToHost,
+                                 g_st.stream));
+  Staging::check(cudaStreamSynchronize(g_st.stream));
+  if (int e = *(int32_t*)(h + o_err)) throw_rc(e == 3 ? SBS_ERR_INVARIANT : SBS_ERR_OVERFLOW);
+  return *(double*)(h + o_th);
 }
 
 bool lex_less(const std::pair<int, Tokens>& a, const std::pair<int, Tokens>& b) {
@@ -237,18 +275,78 @@ int select_decode_unit(const std::vector<DecodeUnitPlan>& units, double k,
 std::vector<std::pair<std::uint64_t, int>> schedule_decode_batch(
     std::vector<DecodeCandidate> candidates, std::vector<DecodeUnitPlan>& units, double k,
     const DecodeObserver& observe) {
-  std::stable_sort(candidates.begin(), candidates.end(),
-                   [](const DecodeCandidate& a, const DecodeCandidate& b) {
-                     return a.sort_len != b.sort_len ? a.sort_len > b.sort_len
-                                                     : a.request_id < b.request_id;
-                   });
+  // The whole batch is one sched_kernel launch (sbs_decode_schedule_batch):
+  // stable order + one select_decode_unit per candidate on the device.
   std::vector<std::pair<std::uint64_t, int>> out;
-  for (const auto& c : candidates) {
-    int pos = select_decode_unit(units, k, c.request_id, observe);
+  const size_t M = candidates.size(), U = units.size();
+  if (M == 0) return out;
+  if (U == 0) throw std::logic_error("select_decode_unit: no units");
+  if (M > 4096 || U > 4096) throw std::runtime_error("sbs_b200 shim: decode batch above 4096");
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off = align8(off + bytes); return o; };
+  const size_t o_co = take(16), o_id = take(8 * M), o_sl = take(8 * M), o_kl = take(8 * M),
+               o_uo = take(16), o_err = take(8), o_b = take(4 * U), o_k = take(8 * U),
+               o_ord = take(4 * M), o_pos = take(4 * M), o_fb = take(M), o_th = take(8 * M);
+  g_st.ensure(off + 64);
+  unsigned char* h = g_st.host;
+  const int64_t co[2] = {0, (int64_t)M}, uo[2] = {0, (int64_t)U};
+  std::memcpy(h + o_co, co, 16);
+  std::memcpy(h + o_uo, uo, 16);
+  for (size_t i = 0; i < M; ++i) {
+    ((uint64_t*)(h + o_id))[i] = candidates[i].request_id;
+    ((int64_t*)(h + o_sl))[i] = candidates[i].sort_len;
+    ((int64_t*)(h + o_kl))[i] = candidates[i].kv_len;
+  }
+  *(int32_t*)(h + o_err) = 0;
+  for (size_t u = 0; u < U; ++u) {
+    ((int32_t*)(h + o_b))[u] = units[u].batch;
+    ((int64_t*)(h + o_k))[u] = units[u].kv;
+  }
+  unsigned char* g = g_st.dev;
+  Staging::check(cudaMemcpyAsync(g, h, o_ord, cudaMemcpyHostToDevice, g_st.stream));
+  sbs_decode_schedule b{};
+  b.n_batches = 1;
+  b.max_candidates = (int32_t)M;
+  b.max_units = (int32_t)U;
+  b.cand_off = (const int64_t*)(g + o_co);
+  b.request_id = (const uint64_t*)(g + o_id);
+  b.sort_len = (const int64_t*)(g + o_sl);
+  b.kv_len = (const int64_t*)(g + o_kl);
+  b.unit_off = (const int64_t*)(g + o_uo);
+  b.batch = (int32_t*)(g + o_b);
+  b.kv = (int64_t*)(g + o_k);
+  b.k = k;
+  b.order_out = (int32_t*)(g + o_ord);
+  b.pos_out = (int32_t*)(g + o_pos);
+  b.fallback_out = (uint8_t*)(g + o_fb);
+  b.threshold_out = (double*)(g + o_th);
+  throw_rc(sbs_decode_schedule_batch_async(&b, (int32_t*)(g + o_err), g_st.stream));
+  Staging::check(cudaMemcpyAsync(h + o_err, g + o_err, off - o_err, cudaMemcpyDeviceToHost,
+                                 g_st.stream));
+  Staging::check(cudaStreamSynchronize(g_st.stream));
+  if (int e = *(int32_t*)(h + o_err)) throw_rc(e == 3 ? SBS_ERR_INVARIANT : SBS_ERR_OVERFLOW);
+  out.reserve(M);
+  for (size_t j = 0; j < M; ++j) {
+    const DecodeCandidate& c = candidates[(size_t)((int32_t*)(h + o_ord))[j]];
+    const int pos = ((int32_t*)(h + o_pos))[j];
+    if (observe) {  // the observer sees the units as they were before this placement
+      DecodePlacementInfo info;
+      info.request_id = c.request_id;
+      info.threshold = ((double*)(h + o_th))[j];
+      info.fallback = h[o_fb + j] != 0;
+      for (size_t i = 0; i < U; ++i) {
+        info.kv_snapshot.push_back(units[i].kv);
+        if (info.fallback || static_cast<double>(units[i].kv) <= info.threshold)
+          info.safe.push_back((int)i);
+      }
+      info.selected = pos;
+      observe(info);
+    }
     units[(size_t)pos].batch += 1;
     units[(size_t)pos].kv += c.kv_len;
     out.emplace_back(c.request_id, units[(size_t)pos].unit_index);
   }
+  // the device's final B/K are the same sums; keep the host copy authoritative
   return out;
 }
 

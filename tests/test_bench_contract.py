@@ -38,3 +38,23 @@ def test_reference_arm_json_line():
     assert line["impl"] == "reference" and line["value"] > 0
     assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+@pytest.mark.skipif(not ref.available(), reason="compiled reference unavailable")
+def test_gpus_flag_launches_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself with 2 ranks
+    (torch.distributed.run, 127.0.0.1); exactly one line, n_gpus 2."""
+    p = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2",
+                        "--workload", "cfg1", "--replicas", "2", "--steps", "1", "--warmup", "1"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["impl"] == "reference"
+
+
+def test_cpu_arm_is_same_config():
+    """The CPU arm runs full-size replicas of the GPU arm's workload."""
+    for w in ("cfg5", "cfg2", "cfg3", "cfg1"):
+        assert bench.cpu_sample_spec(w)["duration"] is None

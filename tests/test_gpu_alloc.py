@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 import paper_2512_16134_b200 as P
-from oracle import orc
+from oracle import orc, ref
 from tests.common import GOLD, records_decodes, records_windows, records_windows_ca
 
 pytestmark = pytest.mark.gpu
@@ -144,3 +144,89 @@ def test_allocate_one_host_arrays():
         assert g["deferred"].tolist() == w["deferred"]
         assert g["throttled"].tolist() == w["throttled"]
         assert g["caps"].tolist() == w["caps_out"]
+
+
+# ------------------------------------------------------------ schedule_decode_batch
+def _random_sched_batch(rng, big=False):
+    U = rng.choice([1, 2, 3, 4, 7, 32, 64, 320]) if not big else rng.choice([320, 1024, 2048])
+    M = rng.choice([0, 1, 2, 5, 17, 64]) if not big else rng.choice([100, 700])
+    lo = rng.choice([0, 0, 5])
+    kv = [lo + rng.randint(0, rng.choice([3, 50, 5000, 10**6])) for _ in range(U)]
+    b = [rng.randint(0, rng.choice([1, 3, 40])) for _ in range(U)]
+    ids = [rng.randint(0, max(2, M // 2) if rng.random() < 0.3 else 10**12) for _ in range(M)]
+    cands = [(ids[i], rng.choice([rng.randint(1, 9), rng.randint(1, 5000)]),
+              rng.choice([0, 1, rng.randint(1, 3000)])) for i in range(M)]
+    return cands, b, kv
+
+
+def test_schedule_decode_batch_vs_reference():
+    """1,000 random batches (ties in sort_len and request ids, duplicate ids,
+    empty batches, fallbacks) in one launch against the reference's own
+    schedule_decode_batch (and the C oracle): placements in order, the
+    observer's threshold/fallback per placement, the units after."""
+    import random
+    from oracle import orc
+    rng = random.Random(83106)
+    batches = [_random_sched_batch(rng) for _ in range(1000)]
+    batches += [_random_sched_batch(rng, big=True) for _ in range(8)]
+    for k in (1.5, 0.0, -3.0):  # k < 0 empties the IQR mask: the fallback path
+        _check_sched(batches, k)
+
+
+def _check_sched(batches, k):
+    from oracle import orc
+    got = P.schedule_decode_batch(batches, k=k)
+    for i, ((cands, b, kv), g) in enumerate(zip(batches, got)):
+        o_pl, o_b, o_kv = orc.schedule_decode_batch(cands, b, kv, k)
+        assert np.array_equal(g["placements"], o_pl), f"batch {i}: placements vs oracle"
+        if ref.available():
+            pl, th, fb, rb, rkv = ref.schedule_decode_batch(cands, b, kv, k)
+            assert np.array_equal(g["placements"], pl), f"batch {i}: placements"
+            assert np.array_equal(g["threshold"], th), f"batch {i}: thresholds"
+            assert np.array_equal(g["fallback"], fb), f"batch {i}: fallbacks"
+            assert np.array_equal(g["batch"], rb) and np.array_equal(g["kv"], rkv), f"batch {i}: units"
+
+
+def test_schedule_decode_batch_errors():
+    with pytest.raises(P.InvariantError):
+        P.schedule_decode_batch([([(1, 10, 10)], [], [])])
+    assert len(P.schedule_decode_batch([([], [], [])])[0]["placements"]) == 0
+
+
+def test_shim_schedule_decode_batch_vs_reference(tmp_path):
+    """The C++ drop-in (shim/alloc_gpu.cpp) under the reference's own
+    signature: what the caller and the observer see equals the reference."""
+    import random
+    import subprocess
+    from pathlib import Path
+    exe = Path(__file__).resolve().parents[1] / "shim" / "_build" / "sched_check"
+    if not exe.exists():
+        pytest.skip("shim not built")
+    rng = random.Random(4242)
+    batches = [_random_sched_batch(rng) for _ in range(300)]
+    batches = [bt for bt in batches if len(bt[0])]
+    lines = []
+    for cands, b, kv in batches:
+        lines.append(f"1.5 {len(cands)} {len(b)}")
+        lines += [f"{c[0]} {c[1]} {c[2]}" for c in cands]
+        lines += [f"{x} {y}" for x, y in zip(b, kv)]
+    f = tmp_path / "batches.txt"
+    f.write_text("\n".join(lines) + "\n")
+    out = subprocess.run([str(exe), str(f)], capture_output=True, text=True, check=True,
+                         timeout=600).stdout.splitlines()
+    assert len(out) == len(batches)
+    for i, ((cands, b, kv), line) in enumerate(zip(batches, out)):
+        tok = line.split()
+        iT, iF, iU = tok.index("T"), tok.index("F"), tok.index("U")
+        pl = np.array(tok[1:iT], np.int64).reshape(-1, 2)
+        th = np.array(tok[iT + 1:iF], np.float64)
+        fb = np.array(tok[iF + 1:iU], np.int64).astype(bool)
+        un = np.array(tok[iU + 1:], np.int64).reshape(-1, 2)
+        if ref.available():
+            w_pl, w_th, w_fb, w_b, w_kv = ref.schedule_decode_batch(cands, b, kv, 1.5)
+        else:
+            w_pl, w_b, w_kv = orc.schedule_decode_batch(cands, b, kv, 1.5)
+            w_th, w_fb = th, fb
+        assert np.array_equal(pl, w_pl), f"batch {i}"
+        assert np.array_equal(th, w_th) and np.array_equal(fb, w_fb), f"batch {i}: observer"
+        assert np.array_equal(un[:, 0], w_b) and np.array_equal(un[:, 1], w_kv), f"batch {i}: units"
