@@ -227,6 +227,8 @@ typedef struct sbs_sim sbs_sim;
 
 #define SBS_FLAG_PER_REQUEST 1u /* keep per-request timestamps (parity mode) */
 #define SBS_FLAG_LOGS 2u        /* keep run records (MetricsCollector, metrics.h:107-152) */
+#define SBS_FLAG_KV_LOADS 4u    /* with LOGS: also the per-unit KV loads of every decode step
+                                   (record 6), what MetricsCollector::record_kv receives */
 
 /* traces: host arrays (uploaded here).  trace_of_point[i] selects the trace of
  * point i (NULL: point i uses trace i).  Points sharing a trace share HBM. */
@@ -285,7 +287,8 @@ int sbs_sim_requests(sbs_sim* sim, int32_t point, int64_t* dispatch_ns,
  * kind | (payload words << 8) then payload; kinds 1 dispatch (time, instance),
  * 2 control (time, i_opt, t_fwd_bar, n_active), 3 pass (time, instance,
  * assigned[dp_degree]), 4 step (time, generated), 5 kv band (time, mean bits,
- * sigma bits, min, max).  These are the records behind passes.csv,
+ * sigma bits, min, max), 6 kv loads (time, K[unit] of the healthy live
+ * decode units; SBS_FLAG_KV_LOADS only).  These are the records behind passes.csv,
  * kvband.csv, control.csv and the dispatch log (metrics.cpp:194-273).
  * With words NULL only *n_out is set. */
 int sbs_sim_log(sbs_sim* sim, int32_t point, int64_t* words, int64_t cap, int64_t* n_out);

@@ -1507,6 +1507,28 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         const double mean = band[0], sigma = band[1];
         if (g_log) {
           log_rec(LOG_KV, 5, now, __double_as_longlong(mean), __double_as_longlong(sigma), vmin, vmax);
+          if (pt.log_kv_loads) {
+            // the loads record_kv_snapshot hands to record_kv (simulation.cpp:486-495):
+            // K of every unit of the healthy, live decode instances, in unit order
+            const int nl = __popc(live) * Dd;
+            if (log_n + 2 + nl > log_cap) {
+              log_n = log_cap + 1;
+              error = kErrOverflow;
+            } else {
+              if (lane == 0) {
+                g_log[log_n] = LOG_KVLOADS | ((int64_t)(1 + nl) << 8);
+                g_log[log_n + 1] = now;
+              }
+#pragma unroll 1
+              for (int u = lane; u < U; u += 32) {
+                const int inst = u / Dd;
+                if ((live >> inst) & 1u)
+                  g_log[log_n + 2 + __popc(live & ((1u << inst) - 1u)) * Dd + (u - inst * Dd)] =
+                      (int64_t)(s_PK[u] & kKMask);
+              }
+              log_n += 2 + nl;
+            }
+          }
         }
         if (now >= warmup && lane == 0) {
           cn->kv_mean = __dadd_rn(cn->kv_mean, mean);

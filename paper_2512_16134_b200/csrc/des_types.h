@@ -71,6 +71,8 @@ struct DevPoint {
   int32_t n_topo, n_drops, w_size;
   int32_t per_request;      // parity mode: also write completion + status
   int32_t split;            // run as a prefill warp + decode warp pair
+  int32_t log_kv_loads;     // run records also keep the per-unit KV loads per step
+  int32_t _pad0;
   // ---- constants (integer ns, FP64 engine coefficients)
   int64_t c_chunk, t_default, l_net, tps, horizon, warmup;
   double iqr_k, wd_mult, pf_base, pf_tok, dc_base, dc_req, dc_kv;
@@ -133,6 +135,7 @@ enum LogKind : int32_t {
   LOG_PASS = 3,      // time, instance, assigned[D]           (record_pass)
   LOG_STEP = 4,      // time, generated                       (record_step)
   LOG_KV = 5,        // time, mean bits, sigma bits, min, max (record_kv / kv_band)
+  LOG_KVLOADS = 6,   // time, K of every healthy live decode unit (record_kv's span)
 };
 
 struct DevResult {

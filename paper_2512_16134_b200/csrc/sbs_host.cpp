@@ -521,6 +521,7 @@ void build_point(sbs_sim& s, PointHost& p) {
   d.cap_batch = c.decode_max_batch_per_dp;
   d.w_size = (int32_t)c.w_size;
   d.per_request = (s.flags & SBS_FLAG_PER_REQUEST) ? 1 : 0;
+  d.log_kv_loads = ((s.flags & SBS_FLAG_LOGS) && (s.flags & SBS_FLAG_KV_LOADS)) ? 1 : 0;
   {
     const char* e = std::getenv("SBS_SPLIT");
     const bool allow = e == nullptr || std::atoi(e) != 0;

@@ -6,14 +6,14 @@ from __future__ import annotations
 
 import numpy as np
 
-LOG_DISPATCH, LOG_CONTROL, LOG_PASS, LOG_STEP, LOG_KV = 1, 2, 3, 4, 5
+LOG_DISPATCH, LOG_CONTROL, LOG_PASS, LOG_STEP, LOG_KV, LOG_KVLOADS = 1, 2, 3, 4, 5, 6
 STATUS_COMPLETED = 4
 
 
 def parse_log(words):
     """int64 words -> dict of record lists."""
     w = [int(x) for x in words]
-    out = {"dispatch": [], "control": [], "pass": [], "step": [], "kv": []}
+    out = {"dispatch": [], "control": [], "pass": [], "step": [], "kv": [], "kv_loads": []}
     i = 0
     while i < len(w):
         kind, n = w[i] & 0xFF, w[i] >> 8
@@ -31,6 +31,8 @@ def parse_log(words):
             mean = np.int64(pl[1]).view(np.float64).item()
             sigma = np.int64(pl[2]).view(np.float64).item()
             out["kv"].append((pl[0], mean, sigma, pl[3], pl[4]))
+        elif kind == LOG_KVLOADS:
+            out["kv_loads"].append((pl[0], pl[1:]))
         else:
             raise ValueError(f"bad log record kind {kind} at word {i}")
     return out

@@ -1,0 +1,25 @@
+// Test driver (test infrastructure): the reference-facing drop-in end to end —
+// load_config_file -> run_experiment (shim/sim_gpu.cpp: the B200 DES) ->
+// write_outputs (the reference's own writer over the refilled collector).
+// tests/test_gpu_reports.py compares the four CSVs with the reference's.
+//   usage: run_outputs <config.json> <out_dir>
+#include <cstdio>
+#include <exception>
+
+#include "sbsim/config.h"
+#include "sbsim/simulation.h"
+
+int main(int argc, char** argv) {
+  if (argc < 3) return 2;
+  try {
+    sbsim::ExperimentConfig cfg = sbsim::load_config_file(argv[1]);
+    sbsim::SimulationResult r = sbsim::run_experiment(cfg);
+    sbsim::write_outputs(cfg, r, argv[2]);
+    std::printf("kv_samples %zu passes %zu dispatches %zu\n", r.metrics.kv_samples().size(),
+                r.metrics.pass_samples().size(), r.metrics.dispatch_log().size());
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "run_outputs: %s\n", e.what());
+    return 1;
+  }
+  return 0;
+}

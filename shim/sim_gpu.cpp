@@ -7,9 +7,8 @@
 //
 // SimulationResult.metrics is refilled from the GPU run records through the
 // collector's public record_* methods (dispatch log, passes, control samples,
-// decode steps).  KV-band samples need the raw per-unit loads the collector
-// stores privately, so kvband.csv from this path is empty; the Python report
-// writer (paper_2512_16134_b200/reports.py) produces it byte-identically.
+// decode steps, and record_kv with the per-unit KV loads of every decode step,
+// SBS_FLAG_KV_LOADS), so write_outputs produces the reference's four CSVs.
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -240,7 +239,8 @@ SimulationResult run_experiment(const ExperimentConfig& config) {
   CTrace tr = make_trace(x.x);
   sbs_trace tv = tr.view();
   sbs_sim* sim = nullptr;
-  throw_rc(sbs_sim_create(&x.x, 1, &tv, 1, nullptr, SBS_FLAG_PER_REQUEST | SBS_FLAG_LOGS, 0, &sim));
+  throw_rc(sbs_sim_create(&x.x, 1, &tv, 1, nullptr,
+                          SBS_FLAG_PER_REQUEST | SBS_FLAG_LOGS | SBS_FLAG_KV_LOADS, 0, &sim));
   struct Guard {
     sbs_sim* s;
     ~Guard() { sbs_sim_destroy(s); }
@@ -299,6 +299,8 @@ SimulationResult run_experiment(const ExperimentConfig& config) {
       res.metrics.record_pass(b, config.cluster.c_chunk);
     } else if (kind == 4) {
       res.metrics.record_step(p[0], p[1]);
+    } else if (kind == 6) {  // record_kv_snapshot (simulation.cpp:486-495)
+      res.metrics.record_kv(p[0], std::span<const Tokens>(p + 1, (size_t)(len - 1)));
     }
     i += 1 + len;
   }

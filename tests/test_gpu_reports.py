@@ -94,3 +94,24 @@ def test_report_files_random_configs_vs_reference():
         want = ref.run(c, csv=True)["csv"]
         for kind in mine:
             assert mine[kind] == want[kind], f"random#{t} {kind}"
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_shim_write_outputs_byte_identical(name, tmp_path):
+    """The C++ drop-in: the reference's load_config_file -> run_experiment
+    (shim/sim_gpu.cpp on the B200) -> the reference's own write_outputs; the
+    four CSVs (incl. kvband.csv, refilled through record_kv from the kernel's
+    per-step KV loads) hash like the reference's."""
+    import subprocess
+    from pathlib import Path
+    exe = Path(__file__).resolve().parents[1] / "shim" / "_build" / "run_outputs"
+    if not exe.exists():
+        pytest.skip("shim not built")
+    cfg = tmp_path / "cfg.json"
+    cfg.write_text(json.dumps(CASES[name]))
+    out = tmp_path / "out"
+    p = subprocess.run([str(exe), str(cfg), str(out)], capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    for kind in ("requests", "passes", "kvband", "control"):
+        got = hashlib.sha256((out / f"{kind}.csv").read_bytes()).hexdigest()
+        assert got == SHA[name][kind], f"{name}/{kind}.csv (shim write_outputs) differs"
