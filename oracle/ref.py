@@ -71,6 +71,9 @@ def lib():
         L.ref_schedule_decode_batch.argtypes = [_i64p, C.c_int64, _i64p, _i64p, C.c_int64,
                                                 C.c_double, _i64p, C.POINTER(C.c_double),
                                                 C.POINTER(C.c_int)]
+        L.ref_find_peak_qps.argtypes = [C.c_char_p, C.c_double, C.c_double, C.c_double,
+                                        C.c_double, C.POINTER(C.c_double), C.c_int,
+                                        C.POINTER(C.c_double), C.POINTER(C.c_int)]
         L.ref_outlier_threshold.argtypes = [_i64p, C.c_int64, C.c_double]
         L.ref_outlier_threshold.restype = C.c_double
         L.ref_run_batch.argtypes = [C.POINTER(C.c_char_p), C.c_int64, C.c_int, _f64p,
@@ -182,6 +185,19 @@ def schedule_decode_batch(cands, batch, kv, k=1.5):
         raise RuntimeError(lib().ref_last_error().decode())
     n = len(c)
     return out[:n], th[:n], fb[:n].astype(bool), b, kv
+
+
+def find_peak_qps(cfg, slo, rmin, rmax, res):
+    """The reference's find_peak_qps: (probes [(rate, ttft, window, feasible)], peak, attainable)."""
+    buf = np.zeros((4096, 4), np.float64)
+    peak = C.c_double(0)
+    att = C.c_int(0)
+    n = lib().ref_find_peak_qps(json.dumps(cfg).encode(), slo, rmin, rmax, res,
+                                buf.ctypes.data_as(C.POINTER(C.c_double)), 4096, C.byref(peak),
+                                C.byref(att))
+    if n < 0:
+        raise RuntimeError(lib().ref_last_error().decode())
+    return buf[:n].copy(), peak.value, bool(att.value)
 
 
 def select_decode_unit(batch, kv, k=1.5):

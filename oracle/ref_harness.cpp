@@ -452,6 +452,33 @@ int ref_schedule_decode_batch(const std::int64_t* cand, std::int64_t n_cand,
   }
 }
 
+// find_peak_qps (simulation.cpp:608-644), the reference's own search: probes
+// as rows (rate, ttft_mean, window_requests, feasible); returns the probe count
+// (-1 on error), *peak / *attainable.
+int ref_find_peak_qps(const char* json_text, double slo, double rmin, double rmax, double res,
+                      double* probes, int cap, double* peak, int* attainable) {
+  try {
+    ExperimentConfig cfg = parse_config(json_text, "<test>");
+    PeakResult r = find_peak_qps(cfg, slo, rmin, rmax, res);
+    int n = 0;
+    for (const auto& p : r.probes) {
+      if (n < cap) {
+        probes[4 * n] = p.rate_qps;
+        probes[4 * n + 1] = p.ttft_mean_s;
+        probes[4 * n + 2] = static_cast<double>(p.window_requests);
+        probes[4 * n + 3] = p.feasible ? 1.0 : 0.0;
+      }
+      ++n;
+    }
+    *peak = r.peak_qps;
+    *attainable = r.attainable ? 1 : 0;
+    return n;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 double ref_percentile(const double* v, std::int64_t n, double p) {
   return percentile(std::vector<double>(v, v + n), p);
 }

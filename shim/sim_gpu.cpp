@@ -1,9 +1,9 @@
 // Drop-in replacement for the reference's simulation.cpp (proj/src), built
 // against the reference's own headers.  run_experiment (simulation.h:33) runs
 // the replica on the B200 through the C-ABI (sbs_sim_*), and find_peak_qps
-// (simulation.h:66-67) evaluates the *whole* bisection tree of candidate rates
-// as one multi-replica launch, then replays the reference's sequential search
-// over those results — same probes, same peak, one kernel.
+// (simulation.h:66-67) evaluates the bisection tree of candidate rates five
+// levels at a time as multi-replica launches and replays the reference's
+// sequential search over those results — same probes, same peak.
 //
 // SimulationResult.metrics is refilled from the GPU run records through the
 // collector's public record_* methods (dispatch log, passes, control samples,
@@ -19,6 +19,7 @@
 #include <map>
 #include <stdexcept>
 #include <thread>
+#include <tuple>
 #include <vector>
 
 #include "sbs_b200.h"
@@ -187,47 +188,98 @@ Aggregates to_agg(const sbs_aggregates& a) {
   return g;
 }
 
-// Many configs, one launch (one warp per replica).
-std::vector<sbs_aggregates> run_many(const std::vector<ExperimentConfig>& cfgs) {
-  std::vector<CExp> xs;
-  xs.reserve(cfgs.size());
-  for (const auto& c : cfgs) {
-    validate(c.cluster);
-    xs.push_back(to_c(c));
+// Many configs, one launch (one warp per replica).  Errors stay per config:
+// err[i] is the SBS_* code of config i (its trace generation or its replica),
+// msg[i] the message; the caller raises only for the configs it consumes.
+struct ManyResult {
+  std::vector<sbs_aggregates> agg;
+  std::vector<int> err;
+  std::vector<std::string> msg;
+};
+
+ManyResult run_many(const std::vector<ExperimentConfig>& cfgs) {
+  ManyResult out;
+  const size_t n = cfgs.size();
+  out.agg.assign(n, sbs_aggregates{});
+  out.err.assign(n, SBS_OK);
+  out.msg.assign(n, std::string());
+  std::vector<CExp> xs(n);
+  std::vector<CTrace> tr(n);
+  for (size_t i = 0; i < n; ++i) {
+    try {
+      validate(cfgs[i].cluster);
+      xs[i] = to_c(cfgs[i]);
+    } catch (const ConfigError& e) {
+      out.err[i] = SBS_ERR_CONFIG;
+      out.msg[i] = e.what();
+    }
   }
-  std::vector<CTrace> tr(cfgs.size());
   std::atomic<size_t> next{0};
-  std::exception_ptr err;
-  std::atomic<bool> bad{false};
   auto work = [&] {
-    for (size_t i; (i = next.fetch_add(1)) < tr.size();) {
+    for (size_t i; (i = next.fetch_add(1)) < n;) {
+      if (out.err[i]) continue;
+      int64_t cnt = 0;
+      uint64_t dg = 0;
+      int rc = sbs_generate_workload(&xs[i].x.workload, xs[i].x.seed, nullptr, nullptr, nullptr,
+                                     nullptr, nullptr, 0, &cnt, &dg);
+      if (rc != SBS_OK) {
+        out.err[i] = rc;
+        out.msg[i] = sbs_last_error();
+        continue;
+      }
       try {
         tr[i] = make_trace(xs[i].x);
-      } catch (...) {
-        if (!bad.exchange(true)) err = std::current_exception();
+      } catch (const std::exception& e) {
+        out.err[i] = SBS_ERR_CONFIG;
+        out.msg[i] = e.what();
       }
     }
   };
   std::vector<std::thread> pool;
-  unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), (unsigned)tr.size()));
+  unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), (unsigned)n));
   for (unsigned t = 0; t < nt; ++t) pool.emplace_back(work);
   for (auto& t : pool) t.join();
-  if (bad) std::rethrow_exception(err);
+  std::vector<size_t> live;
   std::vector<sbs_experiment> px;
   std::vector<sbs_trace> pt;
-  for (size_t i = 0; i < xs.size(); ++i) {
+  for (size_t i = 0; i < n; ++i) {
+    if (out.err[i]) continue;
+    live.push_back(i);
     px.push_back(xs[i].x);
     pt.push_back(tr[i].view());
   }
+  if (px.empty()) return out;
   sbs_sim* sim = nullptr;
-  throw_rc(sbs_sim_create(px.data(), (int32_t)px.size(), pt.data(), (int32_t)pt.size(), nullptr, 0,
-                          0, &sim));
-  std::vector<sbs_aggregates> out(px.size());
-  int rc = sbs_sim_launch(sim, nullptr);
-  if (rc == SBS_OK) rc = sbs_sim_results(sim, out.data(), nullptr, nullptr);
-  std::string msg = sbs_last_error();
+  int rc = sbs_sim_create(px.data(), (int32_t)px.size(), pt.data(), (int32_t)pt.size(), nullptr, 0, 0,
+                          &sim);
+  if (rc != SBS_OK) {  // a create failure is not attributable to one config
+    for (size_t i : live) {
+      out.err[i] = rc;
+      out.msg[i] = sbs_last_error();
+    }
+    return out;
+  }
+  std::vector<sbs_aggregates> agg(px.size());
+  rc = sbs_sim_launch(sim, nullptr);
+  if (rc == SBS_OK) rc = sbs_sim_results(sim, agg.data(), nullptr, nullptr);
+  const std::string m = sbs_last_error();
   sbs_sim_destroy(sim);
-  if (rc != SBS_OK) throw std::runtime_error("sbs_b200: " + msg);
+  for (size_t k = 0; k < live.size(); ++k) {
+    const size_t i = live[k];
+    out.agg[i] = agg[k];
+    if (agg[k].error) {
+      out.err[i] = agg[k].error;
+      out.msg[i] = "replica failed with code " + std::to_string(agg[k].error);
+    } else if (rc != SBS_OK && rc != agg[k].error) {
+      // launch-level failure (CUDA error): every replica of the launch failed
+      bool any = false;
+      for (auto& a : agg) any |= a.error != 0;
+      if (!any) {
+        out.err[i] = rc;
+        out.msg[i] = m;
+      }
+    }
+  }
   return out;
 }
 
@@ -355,31 +407,54 @@ PeakResult find_peak_qps(const ExperimentConfig& base, double slo_ttft_s, double
   if (slo_ttft_s <= 0) throw ConfigError("peak: slo_ttft must be > 0");
   if (rate_min <= 0 || rate_max < rate_min || resolution <= 0)
     throw ConfigError("peak: invalid rate search bounds");
-  // every rate the sequential bisection could probe: both ends + the midpoint
-  // tree (the interval halves identically on every path)
-  std::vector<double> rates{rate_min, rate_max};
-  std::vector<std::pair<double, double>> stack{{rate_min, rate_max}};
-  while (!stack.empty()) {
-    auto [lo, hi] = stack.back();
-    stack.pop_back();
-    if (!(hi - lo > resolution)) continue;
-    double mid = 0.5 * (lo + hi);
-    rates.push_back(mid);
-    stack.push_back({mid, hi});
-    stack.push_back({lo, mid});
-  }
-  std::vector<ExperimentConfig> cfgs;
-  for (double r : rates) {
-    ExperimentConfig c = base;
-    c.workload.rate_qps = r;
-    cfgs.push_back(c);
-  }
-  std::vector<sbs_aggregates> agg = run_many(cfgs);
-  std::map<double, const sbs_aggregates*> by_rate;
-  for (size_t i = 0; i < rates.size(); ++i) by_rate.emplace(rates[i], &agg[i]);
+  // Speculative batches: every launch evaluates the next kLevels levels of
+  // the bisection tree under the current interval (2^kLevels - 1 midpoints,
+  // plus both ends in the first launch); the reference's sequential search
+  // (simulation.cpp:608-644) is then replayed over the results, launching the
+  // next subtree only when the path leaves the evaluated one.  An error is
+  // raised only for a probe the sequential search actually makes.
+  constexpr int kLevels = 5;
+  std::map<double, std::pair<sbs_aggregates, std::pair<int, std::string>>> done;
+  auto evaluate = [&](std::vector<double> rates) {
+    std::vector<ExperimentConfig> cfgs;
+    std::vector<double> todo;
+    std::sort(rates.begin(), rates.end());
+    rates.erase(std::unique(rates.begin(), rates.end()), rates.end());
+    for (double r : rates)
+      if (!done.count(r)) {
+        ExperimentConfig c = base;
+        c.workload.rate_qps = r;
+        cfgs.push_back(c);
+        todo.push_back(r);
+      }
+    if (cfgs.empty()) return;
+    ManyResult m = run_many(cfgs);
+    for (size_t i = 0; i < todo.size(); ++i)
+      done.emplace(todo[i], std::make_pair(m.agg[i], std::make_pair(m.err[i], m.msg[i])));
+  };
+  auto subtree = [&](double lo, double hi, std::vector<double>& out) {
+    std::vector<std::tuple<double, double, int>> st{{lo, hi, 0}};
+    while (!st.empty()) {
+      auto [a, b, d] = st.back();
+      st.pop_back();
+      if (d >= kLevels || !(b - a > resolution)) continue;
+      const double mid = 0.5 * (a + b);
+      out.push_back(mid);
+      st.push_back({mid, b, d + 1});
+      st.push_back({a, mid, d + 1});
+    }
+  };
   PeakResult result;
-  auto probe = [&](double rate) {
-    const sbs_aggregates& a = *by_rate.at(rate);
+  auto probe = [&](double rate, double lo, double hi) {
+    if (!done.count(rate)) {
+      std::vector<double> rs{rate};
+      subtree(lo, hi, rs);
+      evaluate(rs);
+    }
+    const auto& [a, e] = done.at(rate);
+    if (e.first == SBS_ERR_CONFIG) throw ConfigError(e.second);
+    if (e.first == SBS_ERR_INVARIANT) throw std::logic_error(e.second);
+    if (e.first != SBS_OK) throw std::runtime_error("sbs_b200: " + e.second);
     PeakProbe p;
     p.rate_qps = rate;
     p.ttft_mean_s = a.ttft_mean_s;
@@ -388,16 +463,21 @@ PeakResult find_peak_qps(const ExperimentConfig& base, double slo_ttft_s, double
     result.probes.push_back(p);
     return p.feasible;
   };
-  if (!probe(rate_min)) return result;
+  {  // first launch: both ends and the top of the tree
+    std::vector<double> rs{rate_min, rate_max};
+    subtree(rate_min, rate_max, rs);
+    evaluate(rs);
+  }
+  if (!probe(rate_min, rate_min, rate_max)) return result;
   result.attainable = true;
-  if (probe(rate_max)) {
+  if (probe(rate_max, rate_min, rate_max)) {
     result.peak_qps = rate_max;
     return result;
   }
   double lo = rate_min, hi = rate_max;
   while (hi - lo > resolution) {
     double mid = 0.5 * (lo + hi);
-    if (probe(mid)) lo = mid;
+    if (probe(mid, lo, hi)) lo = mid;
     else hi = mid;
   }
   result.peak_qps = lo;

@@ -115,3 +115,30 @@ def test_shim_write_outputs_byte_identical(name, tmp_path):
     for kind in ("requests", "passes", "kvband", "control"):
         got = hashlib.sha256((out / f"{kind}.csv").read_bytes()).hexdigest()
         assert got == SHA[name][kind], f"{name}/{kind}.csv (shim write_outputs) differs"
+
+
+@pytest.mark.skipif(not HAVE_REF, reason="compiled reference unavailable")
+@pytest.mark.parametrize("slo,rmin,rmax,res", [(0.58, 1, 2048, 1), (0.3, 1, 2048, 0.01),
+                                                (0.58, 1, 256, 1), (1e-6, 1, 100, 1)])
+def test_shim_find_peak_qps_vs_reference(tmp_path, slo, rmin, rmax, res):
+    """find_peak_qps through the drop-in (speculative batches of the
+    bisection tree on the GPU, replayed): same probes in the same order,
+    same peak as the reference's sequential search (simulation.cpp:608-644)."""
+    import subprocess
+    from pathlib import Path
+    exe = Path(__file__).resolve().parents[1] / "shim" / "_build" / "run_outputs"
+    if not exe.exists():
+        pytest.skip("shim not built")
+    cfg = tmp_path / "cfg.json"
+    cfg.write_text(json.dumps(CASES["short_3k"]))
+    p = subprocess.run([str(exe), "peak", str(cfg), str(slo), str(rmin), str(rmax), str(res)],
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = p.stdout.splitlines()
+    peak, att = float(lines[0].split()[1]), lines[0].split()[2] == "1"
+    got = np.array([[float(x) for x in ln.split()[1:]] for ln in lines[1:]]).reshape(-1, 4)
+    want, wpeak, watt = ref.find_peak_qps(CASES["short_3k"], slo, rmin, rmax, res)
+    assert (peak, att) == (wpeak, watt)
+    assert got.shape == want.shape
+    assert np.array_equal(got[:, [0, 2, 3]], want[:, [0, 2, 3]])
+    assert np.allclose(got[:, 1], want[:, 1], rtol=1e-9, atol=0)
