@@ -13,6 +13,10 @@
  *   SBS_ERR_OVERFLOW   4  a fixed-capacity device arena overflowed (the host
  *                          wrappers retry with doubled capacity; never silent)
  *   SBS_ERR_CUDA       5  CUDA runtime error / no device / extension missing
+ *   SBS_ERR_ENVELOPE   6  a replica left the GPU path's integer envelope: a
+ *                          decode unit with B >= 2^15 or K >= 2^32, or more
+ *                          than 2^32 - 2^16 scheduled events (the device seq
+ *                          counter is 32-bit; simclock.h:63 uses 64)
  * sbs_last_error() returns a thread-local message for the last failure.
  */
 #ifndef SBS_B200_H_
@@ -29,6 +33,7 @@ extern "C" {
 #define SBS_ERR_INVARIANT 3
 #define SBS_ERR_OVERFLOW 4
 #define SBS_ERR_CUDA 5
+#define SBS_ERR_ENVELOPE 6
 
 /* SchedulerPolicy (config.h:19-24) */
 #define SBS_POLICY_SBS 0

@@ -21,7 +21,7 @@ import numpy as np
 PKG = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ["SBS_LIB"]) if os.environ.get("SBS_LIB") else PKG / "lib" / "libsbs_b200.so"
 
-OK, ERR_CONFIG, ERR_INVARIANT, ERR_OVERFLOW, ERR_CUDA = 0, 1, 3, 4, 5
+OK, ERR_CONFIG, ERR_INVARIANT, ERR_OVERFLOW, ERR_CUDA, ERR_ENVELOPE = 0, 1, 3, 4, 5, 6
 
 
 class ConfigError(RuntimeError):
@@ -636,10 +636,16 @@ class Simulator:
                          ps[:k] if has_pfx else None)
 
     def upload_traces(self, traces=None, stream=0, slot=0):
+        # The copy reads the host buffers asynchronously on `stream`: the
+        # previous upload's traces stay referenced until this call returns,
+        # by which point the library has waited for that copy to finish.
+        prev = (self.traces, self._tr)
         if traces is not None:
             self.traces = list(traces)
             self._tr = (Trace * len(self.traces))(*[t.as_c() for t in self.traces])
         _check(lib().sbs_sim_upload_traces_slot(self.handle, self._tr, slot, C.c_void_p(stream)))
+        self._inflight = (self.traces, self._tr)
+        del prev
 
     def enable_trace_slots(self, n=2):
         """Second trace buffer set: upload step k+1 while step k runs."""

@@ -104,7 +104,11 @@ __device__ __noinline__ void mt_twist_ool(uint64_t* mt) { mt_twist(mt); }
 // ---------------------------------------------------------------------------
 constexpr uint64_t kBOne = 1ull << 48;       // packed decode unit: B << 48 | K
 constexpr uint64_t kKMask = kBOne - 1;
-constexpr int kErrEnvelope = 6;               // B >= 2^15 or K >= 2^32 on a decode unit
+constexpr int kErrEnvelope = 6;               // B >= 2^15 or K >= 2^32 on a decode unit, or seq wrap
+// The event seq counter is 32-bit (the reference's is 64-bit, simclock.h:63):
+// a replica stops with kErrEnvelope before it can wrap.  One handler makes far
+// fewer than 2^16 schedule() calls, so checking once per event is enough.
+constexpr uint32_t kSeqLimit = 0xFFFF0000u;
 
 // Per-replica counters and FP sums (metrics.h:107-152 state), in shared memory
 // and written by lane 0 only: they are rarely read, so they should not occupy
@@ -1580,6 +1584,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     };
     int64_t dt_t = next_dtopo();
     for (;;) {
+      if (SBS_UNLIKELY(seq > kSeqLimit) && !aborted) { error = kErrEnvelope; aborted = true; }
       if (odirty) recompute_other();
       const int64_t td = o_t <= horizon ? o_t : kInf64;
       const int64_t tt = dt_t <= horizon ? dt_t : kInf64;
@@ -1699,6 +1704,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   if (g_log && sbs) log_rec(LOG_CONTROL, 4, 0, i_opt, t_bar, n_active, 0);  // simulation.cpp:152
   while (error == 0) {
     PROF_BEGIN(0);
+    if (SBS_UNLIKELY(seq > kSeqLimit)) { error = kErrEnvelope; break; }
     if (odirty) recompute_other();
     // live internal minimum: tick vs other
     int64_t it = o_t;
@@ -2259,10 +2265,21 @@ cudaError_t launch_des_cluster(int variant, const DevPoint* d_pts, int n_pts, De
   if (smem_per_rep > kMaxSmem) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem);
   if (e != cudaSuccess) return e;
-  static int max_clusters = 0;  // per process: one device kind
+  // co-resident clusters, per (device, kernel, block size): the grid is one
+  // CTA per SM of the current device (its SM count, not a constant)
+  int dev = 0;
+  e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 0 || dev >= 16) return cudaErrorInvalidDevice;
+  static int cache[16][4][9] = {};
+  const int vi = variant == 4 ? 0 : variant == 5 ? 1 : variant == 10 ? 2 : 3;
+  int& max_clusters = cache[dev][vi][wmax];
   if (max_clusters == 0) {
+    int n_sm = 0;
+    e = cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * 148, 1, 1);
+    cfg.gridDim = dim3((unsigned)(n_sm & ~1), 1, 1);
     cfg.blockDim = dim3(32 * wmax, 1, 1);
     cfg.dynamicSmemBytes = kOnePerSm;
     cudaLaunchAttribute at[1];

@@ -894,6 +894,9 @@ bool upload_traces_gather(sbs_sim& s, const sbs_trace* traces, int slot, cudaStr
     }
   }
   if (segs.empty()) return true;
+  // the previous gather has finished reading its host sources and table (the
+  // Python wrapper keeps those host buffers alive until this returns)
+  if (s.ev_segs) CUDA_OR_THROW(cudaEventSynchronize(s.ev_segs));
   if ((int)segs.size() > s.seg_cap) {
     if (s.h_segs) cudaFreeHost(s.h_segs);
     if (s.d_segs) cudaFree(s.d_segs);
@@ -901,8 +904,6 @@ bool upload_traces_gather(sbs_sim& s, const sbs_trace* traces, int slot, cudaStr
     CUDA_OR_THROW(cudaMallocHost(&s.h_segs, sizeof(sbs::CopySeg) * s.seg_cap));
     CUDA_OR_THROW(cudaMalloc(&s.d_segs, sizeof(sbs::CopySeg) * s.seg_cap));
     if (s.ev_segs == nullptr) CUDA_OR_THROW(cudaEventCreateWithFlags(&s.ev_segs, cudaEventDisableTiming));
-  } else if (s.ev_segs) {
-    CUDA_OR_THROW(cudaEventSynchronize(s.ev_segs));  // previous table no longer in use
   }
   int64_t blocks = 0;
   for (size_t k = 0; k < segs.size(); ++k) {
@@ -1078,7 +1079,8 @@ Scratch& scratch() {
   thread_local Scratch sc[16];
   int dev = 0;
   CUDA_OR_THROW(cudaGetDevice(&dev));
-  Scratch& s = sc[dev & 15];
+  if (dev < 0 || dev >= 16) throw Error{SBS_ERR_CUDA, "device ordinal above 15"};
+  Scratch& s = sc[dev];
   if (s.d_err == nullptr) {
     CUDA_OR_THROW(cudaMalloc(&s.d_err, sizeof(int32_t)));
     CUDA_OR_THROW(cudaMallocHost(&s.h_err, sizeof(int32_t)));
@@ -1535,7 +1537,10 @@ int sbs_sim_results(sbs_sim* s, sbs_aggregates* out, sbs_histograms* hist, void*
       finish_aggregates(p, s->h_res[i], out[s->order[i]], live_n(*s, p));
       if (s->h_res[i].error != 0) {
         rc = s->h_res[i].error;
-        g_err = "replica " + std::to_string(s->order[i]) + " failed with code " + std::to_string(rc);
+        g_err = "replica " + std::to_string(s->order[i]) + " failed with code " + std::to_string(rc) +
+                (rc == SBS_ERR_ENVELOPE
+                     ? " (integer envelope: decode unit B >= 2^15 or K >= 2^32, or 2^32 scheduled events)"
+                     : "");
       }
       if (hist) {
         CUDA_OR_THROW(cudaMemcpy(th.data(), p.dp.tpot_hist, 8 * sbs::kHistBins, cudaMemcpyDeviceToHost));
@@ -1716,10 +1721,14 @@ struct OneWindow {
   unsigned char* dev = nullptr;
   size_t cap = 0;
 };
+// One staging block per (thread, device), like scratch(): a device switch
+// never reuses another device's stream or staging memory.
 OneWindow& one_window() {
-  thread_local OneWindow w;
+  thread_local OneWindow ws[16];
   int dev = 0;
   CUDA_OR_THROW(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 16) throw Error{SBS_ERR_CUDA, "device ordinal above 15"};
+  OneWindow& w = ws[dev];
   if (w.device != dev) {
     CUDA_OR_THROW(cudaStreamCreateWithFlags(&w.stream, cudaStreamNonBlocking));
     CUDA_OR_THROW(cudaHostAlloc(&w.mapped, 4096, cudaHostAllocMapped));
