@@ -84,11 +84,6 @@ __device__ __forceinline__ int32_t key_len(uint64_t k) {
 }
 __device__ __forceinline__ int64_t key_id(uint64_t k) { return (int64_t)(k & 0xffffffffu); }
 
-__device__ __forceinline__ uint64_t decode_key(int64_t len, int64_t id) {
-  // ascending == (prompt+output desc, id asc) (simulation.cpp:446-453)
-  return ((uint64_t)(0xffffffffu - (uint32_t)len) << 32) | (uint64_t)(uint32_t)id;
-}
-
 __device__ __forceinline__ int hist_bin(int64_t v) {
   if (v <= 0) return 0;
   int b = 63 - __clzll(v);
@@ -262,11 +257,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   int64_t* const o_ftok = pt.o_ftok;
   int64_t* const o_comp = pt.o_comp;
   int8_t* const o_status = pt.o_status;
-  int64_t* const g_ttft = pt.ttft;
   int2* const g_fifo = pt.fifo;
   int4* const g_buckets = pt.buckets;
   uint64_t* const g_dwait = pt.dwait;
-  int64_t* const g_tpot_hist = pt.tpot_hist;
   int64_t* const g_log = LOG ? pt.log : nullptr;
   const int64_t log_cap = LOG ? pt.log_cap : 0;
   int64_t log_n = 0;
@@ -357,6 +350,10 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   int32_t mti = 312;
   bool S_valid = false, ul_dirty = true, ul_ident = false;
   bool S_gathered = false;      // s_S holds the unit Ks (unsorted) after a step
+  // IQR fast path (one decode instance, every unit listed, U <= 1024): lane l
+  // keeps the minimum of (B << 48 | K << 16 | u) over its units u = l mod 32
+  bool lmin_ok = false;
+  uint64_t lmin = UINT64_MAX;
   uint64_t S_mx = 0;
   // percentile ranks (decode_alloc.cpp:17-20) depend only on the unit count
   int pc_n = -1, lo25 = 0, hi25 = 0, lo75 = 0, hi75 = 0;
@@ -366,7 +363,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   int32_t pidx = 0, cur_ext = 0;   // ROLE 1: prefill-warp event index, handler is arrival/topology
   int32_t d_hk = 1, d_hi = 0;      // ROLE 2: handler of the decode event being processed
   int32_t ktail = 0;               // ROLE 1: hand-off keys written
-  int32_t ctail = 0, chead = 0;    // ROLE 2 / ROLE 1: completion ring positions
+  bool wreg = false;               // ROLE 2: the ndw (<= 32) waiters' sorted keys are in rkey
+  uint64_t rkey = 0;
 
   // other-event cache (EF/WD/DS min)
   bool odirty = true;
@@ -374,9 +372,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   uint32_t o_s = 0;
   int o_k = 0, o_i = 0;
 
-  // ---- counters (shared memory, lane 0) + lane-local TPOT partials
-  int64_t n_ttft = 0, tpot_n = 0;
-  double tpot_sum = 0.0;
+  // ---- counters (shared memory, lane 0)
 #ifdef SBS_PROF
   long long prof_acc[24] = {0};
   const long long prof_t0 = clock64();
@@ -514,86 +510,26 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     __syncwarp();
   };
 
-  // ---- completion accounting (metrics.cpp:117-153), called by the lanes
-  //      holding a completed request; all lanes must call (ballots inside).
-  int64_t l_cw = 0, l_wr = 0, l_ttft = 0, l_sched = 0, l_dev = 0, l_done = 0;
-  // All per-request inputs are passed in: the callers issue every global
-  // load of a completer at once (one memory round trip, not a chain).
-  auto complete_lanes = [&](bool has, int64_t id, int64_t ftok, bool decode, int64_t arr,
-                            int32_t out, int64_t disp, int64_t ps, int64_t t_done) {
-    int64_t ttft = 0;
-    bool inwin = false;
+  // ---- completion (metrics.cpp:117-153 inputs): the loop only stamps the
+  //      completion time; TTFT / scheduler / device waits, the window TTFT
+  //      buffer, TPOT and the completion counts are derived from the
+  //      per-request arrays by finalize_kernel after the run (deferred
+  //      accounting: no gathers on the event chains).
+  auto complete_req = [&](bool has, int64_t id, int64_t t_done) {
     if (has) {
-      l_done += 1;
-      if (t_done >= warmup) l_cw += 1;
-      if (per_req) {
-        o_comp[id] = t_done;
-        o_status[id] = kStCompleted;
-      }
-      if (decode) {
-        // TPOT (not in the reference): ns per output token after the first,
-        // one IEEE division (include/sbs_b200.h; pinned by test_gpu_north_star)
-        const double per = __ddiv_rn((double)(t_done - ftok), (double)(out - 1));
-        tpot_sum = __dadd_rn(tpot_sum, per);
-        tpot_n += 1;
-        atomicAdd((unsigned long long*)&g_tpot_hist[hist_bin((int64_t)per)], 1ull);
-      }
-      if (arr >= warmup) {
-        inwin = true;
-        ttft = ftok - arr;
-        l_wr += 1;
-        l_ttft += ttft;
-        l_sched += disp - arr;
-        l_dev += ps - disp;
-      }
+      o_comp[id] = t_done;
+      if (per_req) o_status[id] = kStCompleted;
     }
-    unsigned m = __ballot_sync(kFull, inwin);
-    if (inwin) {
-      const int64_t k = n_ttft + __popc(m & lt_mask);
-      g_ttft[ROLE == 2 ? N - 1 - k : k] = ttft;  // decode warp fills from the top
-    }
-    n_ttft += __popc(m);
   };
 
-  // ROLE 1: account the decode warp's completions (metrics.cpp:117-153 inputs)
-  auto consume_completions = [&]() {
-#ifdef SBS_PROF
-    const long long pc0 = clock64();
-#endif
-    for (;;) {
-      // one decode-warp chunk at a time, each record on the lane that held it
-      // there: the lane-local TPOT sums accumulate exactly as in a serial run.
-      // Entries carry the ring lap of their position: a chunk is taken once
-      // every word of it is visible (no release fence on the decode side).
-      const int i = chead + lane;
-      const uint64_t lap = (uint64_t)((i / kChanComp) & 0xFFFF);
-      const uint64_t w0 = (uint64_t)*(volatile long long*)&chL->comp_id[i % kChanComp];
-      const uint64_t w1 = (uint64_t)*(volatile long long*)&chL->comp_t[i % kChanComp];
-      const int cnt = __shfl_sync(kFull, (w0 >> 48) == lap ? (int)((w0 >> 32) & 63) : 0, 0);
-      if (cnt == 0) break;
-      const bool has = lane < cnt;
-      if (!__all_sync(kFull, !has || ((w0 >> 48) == lap && (w1 >> 48) == lap))) break;
-      int64_t id = 0, t = 0, ft = 0, arr = 0, disp = 0, ps = 0;
-      int32_t out = 0;
-      if (has) {
-        id = (int64_t)(w0 & 0xFFFFFFFFull);
-        t = (int64_t)(w1 & ((1ull << 48) - 1));
-        ft = o_ftok[id];
-        arr = __ldg(g_arr + id);
-        out = __ldg(g_output + id);
-        disp = o_dispatch[id];
-        ps = o_pstart[id];
-      }
-      complete_lanes(has, id, ft, true, arr, out, disp, ps, t);
-      chead += cnt;
-      __syncwarp();  // every lane's entry reads precede the release of the slots
-      if (lane == 0) chR->chead = chead;
-    }
-#ifdef SBS_PROF
-    prof_acc[19] += clock64() - pc0;
-#endif
+  // decode waiter key (DevPoint::kq_*): ascending == (prompt+output desc, id
+  // asc) (simulation.cpp:446-453), carrying output_len when there is room
+  auto wait_key = [&](int32_t prompt, int32_t out, int64_t id) -> uint64_t {
+    const int ob = pt.kq_ob, ib = pt.kq_ib;
+    const uint64_t len = (uint64_t)(int64_t)prompt + (uint64_t)(int64_t)out;
+    return (((uint64_t)pt.kq_lmax - len) << (ib + ob)) | ((uint64_t)id << ob) |
+           (ob ? (uint64_t)(uint32_t)out : 0ull);
   };
-  // (the lane-local partial sums above are exact integers: reduced once at the end)
 
   // ---- decode unit list over healthy, live decode instances, skipping
   //      capped units (simulation.cpp:432-442)
@@ -613,12 +549,16 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     nul = cnt;
     ul_ident = cnt == U;
     ul_dirty = false;
+    lmin_ok = false;  // per-lane minima are rebuilt by the next decode step
     S_valid = false;
     S_gathered = false;
   };
 
   // sorted K multiset (for Q1/Q3) by warp radix sort
   auto rebuild_S = [&]() {
+#ifdef SBS_PROF
+    prof_acc[18] += 1;  // sorts
+#endif
     uint64_t mx = S_mx;
     if (!S_gathered) {
       mx = 0;
@@ -709,6 +649,17 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     else if ((int64_t)s_S[nul - 1] > thi) CNT(mask, 1);
     // lexicographic (B, K, position) as one u64: B << 48 | K << 16 | position
     // (K < 2^32, position < 2^16)
+    if (lmin_ok) {
+      // the lex-min over all units is the answer whenever it is safe (or the
+      // safe set is empty): the minimum over a superset that lies in the set
+      const uint32_t h = __reduce_min_sync(kFull, (uint32_t)(lmin >> 32));
+      const uint32_t l = __reduce_min_sync(kFull, (uint32_t)(lmin >> 32) == h ? (uint32_t)lmin : 0xffffffffu);
+      const uint64_t gm = ((uint64_t)h << 32) | l;
+      if (SBS_LIKELY(fallback || (int64_t)((gm >> 16) & 0xffffffffull) <= thi)) {
+        PROF_END(5);
+        return (int)(gm & 0xffffu);
+      }
+    }
     uint64_t best = UINT64_MAX;
     if (ul_ident) {
       // rolled, with the next unit's load issued ahead (hides the smem latency)
@@ -764,22 +715,31 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     int32_t order_lane = -1;  // lane t holds the t-th instance to begin
     int ntouched = 0;
     if (ndw > 0) {
+#ifdef SBS_PROF
+    prof_acc[15] += 1;  // drains with waiters
+#endif
     for (int j = 0; j < Dn; ++j) maybe_die_d(j);
-    warp_sort_buf<true>(g_dwait, ndw);
+    if (!wreg) warp_sort_buf<true>(g_dwait, ndw);
     int wi = 0;
-    uint64_t w_key = 0;
+    int64_t w_id = 0;
     int32_t w_prompt = 0, w_out = 0;
+    const int kq_ob = pt.kq_ob, kq_ib = pt.kq_ib;
     while (wi < ndw) {
       if (SBS_UNLIKELY(ul_dirty)) rebuild_ulist();
       if (nul == 0) break;
-      if ((wi & 31) == 0) {  // next 32 waiters: keys + lengths fetched in parallel
-        w_key = (wi + lane < ndw) ? g_dwait[wi + lane] : 0;
-        const int64_t wid = key_id(w_key);
-        w_prompt = (wi + lane < ndw) ? __ldg(g_prompt + wid) : 0;
-        w_out = (wi + lane < ndw) ? __ldg(g_output + wid) : 0;
+      if ((wi & 31) == 0) {  // next 32 waiters: ids + lengths decoded in parallel
+        const bool v = wi + lane < ndw;
+        const uint64_t w_key = wreg ? rkey : (v ? g_dwait[wi + lane] : 0);
+        w_id = (int64_t)((w_key >> kq_ob) & ((1ull << kq_ib) - 1));
+        if (SBS_LIKELY(kq_ob != 0)) {  // lengths travel in the key
+          w_out = (int32_t)(w_key & ((1ull << kq_ob) - 1));
+          w_prompt = (int32_t)((int64_t)pt.kq_lmax - (int64_t)(w_key >> (kq_ib + kq_ob)) - w_out);
+        } else {
+          w_prompt = v ? __ldg(g_prompt + w_id) : 0;
+          w_out = v ? __ldg(g_output + w_id) : 0;
+        }
       }
-      const uint64_t key = bcast(w_key, wi & 31);
-      const int64_t id = key_id(key);
+      const int64_t id = bcast(w_id, wi & 31);
       const int32_t prompt = bcast(w_prompt, wi & 31);
       const int32_t out = bcast(w_out, wi & 31);
       int pos;
@@ -820,6 +780,17 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         d_worst = t > d_worst ? t : d_worst;
       }
       __syncwarp();
+      if (lmin_ok) {  // unit u's owner lane re-takes its minimum (all lanes load one unit each)
+        const int ow = u & 31, v = ow + 32 * lane;
+        uint64_t c = UINT64_MAX;
+        if (v < U) {
+          const uint64_t k = s_PK[v];
+          c = (k & ~kKMask) | ((k & kKMask) << 16) | (uint64_t)v;
+        }
+        const uint32_t h = __reduce_min_sync(kFull, (uint32_t)(c >> 32));
+        const uint32_t l = __reduce_min_sync(kFull, (uint32_t)(c >> 32) == h ? (uint32_t)c : 0xffffffffu);
+        if (lane == ow) lmin = ((uint64_t)h << 32) | l;
+      }
       PROF_BEGIN(6);
       if (S_valid) S_update(K0, K1);
       PROF_END(6);
@@ -846,7 +817,11 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       wi += 1;
     }
     // keep unadmitted waiters (still sorted)
-    if (wi > 0 && wi < ndw) {
+    if (wreg) {
+      if (lane >= wi && lane < ndw) g_dwait[lane - wi] = rkey;
+      __syncwarp();
+      wreg = false;
+    } else if (wi > 0 && wi < ndw) {
 #pragma unroll 1
       for (int base = 0; base < ndw - wi; base += 32) {
         int i = base + lane;
@@ -970,20 +945,17 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       }
       bool has = d < D;
       if (!__any_sync(kFull, has)) break;
-      int64_t id = 0, arr = 0, disp = 0, ps = 0;
+      int64_t id = 0;
       int32_t out = 0;
       if (has) {
         id = g_fifo[(int64_t)(g0 + d) * F + (idx & Fm)].x;
         idx += 1;
         out = __ldg(g_output + id);
-        arr = __ldg(g_arr + id);
-        disp = o_dispatch[id];
-        ps = o_pstart[id];
         o_ftok[id] = now;
       }
       bool done = has && out <= 1;   // decode_target() == 0
       bool wait = has && out > 1;
-      complete_lanes(done, id, now, false, arr, out, disp, ps, now);
+      complete_req(done, id, now);
       unsigned m = __ballot_sync(kFull, wait);
       if (ROLE == 1) {
         // hand-off ring: wait for room (the decode warp consumes independently);
@@ -993,13 +965,12 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
           for (;;) {
             const int kh = chL->khead;
             if (ktail + 32 - kh <= kChanKeys) break;
-            consume_completions();  // the decode warp may be waiting on us
             __nanosleep(100);
           }
           chan_fence<CL>();
           if (wait) {
             int32_t prompt = __ldg(g_prompt + id);
-            chR->keys[(ktail + __popc(m & lt_mask)) % kChanKeys] = decode_key((int64_t)prompt + out, id);
+            chR->keys[(ktail + __popc(m & lt_mask)) % kChanKeys] = wait_key(prompt, out, id);
           }
           ktail += __popc(m);
           ndw += __popc(m);  // keys of this EndForward
@@ -1007,7 +978,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       } else {
         if (wait) {
           int32_t prompt = __ldg(g_prompt + id);
-          g_dwait[ndw + __popc(m & lt_mask)] = decode_key((int64_t)prompt + out, id);
+          g_dwait[ndw + __popc(m & lt_mask)] = wait_key(prompt, out, id);
         }
         ndw += __popc(m);
         if (ndw > QD - 32) { error = kErrOverflow; break; }
@@ -1352,52 +1323,17 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     const int4* ent = g_buckets + (int64_t)b * BC;
     const int4* stg = s_stage + j * kStageEntries;  // entries < kStageEntries (lane-owned copies)
     asm volatile("cp.async.wait_all;" ::: "memory");
-    int64_t exc = 0, rel = 0;
+    int64_t exc = 0;
     PROF_BEGIN(11);
 #pragma unroll 1
     for (int base = 0; base < n; base += 32) {
-      int e = base + lane;
-      bool has = e < n;
-      int64_t id = 0, ft = 0, arr = 0, disp = 0, ps = 0;
-      int32_t out = 0;
-      if (ROLE == 2) {
-        // completion accounting goes back to the prefill warp: (id, time)
-        const int cnt = n - base < 32 ? n - base : 32;
-        for (;;) {
-          const int chd = chan_ld<CL>(&chL->chead);
-          if (ctail + cnt - chd <= kChanComp) break;
-#ifdef SBS_PROF
-          prof_acc[18] += 1;
-#endif
-          __nanosleep(64);
-        }
-        if (has) {
-          const int4 v = e < kStageEntries ? stg[e] : ent[e];
-          const int pos = ctail + lane, slot = pos % kChanComp;
-          const uint64_t lap = (uint64_t)((pos / kChanComp) & 0xFFFF) << 48;
-          chR->comp_t[slot] = (int64_t)((uint64_t)now | lap);
-          chR->comp_id[slot] =
-              (int64_t)((uint64_t)(uint32_t)v.x | (lane == 0 ? (uint64_t)cnt << 32 : 0) | lap);
-          atomicAdd((unsigned long long*)&s_R[v.y], (unsigned long long)(kBOne | (uint64_t)(uint32_t)v.z));
-          exc += v.w;
-          rel += (uint32_t)v.z;
-        }
-        ctail += cnt;
-        continue;
-      }
-      if (has) {
+      const int e = base + lane;
+      if (e < n) {
         const int4 v = e < kStageEntries ? stg[e] : ent[e];
-        id = v.x;
-        ft = o_ftok[id];  // every load of the completer issued before any use
-        arr = __ldg(g_arr + id);
-        out = __ldg(g_output + id);
-        disp = o_dispatch[id];
-        ps = o_pstart[id];
+        complete_req(true, v.x, now);
         atomicAdd((unsigned long long*)&s_R[v.y], (unsigned long long)(kBOne | (uint64_t)(uint32_t)v.z));
         exc += v.w;
-        rel += (uint32_t)v.z;
       }
-      complete_lanes(has, id, ft, true, arr, out, disp, ps, now);
     }
     __syncwarp();
     if (lane == 0) s_bcnt[b] = 0;
@@ -1409,6 +1345,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     uint64_t mx = 0, s1 = 0, s2lo = 0, s2hi = 0;  // sum K, sum K^2 (128-bit)
     const bool band_fast = !LOG && Dn == 1 && now >= warmup;
     double worst = 0.0;
+    uint64_t lm = UINT64_MAX;
 #pragma unroll 1
     for (int d = lane; d < Dd; d += 32) {
       const int u = u0 + d;
@@ -1418,6 +1355,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       const uint64_t K = (k & kKMask) + (uint64_t)(tps * st) - (r & kKMask);
       const uint64_t B = (k >> 48) - (r >> 48);
       s_PK[u] = (B << 48) | K;
+      const uint64_t c = (B << 48) | (K << 16) | (uint64_t)u;
+      lm = c < lm ? c : lm;
       s_nst[u] = (int32_t)B;
       if (r) s_R[u] = 0;
       if (gather) s_S[u] = (uint32_t)K;
@@ -1431,7 +1370,6 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     }
     PROF_END(12);
     PROF_BEGIN(13);
-    (void)rel;
     // per-step reductions as independent 32-bit REDUX: the step time's max
     // over non-negative doubles is the max of their bit patterns; the exact
     // sums are split into chunks whose 32-lane sums cannot overflow 32 bits
@@ -1458,13 +1396,14 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     exc = (int64_t)__reduce_add_sync(kFull, (uint32_t)exc);
     const int64_t stamped = bcast(d_res_begin, j);
     const int64_t gen = tps * stamped - exc;
-    (void)rel;
     if (lane == j) {
       d_res -= n;
       d_worst = worst;
       dflags &= ~G_STEP;
     }
     S_valid = false;
+    lmin = lm;
+    lmin_ok = dec_policy == kIqr && Dn == 1 && U <= 1024 && ul_ident && !ul_dirty;
     if (gather) {
       S_gathered = true;
       S_mx = (uint64_t)__reduce_max_sync(kFull, (uint32_t)mx);
@@ -1654,8 +1593,15 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         // record's are released at the next one, or exactly before a wait)
         if (lane == 0) { chR->head = rhead; chR->khead = khead; }
         pub_head = rhead;
+        if (ndw == 0 && nk <= 32) {
+          // the usual case: this record's waiters only, sorted in registers
+          rkey = lane < nk ? chL->keys[(k0 + lane) % kChanKeys] : UINT64_MAX;
+          if (nk > 1) rkey = warp_sort32<true>(rkey);
+          wreg = true;
+        } else {
 #pragma unroll 1
-        for (int i = lane; i < nk; i += 32) g_dwait[ndw + i] = chL->keys[(k0 + i) % kChanKeys];
+          for (int i = lane; i < nk; i += 32) g_dwait[ndw + i] = chL->keys[(k0 + i) % kChanKeys];
+        }
         ndw += nk;
         rhead += 1;
         khead += nk;
@@ -1692,9 +1638,6 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       }
       if (error) aborted = true;
     }
-    chan_fence<CL>();
-    __syncwarp();
-    if (lane == 0) chR->d_done = 1;
 #ifdef SBS_PROF
     prof_acc[20] += clock64() - prof_t0;
 #endif
@@ -1722,7 +1665,6 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     PROF_END(0);
     CNT(events, 1);
     if (ROLE == 1) {
-      consume_completions();
       // progress for the decode warp: every event before `et` is processed.
       // (Ordered after every earlier record by the fence that follows each
       // record publish; a stale value only makes the decode warp wait.)
@@ -1775,7 +1717,6 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
 #ifdef SBS_PROF
           prof_acc[17] += 1;
 #endif
-          consume_completions();  // the decode warp may be waiting on us
           __nanosleep(100);
         }
         chan_fence<CL>();
@@ -1907,37 +1848,18 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
 #ifdef SBS_PROF
     prof_acc[21] += clock64() - prof_t0;
 #endif
-    // the decode warp finishes later: keep accounting its completions
-    for (;;) {
-      const int dd = chL->d_done;
-      chan_fence<CL>();
-      consume_completions();
-      if (dd) break;
-      __nanosleep(128);
-    }
-    consume_completions();
   }
   }  // ROLE != 2
 
   asm volatile("cp.async.wait_all;" ::: "memory");  // staged buckets: nothing in flight
-  // ---- results
-  tpot_sum = warp_sum_f64(tpot_sum);
-  tpot_n = warp_sum_i64(tpot_n);
-  l_done = warp_sum_i64(l_done);
-  l_cw = warp_sum_i64(l_cw);
-  l_wr = warp_sum_i64(l_wr);
-  l_ttft = warp_sum_i64(l_ttft);
-  l_sched = warp_sum_i64(l_sched);
-  l_dev = warp_sum_i64(l_dev);
+  // ---- results (completion-derived fields: finalize_kernel)
 #ifdef SBS_PROF
   if (ROLE == 0) prof_acc[21] += clock64() - prof_t0;
 #endif
   __syncwarp();
   if (ROLE != 0) {
     if (lane == 0) {
-      cn->completed = l_done; cn->cw = l_cw; cn->wr = l_wr;
-      cn->ttft = l_ttft; cn->sched = l_sched; cn->dev = l_dev;
-      cn->n_ttft = n_ttft; cn->tpot_n = tpot_n; cn->tpot = tpot_sum; cn->err = error;
+      cn->err = error;
 #ifdef SBS_PROF
       for (int i = 0; i < 24; ++i) atomicAdd((unsigned long long*)&res.prof[i], (unsigned long long)prof_acc[i]);
 #endif
@@ -1946,10 +1868,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     return;
   }
   if (lane == 0) {
-    res.completed = l_done;
     res.throttled = cn->throttled;
-    res.cw = l_cw;
-    res.wr = l_wr;
     res.passes = cn->passes;
     res.steps = cn->steps;
     res.out_tokens = cn->outtok;
@@ -1963,16 +1882,10 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     res.alloc_calls = cn->alloc;
     res.dec_selects = cn->dsel;
     res.events = cn->events;
-    res.n_ttft = n_ttft;
-    res.ttft_sum = l_ttft;
-    res.sched_sum = l_sched;
-    res.dev_sum = l_dev;
     res.util_sum = cn->util;
     res.kv_mean_sum = cn->kv_mean;
     res.kv_sigma_sum = cn->kv_sig;
-    res.tpot_sum = tpot_sum / 1e9;
     res.kv_n = cn->kv_n;
-    res.tpot_n = tpot_n;
     res.log_n = log_n;
     res.error = error;
 #ifdef SBS_PROF
@@ -2003,15 +1916,11 @@ __global__ void __launch_bounds__(128) des_kernel(const DevPoint* __restrict__ p
   }
 }
 
-// Channel reset before a replica (one warp).  Completion-ring entries get a
-// lap tag no live position carries, so nothing left from an earlier replica
-// reads as a published entry.
+// Channel reset before a replica (one warp).
 __device__ void chan_init(Chan* ch, int lane) {
-  for (int i = lane; i < kChanComp; i += 32) ch->comp_id[i] = (long long)(0xFFFFull << 48);
   if (lane == 0) {
     ch->p_done = 0;
     ch->tail = 0; ch->head = 0; ch->ktail = 0; ch->khead = 0; ch->abort = 0;
-    ch->ctail = 0; ch->chead = 0; ch->d_done = 0;
   }
   __syncwarp();
 }
@@ -2021,22 +1930,10 @@ __device__ void chan_init(Chan* ch, int lane) {
 __device__ void combine_pair(const DevPoint& pt, DevResult& res, const Counters* a,
                              const Counters* b) {
   const int lane = lane_id();
-  // decode-warp TTFTs were written from the top of the buffer: move them
-  // down behind the prefill warp's (the finalize select reads [0, n))
-  const int64_t na = a->n_ttft, nb = b->n_ttft, N = pt.n_dev ? *pt.n_dev : pt.N;
-  for (int64_t base = 0; base < nb; base += 32) {
-    const int64_t i = base + lane;
-    const int64_t v = i < nb ? pt.ttft[N - nb + i] : 0;
-    __syncwarp();
-    if (i < nb) pt.ttft[na + i] = v;
-    __syncwarp();
-  }
+  (void)pt;
   if (lane == 0) {
     DevResult& r = res;
-    r.completed = a->completed + b->completed;
     r.throttled = a->throttled;
-    r.cw = a->cw + b->cw;
-    r.wr = a->wr + b->wr;
     r.passes = a->passes;
     r.steps = b->steps;
     r.out_tokens = b->outtok;
@@ -2050,16 +1947,10 @@ __device__ void combine_pair(const DevPoint& pt, DevResult& res, const Counters*
     r.alloc_calls = a->alloc;
     r.dec_selects = b->dsel;
     r.events = a->events + b->events;
-    r.n_ttft = na + nb;
-    r.ttft_sum = a->ttft + b->ttft;
-    r.sched_sum = a->sched + b->sched;
-    r.dev_sum = a->dev + b->dev;
     r.util_sum = a->util;
     r.kv_mean_sum = b->kv_mean;
     r.kv_sigma_sum = b->kv_sig;
-    r.tpot_sum = (a->tpot + b->tpot) / 1e9;
     r.kv_n = b->kv_n;
-    r.tpot_n = a->tpot_n + b->tpot_n;
     r.log_n = 0;
     const long long e = b->err ? b->err : a->err;
     r.error = (int)e;
@@ -2152,22 +2043,117 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------
-// Finalize: exact TTFT order statistics (percentile, decode_alloc.cpp:13-23,
-// as used by metrics.cpp:151-152) by 8-bit MSB radix select over the replica's
-// window TTFT buffer, four ranks at once, plus the log2 TTFT histogram.
-// One CTA per replica.
+// Finalize (MetricsCollector::finalize, metrics.cpp:103-190), one CTA per
+// replica, after the event loops.  Deferred accounting: the loops only stamp
+// per-request times; this kernel derives every completion-based field from
+// the per-request arrays in one coalesced pass over the trace —
+//   completed / completed-in-window counts (metrics.cpp:117-121, 174-176),
+//   window TTFT / scheduler / device sums over completed requests with
+//   arrival >= warmup (metrics.cpp:122-136; exact int64 ns),
+//   TPOT = (completion - first_token) / (output_len - 1) per completed decode
+//   request (one IEEE division; not in the reference), its FP64 sum in a fixed
+//   thread/tree order and its log2 histogram,
+// and compacts the window TTFTs into the replica's buffer; then the exact
+// p50/p95 order statistics (percentile, decode_alloc.cpp:13-23, as used by
+// metrics.cpp:151-152) by 8-bit MSB radix select, four ranks at once, plus
+// the log2 TTFT histogram.
 // ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) reset_kernel(const DevPoint* __restrict__ pts, int n_pts) {
+  // completion stamps of every replica := -1 (unset), one launch for all
+  for (int pi = blockIdx.y; pi < n_pts; pi += gridDim.y) {
+    const DevPoint& pt = pts[pi];
+    const int64_t n = pt.N;
+    int4* c = (int4*)pt.o_comp;  // 256-byte aligned carve
+    const int64_t n16 = n >> 1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
+      c[i] = make_int4(-1, -1, -1, -1);
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) pt.o_comp[n - 1] = -1;
+  }
+}
+
 __global__ void __launch_bounds__(256) finalize_kernel(const DevPoint* __restrict__ pts,
                                                        DevResult* __restrict__ res) {
   const DevPoint& pt = pts[blockIdx.x];
   DevResult& r = res[blockIdx.x];
-  const int64_t n = r.n_ttft;
   __shared__ unsigned int hist[4][256];
   __shared__ unsigned long long hbin[kHistBins];
+  __shared__ unsigned long long tbin[kHistBins];
   __shared__ uint64_t prefix[4];
   __shared__ int64_t want[4];
-  const int tid = threadIdx.x;
-  if (tid < kHistBins) hbin[tid] = 0;
+  __shared__ long long red[8][7];
+  __shared__ double redf[8];
+  __shared__ unsigned long long n_win;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid < kHistBins) { hbin[tid] = 0; tbin[tid] = 0; }
+  if (tid == 0) n_win = 0;
+  __syncthreads();
+
+  // ---- pass 1: completion-derived sums (deferred accounting)
+  {
+    const int64_t N = pt.n_dev ? *pt.n_dev : pt.N;
+    const int64_t warmup = pt.warmup;
+    const int64_t* __restrict__ comp = pt.o_comp;
+    long long done = 0, cw = 0, wr = 0, s_ttft = 0, s_sched = 0, s_dev = 0, tpn = 0;
+    double tps = 0.0;
+    for (int64_t b0 = 0; b0 < N; b0 += blockDim.x) {  // warp-uniform trip count (ballot below)
+      const int64_t i = b0 + tid;
+      const int64_t c = i < N ? comp[i] : -1;
+      const bool has = c >= 0;
+      int64_t ttft = 0;
+      bool win = false;
+      if (has) {
+        done += 1;
+        cw += c >= warmup;
+        const int64_t arr = __ldg(pt.arr + i), ft = pt.o_ftok[i];
+        const int32_t out = __ldg(pt.output + i);
+        if (arr >= warmup) {
+          const int64_t disp = pt.o_dispatch[i], ps = pt.o_pstart[i];
+          win = true;
+          ttft = ft - arr;
+          wr += 1;
+          s_ttft += ttft;
+          s_sched += disp - arr;
+          s_dev += ps - disp;
+        }
+        if (out > 1) {
+          const double per = __ddiv_rn((double)(c - ft), (double)(out - 1));
+          tps = __dadd_rn(tps, per);
+          tpn += 1;
+          atomicAdd(&tbin[hist_bin((int64_t)per)], 1ull);
+        }
+      }
+      // compact the window TTFTs (their order is irrelevant to the select)
+      const unsigned m = __ballot_sync(kFull, win);
+      unsigned long long base = 0;
+      if (lane == __ffs(m) - 1) base = atomicAdd(&n_win, (unsigned long long)__popc(m));
+      base = __shfl_sync(kFull, base, m ? __ffs(m) - 1 : 0);
+      if (win) pt.ttft[base + __popc(m & ((1u << lane) - 1u))] = ttft;
+    }
+    long long v[7] = {done, cw, wr, s_ttft, s_sched, s_dev, tpn};
+#pragma unroll
+    for (int k = 0; k < 7; ++k) v[k] = warp_sum_i64(v[k]);
+    tps = warp_sum_f64(tps);
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < 7; ++k) red[wid][k] = v[k];
+      redf[wid] = tps;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      long long t[7] = {0, 0, 0, 0, 0, 0, 0};
+      double f = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        for (int k = 0; k < 7; ++k) t[k] += red[w][k];
+        f = __dadd_rn(f, redf[w]);
+      }
+      r.completed = t[0]; r.cw = t[1]; r.wr = t[2]; r.n_ttft = t[2];
+      r.ttft_sum = t[3]; r.sched_sum = t[4]; r.dev_sum = t[5];
+      r.tpot_n = t[6]; r.tpot_sum = f / 1e9;
+    }
+    if (tid < kHistBins) pt.tpot_hist[tid] = (int64_t)tbin[tid];
+  }
+  __syncthreads();
+  const int64_t n = (int64_t)n_win;
   if (tid < 4) {
     prefix[tid] = 0;
     int64_t k = 0;
@@ -2339,6 +2325,11 @@ cudaError_t launch_gather(const CopySeg* d_segs, int n_segs, int64_t n_blocks, c
 cudaError_t launch_finalize(const DevPoint* d_pts, int n_pts, DevResult* d_res, cudaStream_t st) {
   if (n_pts == 0) return cudaSuccess;
   finalize_kernel<<<n_pts, 256, 0, st>>>(d_pts, d_res);
+  return cudaGetLastError();
+}
+cudaError_t launch_reset(const DevPoint* d_pts, int n_pts, cudaStream_t st) {
+  if (n_pts == 0) return cudaSuccess;
+  reset_kernel<<<dim3(16, n_pts < 65535 ? n_pts : 65535), 256, 0, st>>>(d_pts, n_pts);
   return cudaGetLastError();
 }
 }  // namespace sbs

@@ -25,9 +25,8 @@ constexpr int kSmemWinKeys = 256;   // window keys kept in shared memory
 constexpr int kHistBins = 64;
 constexpr int kChanRecs = 32;       // prefill->decode hand-off records in flight
 constexpr int kChanKeys = 1024;     // hand-off waiter keys in flight
-constexpr int kChanComp = 256;
-constexpr int kMaxProbes = 32;
-constexpr int kStageEntries = 32;   // completion-bucket entries staged in smem per decode step      // distinct prefix-cache probe lengths      // decode completions returned to the prefill warp
+constexpr int kMaxProbes = 32;      // distinct prefix-cache probe lengths
+constexpr int kStageEntries = 32;   // completion-bucket entries staged in smem per decode step
 constexpr int kErrSplitTie = 7;     // two-warp replica met an unresolvable tie: rerun serially
 
 // Prefill-warp -> decode-warp hand-off channel of a two-warp replica (shared
@@ -47,14 +46,9 @@ struct Chan {
   volatile int tail, head;    // records written / consumed
   volatile int ktail, khead;  // keys written / consumed
   volatile int abort;         // decode warp met an unresolvable tie
-  volatile int ctail, chead;  // decode completions written / accounted
-  volatile int d_done;        // decode warp finished (all completions published)
-  int n_ttft_p;               // prefill warp's TTFT appends
-  long long part[16];         // prefill warp's partial results
+  int pad_;
   ChanRec rec[kChanRecs];
   unsigned long long keys[kChanKeys];
-  long long comp_id[kChanComp];  // completion accounting is done by the prefill warp
-  long long comp_t[kChanComp];
 };
 
 enum Policy : int32_t { kSbs = 0, kImmediate = 1, kRoundRobin = 2, kLeastOutstanding = 3 };
@@ -72,6 +66,12 @@ struct DevPoint {
   int32_t per_request;      // parity mode: also write completion + status
   int32_t split;            // run as a prefill warp + decode warp pair
   int32_t log_kv_loads;     // run records also keep the per-unit KV loads per step
+  // decode waiter key (simulation.cpp:446-453 order): (kq_lmax - len) << (kq_ib + kq_ob)
+  // | id << kq_ob | output_len, ascending == (prompt+output desc, id asc); the
+  // low field carries output_len (prompt = len - output) so the decode side
+  // never reads the trace.  kq_ob = 0 (no room): 32-bit fields, lengths loaded.
+  int32_t kq_ob, kq_ib;
+  uint32_t kq_lmax;
   int32_t _pad0;
   // ---- constants (integer ns, FP64 engine coefficients)
   int64_t c_chunk, t_default, l_net, tps, horizon, warmup;

@@ -38,6 +38,7 @@ cudaError_t launch_des(int variant, const DevPoint* d_pts, int n_pts, int* d_cou
 cudaError_t launch_des_cluster(int variant, const DevPoint* d_pts, int n_pts, DevResult* d_res,
                                int smem_per_rep, cudaStream_t st);
 cudaError_t launch_finalize(const DevPoint* d_pts, int n_pts, DevResult* d_res, cudaStream_t st);
+cudaError_t launch_reset(const DevPoint* d_pts, int n_pts, cudaStream_t st);
 struct CopySeg {
   const unsigned char* src;
   unsigned char* dst;
@@ -362,6 +363,7 @@ struct TraceDev {
   int32_t* psize1 = nullptr;
   int64_t n = 0;              // length (host traces) or capacity (generated traces)
   int32_t max_output = 0;
+  int32_t max_prompt = 0;
   int32_t n_pools = 0;       // 1 + max pool id
   int64_t max_psize = 0;
   uint64_t digest = 0;
@@ -492,6 +494,7 @@ int64_t length_bound(const sbs_length_spec& l, bool output) {
 // arenas of a generated trace are sized by (a host trace uses its own maxima).
 void bound_trace_shape(TraceDev& t, const sbs_workload& w) {
   t.max_output = (int32_t)std::min<int64_t>(std::max<int64_t>(0, length_bound(w.output, true)), 0x3fffffff);
+  t.max_prompt = (int32_t)std::min<int64_t>(std::max<int64_t>(0, length_bound(w.prompt, false)), 0x3fffffff);
   if (w.shared_prefix_fraction > 0) {
     t.n_pools = w.prefix_pool;
     t.max_psize = std::max<int64_t>(0, std::min<int64_t>(w.prefix_len, length_bound(w.prompt, false)));
@@ -586,6 +589,19 @@ void build_point(sbs_sim& s, PointHost& p) {
   int64_t max_steps = (max_target + c.decode_tokens_per_step - 1) / c.decode_tokens_per_step;
   d.R = (int32_t)next_pow2(max_steps + 1);
   if ((int64_t)d.R * d.Dn > (1 << 16)) throw Error{SBS_ERR_CONFIG, "decode ring too large"};
+  // decode waiter key fields: length bits + id bits + output bits <= 64, else
+  // the unpacked 32/32 layout (output and prompt then read from the trace)
+  {
+    auto bits = [](int64_t v) { int b = 0; while (b < 63 && (v >> b) != 0) ++b; return b; };
+    const int64_t lmax = (int64_t)t.max_prompt + t.max_output;
+    const int lb = bits(lmax), ib = std::max(1, bits(std::max<int64_t>(t.n, 1) - 1)),
+              ob = std::max(1, bits(t.max_output));
+    if (lb + ib + ob <= 64 && lmax <= 0xffffffffLL) {
+      d.kq_ob = ob; d.kq_ib = ib; d.kq_lmax = (uint32_t)lmax;
+    } else {
+      d.kq_ob = 0; d.kq_ib = 32; d.kq_lmax = 0xffffffffu;
+    }
+  }
 
   // faults: deaths (min over entries), topology sorted by (time, order), drops
   const int n_inst = d.P + d.Dn;
@@ -650,7 +666,7 @@ void build_point(sbs_sim& s, PointHost& p) {
     return o;
   };
   size_t o_disp = carve(8 * N), o_ps = carve(8 * N), o_ft = carve(8 * N);
-  size_t o_comp = d.per_request ? carve(8 * N) : 0;
+  size_t o_comp = carve(8 * N);  // completion stamps (finalize_kernel reads them)
   size_t o_st = d.per_request ? carve(N) : 0;
   size_t o_ttft = carve(8 * N);
   size_t o_pk0 = carve(8 * (size_t)p.QP), o_pk1 = carve(8 * (size_t)p.QP);
@@ -677,7 +693,7 @@ void build_point(sbs_sim& s, PointHost& p) {
   d.o_dispatch = (int64_t*)(b + o_disp);
   d.o_pstart = (int64_t*)(b + o_ps);
   d.o_ftok = (int64_t*)(b + o_ft);
-  d.o_comp = d.per_request ? (int64_t*)(b + o_comp) : nullptr;
+  d.o_comp = (int64_t*)(b + o_comp);
   d.o_status = d.per_request ? (int8_t*)(b + o_st) : nullptr;
   d.ttft = (int64_t*)(b + o_ttft);
   d.pend_key[0] = (uint64_t*)(b + o_pk0);
@@ -703,7 +719,6 @@ void build_point(sbs_sim& s, PointHost& p) {
 // Per-run reset of the parts of the arena the kernel reads before writing.
 void reset_point(const PointHost& p, cudaStream_t st) {
   const sbs::DevPoint& d = p.dp;
-  CUDA_OR_THROW(cudaMemsetAsync(d.tpot_hist, 0, 8 * sbs::kHistBins, st));
   if (d.cache_on) {  // empty prefix caches
     const size_t PD = (size_t)d.P * d.D;
     CUDA_OR_THROW(cudaMemsetAsync(d.c_stamp, 0, 4 * PD * (size_t)d.n_pools * d.n_probes, st));
@@ -714,7 +729,6 @@ void reset_point(const PointHost& p, cudaStream_t st) {
     CUDA_OR_THROW(cudaMemsetAsync(d.o_dispatch, 0xff, 8 * (size_t)d.N, st));
     CUDA_OR_THROW(cudaMemsetAsync(d.o_pstart, 0xff, 8 * (size_t)d.N, st));
     CUDA_OR_THROW(cudaMemsetAsync(d.o_ftok, 0xff, 8 * (size_t)d.N, st));
-    CUDA_OR_THROW(cudaMemsetAsync(d.o_comp, 0xff, 8 * (size_t)d.N, st));
     CUDA_OR_THROW(cudaMemsetAsync(d.o_status, 0, (size_t)d.N, st));
   }
 }
@@ -790,6 +804,10 @@ void launch_all(sbs_sim& s, cudaStream_t st) {
     total_blocks += (n + per - 1) / per;
   }
   const int min_smem = total_blocks <= s.sm_count ? 116 * 1024 : 0;
+  // completion stamps := unset, every replica in one launch (finalize_kernel
+  // derives the completion-based aggregates from them)
+  CUDA_OR_THROW(sbs::launch_reset(dp, (int)s.order.size(), st));
+  s.n_launches += 1;
   CUDA_OR_THROW(cudaEventRecord(s.ev_des[0], st));
   int used[sbs_sim::kVariants] = {};
   for (int v = 0; v < sbs_sim::kVariants; ++v) {
@@ -926,11 +944,13 @@ void check_reupload(const TraceDev& t, const sbs_trace& tr) {
   if (tr.n != t.n) throw Error{SBS_ERR_CONFIG, "trace shape changed (length)"};
   if ((tr.prefix_pool_id != nullptr) != (t.pool != nullptr))
     throw Error{SBS_ERR_CONFIG, "trace shape changed (shared prefixes)"};
-  int32_t mo = 0;
+  int32_t mo = 0, mp = 0;
   for (int64_t k = 0; k < tr.n; ++k) mo = std::max(mo, tr.output_len[k]);
-  if (mo > t.max_output)
-    throw Error{SBS_ERR_CONFIG, "re-uploaded trace has longer outputs than the one the simulator was "
-                                "created with (decode completion ring); create a new simulator"};
+  for (int64_t k = 0; k < tr.n; ++k) mp = std::max(mp, tr.prompt_len[k]);
+  if (mo > t.max_output || mp > t.max_prompt)
+    throw Error{SBS_ERR_CONFIG, "re-uploaded trace has longer prompts or outputs than the one the "
+                                "simulator was created with (completion ring, waiter keys); create a "
+                                "new simulator"};
   if (tr.prefix_pool_id != nullptr) {
     for (int64_t k = 0; k < tr.n; ++k) {
       const int32_t pid = tr.prefix_pool_id[k], ps = tr.prefix_size[k];
@@ -1274,6 +1294,7 @@ int sbs_sim_create(const sbs_experiment* points, int32_t n_points, const sbs_tra
       t.digest = traces[i].digest;
       if (t.n >= (int64_t)1 << 31) throw Error{SBS_ERR_CONFIG, "trace longer than 2^31 requests"};
       for (int64_t k = 0; k < t.n; ++k) t.max_output = std::max(t.max_output, traces[i].output_len[k]);
+      for (int64_t k = 0; k < t.n; ++k) t.max_prompt = std::max(t.max_prompt, traces[i].prompt_len[k]);
       const bool prefixes = traces[i].prefix_pool_id != nullptr && traces[i].prefix_size != nullptr;
       if (prefixes) {
         for (int64_t k = 0; k < t.n; ++k) {

@@ -15,8 +15,8 @@ c = sim.profile_counters()
 n = sum(r["generated"] for r in res)
 names = ["select", "arrival", "finish_pass", "finish_step", "drain", "iqr_select", "S_update",
          "rebuild_S", "try_start_pass", "dispatch_chain", "begin_step", "fs.completers",
-         "fs.unit_loop", "fs.reduce", "fs.band", "D.drain_after_step", "D.wait_P", "P.wait_recroom",
-         "D.wait_comproom", "P.consume", "D.total", "P.total", "sum_np_per_dispatch", "sum_nn"]
+         "fs.unit_loop", "fs.reduce", "fs.band", "D.n_drains_with_waiters", "D.wait_P", "P.wait_recroom",
+         "D.n_sorts", "P.consume", "D.total", "P.total", "sum_np_per_dispatch", "sum_nn"]
 ev = sum(r["events"] for r in res)
 steps = sum(r["decode_steps"] for r in res)
 print("steps/request %.3f (post-warmup)" % (steps / n))
