@@ -581,7 +581,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     }
     S_gathered = false;
     __syncwarp();
-    warp_radix_sort<uint32_t>(s_S, s_T, s_hist, nul, mx ? 64 - __clzll((long long)mx) : 0);
+    if (nul <= 64) warp_sort_reg_u32<2>(s_S, nul, lane);
+    else if (nul <= 512) warp_sort_reg_u32<16>(s_S, nul, lane);
+    else warp_radix_sort<uint32_t>(s_S, s_T, s_hist, nul, mx ? 64 - __clzll((long long)mx) : 0, lane, lt_mask);
     S_valid = true;
   };
 
@@ -690,15 +692,24 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   // S multiset: replace one copy of `oldv` by `newv` (> oldv).
   auto S_update = [&](uint64_t oldv, uint64_t newv) {
     const uint32_t o = (uint32_t)oldv, nv = (uint32_t)newv;
-    const int c_old = warp_lower_bound<uint32_t>(s_S, nul, o);
-    const int c_new = warp_lower_bound<uint32_t>(s_S, nul, nv);
-    // shift S[c_old+1 .. c_new-1] left by one, then S[c_new-1] = newv
+    int c_old, c_new;
+    warp_lower_bound2<uint32_t>(s_S, nul, o, nv, lane, c_old, c_new);
+    // shift S[c_old+1 .. c_new-1] left by one (128 per round: every load of a
+    // round is issued before its stores), then S[c_new-1] = newv
 #pragma unroll 1
-    for (int base = c_old; base < c_new - 1; base += 32) {
-      int i = base + lane;
-      uint32_t v = (i < c_new - 1) ? s_S[i + 1] : 0;
+    for (int base = c_old; base < c_new - 1; base += 128) {
+      uint32_t v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = base + lane + 32 * q;
+        v[q] = i < c_new - 1 ? s_S[i + 1] : 0u;
+      }
       __syncwarp();
-      if (i < c_new - 1) s_S[i] = v;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = base + lane + 32 * q;
+        if (i < c_new - 1) s_S[i] = v[q];
+      }
       __syncwarp();
     }
     if (lane == 0) s_S[c_new - 1] = nv;
@@ -719,7 +730,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     prof_acc[15] += 1;  // drains with waiters
 #endif
     for (int j = 0; j < Dn; ++j) maybe_die_d(j);
-    if (!wreg) warp_sort_buf<true>(g_dwait, ndw);
+    if (!wreg) warp_sort_buf<true>(g_dwait, ndw, lane);
     int wi = 0;
     int64_t w_id = 0;
     int32_t w_prompt = 0, w_out = 0;
@@ -1018,7 +1029,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       nk[i] = pbaa_key(__ldg(g_prompt + id), id);
     }
     __syncwarp();
-    warp_sort_buf(nk, nn);
+    warp_sort_buf(nk, nn, lane);
     uint64_t* pk = pt.pend_key[pcur];
     int32_t* pw = pt.pend_wait[pcur];
 #ifdef SBS_PROF
@@ -1342,32 +1353,41 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     // every stamped resident produced tps tokens (minus the last-step excess
     // of completers); completers release B and prompt + decode_done of K
     const bool gather = ul_ident && Dn == 1;  // s_S order == unit order
-    uint64_t mx = 0, s1 = 0, s2lo = 0, s2hi = 0;  // sum K, sum K^2 (128-bit)
+    // 32-bit unit arithmetic: K < 2^32 (decode-unit envelope, checked here:
+    // a carry out of K + tps * stamped sets kErrEnvelope), B < 2^15, and
+    // tps * stamped < 2^32 (tps < 2^17, host check)
+    uint32_t mx = 0, ovf = 0;
+    uint64_t s1 = 0, s2lo = 0, s2hi = 0;  // sum K, sum K^2 (128-bit)
     const bool band_fast = !LOG && Dn == 1 && now >= warmup;
     double worst = 0.0;
     uint64_t lm = UINT64_MAX;
+    const uint32_t tps32 = (uint32_t)tps;
 #pragma unroll 1
     for (int d = lane; d < Dd; d += 32) {
       const int u = u0 + d;
       const uint64_t k = s_PK[u];
       const uint64_t r = s_R[u];
-      const int32_t st = s_nst[u];
-      const uint64_t K = (k & kKMask) + (uint64_t)(tps * st) - (r & kKMask);
-      const uint64_t B = (k >> 48) - (r >> 48);
-      s_PK[u] = (B << 48) | K;
-      const uint64_t c = (B << 48) | (K << 16) | (uint64_t)u;
+      const uint32_t st = (uint32_t)s_nst[u];
+      const uint32_t kk = (uint32_t)k, rk = (uint32_t)r;
+      const uint32_t grown = kk + tps32 * st;
+      ovf |= grown < kk;
+      const uint32_t K = grown - rk;
+      const uint32_t B = (uint32_t)(k >> 48) - (uint32_t)(r >> 48);
+      s_PK[u] = ((uint64_t)B << 48) | K;
+      const uint64_t c = ((uint64_t)((B << 16) | (K >> 16)) << 32) | ((K << 16) | (uint32_t)u);
       lm = c < lm ? c : lm;
       s_nst[u] = (int32_t)B;
       if (r) s_R[u] = 0;
-      if (gather) s_S[u] = (uint32_t)K;
+      if (gather) s_S[u] = K;
       mx = K > mx ? K : mx;
       s1 += K;
-      const uint64_t k2 = K * K;  // K < 2^32 (decode-unit envelope)
+      const uint64_t k2 = (uint64_t)K * K;
       s2lo += k2;
       s2hi += s2lo < k2;
       double t = __dadd_rn(__dmul_rn(dc_req, (double)B), __dmul_rn(dc_kv, (double)K));
       worst = t > worst ? t : worst;
     }
+    if (SBS_UNLIKELY(__any_sync(kFull, ovf != 0))) error = kErrEnvelope;
     PROF_END(12);
     PROF_BEGIN(13);
     // per-step reductions as independent 32-bit REDUX: the step time's max
@@ -1406,7 +1426,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     lmin_ok = dec_policy == kIqr && Dn == 1 && U <= 1024 && ul_ident && !ul_dirty;
     if (gather) {
       S_gathered = true;
-      S_mx = (uint64_t)__reduce_max_sync(kFull, (uint32_t)mx);
+      S_mx = (uint64_t)__reduce_max_sync(kFull, mx);
     }
     if (cap_batch > 0 && n > 0) ul_dirty = true;
     __syncwarp();
@@ -1596,7 +1616,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         if (ndw == 0 && nk <= 32) {
           // the usual case: this record's waiters only, sorted in registers
           rkey = lane < nk ? chL->keys[(k0 + lane) % kChanKeys] : UINT64_MAX;
-          if (nk > 1) rkey = warp_sort32<true>(rkey);
+          if (nk > 1) rkey = warp_sort32<true>(rkey, lane);
           wreg = true;
         } else {
 #pragma unroll 1

@@ -322,6 +322,7 @@ void validate(const sbs_experiment& x) {
           "GPU path supports at most 32 prefill and 32 decode instances");
   require(c.dp_degree <= sbs::kMaxPrefillDp, "GPU path supports dp_degree <= 128");
   require(c.c_chunk <= 0x7fffffff, "GPU path supports c_chunk < 2^31");
+  require(c.decode_tokens_per_step < (1 << 17), "GPU path supports decode_tokens_per_step < 2^17");
   require(c.w_size <= sbs::kMaxWSize, "GPU path supports w_size <= 1024");
   require(x.policy >= 0 && x.policy <= 3, "scheduler.policy out of range");
   require(x.decode_policy >= 0 && x.decode_policy <= 2, "scheduler.decode_policy out of range");

@@ -85,9 +85,10 @@ __device__ __forceinline__ uint64_t bitonic_step(uint64_t x, int lane, int k, in
   const uint64_t mn = x < y ? x : y, mx = x < y ? y : x;
   return take_min ? mn : mx;
 }
+// (callers that hold the lane index pass it: lane_id() is an S2R whose
+// latency shows up when the compiler rematerialises it inside hot loops)
 template <bool ROLLED = false>
-__device__ __forceinline__ uint64_t warp_sort32(uint64_t x) {
-  const int lane = lane_id();
+__device__ __forceinline__ uint64_t warp_sort32(uint64_t x, int lane) {
   if constexpr (ROLLED) {
 #pragma unroll 1
     for (int k = 2; k <= 32; k <<= 1)
@@ -101,16 +102,17 @@ __device__ __forceinline__ uint64_t warp_sort32(uint64_t x) {
   }
   return x;
 }
+template <bool ROLLED = false>
+__device__ __forceinline__ uint64_t warp_sort32(uint64_t x) { return warp_sort32<ROLLED>(x, lane_id()); }
 
 // Warp bitonic sort of n keys (ascending) in a buffer of capacity >= pow2(n)
 // (generic pointer: shared or global).  Pads with UINT64_MAX.
 template <bool ROLLED = false>
-__device__ __forceinline__ void warp_sort_buf(uint64_t* buf, int n) {
-  const int lane = lane_id();
+__device__ __forceinline__ void warp_sort_buf(uint64_t* buf, int n, int lane) {
   if (n <= 1) return;
   if (n <= 32) {
     uint64_t x = lane < n ? buf[lane] : UINT64_MAX;
-    x = warp_sort32<ROLLED>(x);
+    x = warp_sort32<ROLLED>(x, lane);
     if (lane < n) buf[lane] = x;
     __syncwarp();
     return;
@@ -136,6 +138,8 @@ __device__ __forceinline__ void warp_sort_buf(uint64_t* buf, int n) {
     }
   }
 }
+template <bool ROLLED = false>
+__device__ __forceinline__ void warp_sort_buf(uint64_t* buf, int n) { warp_sort_buf<ROLLED>(buf, n, lane_id()); }
 
 // lower_bound over a sorted buffer (all lanes may search different keys).
 __device__ __forceinline__ int lower_bound_u64(const uint64_t* a, int n, uint64_t key) {
@@ -158,9 +162,8 @@ namespace sbs {
 // __match_any_sync groups equal digits and popc(peers & lanemask_lt) ranks
 // each key inside its group.
 template <typename Key>
-__device__ __forceinline__ void warp_radix_sort(Key* a, Key* t, uint32_t* hist, int n, int nbits) {
-  const int lane = lane_id();
-  const unsigned lt = lanemask_lt();
+__device__ __forceinline__ void warp_radix_sort(Key* a, Key* t, uint32_t* hist, int n, int nbits, int lane,
+                                                unsigned lt) {
   const int passes = (nbits + 7) >> 3;
   Key* src = a;
   Key* dst = t;
@@ -210,6 +213,75 @@ __device__ __forceinline__ void warp_radix_sort(Key* a, Key* t, uint32_t* hist, 
   }
 }
 
+// Ascending sort of n <= 32*KP uint32 keys a[0..n) (shared memory) by one
+// warp in registers: lane l holds positions KP*l .. KP*l+KP-1 (padding
+// 0xffffffff) and a bitonic network runs over all 32*KP positions.  Phases up
+// to KP stay inside a lane (register compare-exchanges); later phases
+// exchange whole registers with the partner lane (one shuffle + one min/max
+// per register), then finish inside the lane.  A descending block is merged
+// as an ascending one on complemented keys (bitonic sequences stay bitonic),
+// so every compare-exchange is a plain min/max pair.  Replaces two 8-bit
+// radix passes (smem histogram + match_any scatter per 32 keys) for the
+// sorted-K multiset of <= 512 decode units.
+template <int KP>
+__device__ __forceinline__ void warp_sort_reg_u32(uint32_t* a, int n, int lane) {
+  static_assert(KP >= 2 && KP <= 16 && (KP & (KP - 1)) == 0, "KP: power of two in [2, 16]");
+  uint32_t x[KP];
+#pragma unroll
+  for (int i = 0; i < KP; ++i) {
+    const int p = KP * lane + i;
+    x[i] = p < n ? a[p] : 0xffffffffu;
+  }
+  auto cas_up = [&](uint32_t& lo, uint32_t& hi) {
+    const uint32_t a0 = lo, b0 = hi;
+    lo = a0 < b0 ? a0 : b0;
+    hi = a0 < b0 ? b0 : a0;
+  };
+  // phases k < KP: directions follow the register index only
+#pragma unroll
+  for (int k = 2; k < KP; k <<= 1)
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+      for (int i = 0; i < KP; ++i)
+        if ((i & j) == 0) {
+          if ((i & k) == 0) cas_up(x[i], x[i | j]);
+          else cas_up(x[i | j], x[i]);
+        }
+  // phases k >= KP: direction per lane ((KP*lane) & k), first the cross-lane
+  // stages (j >= KP), then the in-lane ones
+#pragma unroll 1
+  for (int k = KP; k <= 32 * KP; k <<= 1) {
+    const uint32_t flip = ((KP * lane) & k) ? 0xffffffffu : 0u;
+#pragma unroll
+    for (int i = 0; i < KP; ++i) x[i] ^= flip;
+#pragma unroll 1
+    for (int j = k >> 1; j >= KP; j >>= 1) {
+      const int m = j / KP;
+      const bool lower = (lane & m) == 0;
+#pragma unroll
+      for (int i = 0; i < KP; ++i) {
+        const uint32_t y = __shfl_xor_sync(kFull, x[i], m);
+        x[i] = lower ? (x[i] < y ? x[i] : y) : (x[i] < y ? y : x[i]);
+      }
+    }
+#pragma unroll
+    for (int j = KP >> 1; j > 0; j >>= 1)
+#pragma unroll
+      for (int i = 0; i < KP; ++i)
+        if ((i & j) == 0) cas_up(x[i], x[i | j]);
+#pragma unroll
+    for (int i = 0; i < KP; ++i) x[i] ^= flip;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < KP; ++i) {
+    const int p = KP * lane + i;
+    if (p < n) a[p] = x[i];
+  }
+  __syncwarp();
+}
+
 }  // namespace sbs
 
 namespace sbs {
@@ -217,8 +289,7 @@ namespace sbs {
 // Number of elements < x in a sorted array (a lower bound), by a warp: one
 // 32-ary partition round per 32x narrowing, then a ballot over the last <= 32.
 template <typename Key>
-__device__ __forceinline__ int warp_lower_bound(const Key* a, int n, Key x) {
-  const int lane = lane_id();
+__device__ __forceinline__ int warp_lower_bound(const Key* a, int n, Key x, int lane) {
   int lo = 0, hi = n;  // answer in [lo, hi]
   while (hi - lo > 32) {
     const int step = (hi - lo + 31) >> 5;
@@ -233,6 +304,40 @@ __device__ __forceinline__ int warp_lower_bound(const Key* a, int n, Key x) {
   }
   const int idx = lo + lane;
   return lo + __popc(__ballot_sync(kFull, idx < hi && a[idx] < x));
+}
+
+// Two lower bounds over one sorted array (x0 < x1) with shared probe rounds:
+// one 32-ary pivot round serves both keys, then lanes 0-15 finish x0 and lanes
+// 16-31 finish x1 when each window holds <= 16 elements (n <= 512); larger
+// arrays take two single searches.
+template <typename Key>
+__device__ __forceinline__ void warp_lower_bound2(const Key* a, int n, Key x0, Key x1, int lane, int& r0,
+                                                  int& r1) {
+  if (n > 512) {
+    r0 = warp_lower_bound<Key>(a, n, x0, lane);
+    r1 = warp_lower_bound<Key>(a, n, x1, lane);
+    return;
+  }
+  int lo0 = 0, hi0 = n, lo1 = 0, hi1 = n;
+  if (n > 16) {
+    const int step = (n + 31) >> 5;  // <= 16
+    const int idx = lane * step;
+    const Key v = idx < n ? a[idx] : Key(0);
+    const int k0 = __popc(__ballot_sync(kFull, idx < n && v < x0));
+    const int k1 = __popc(__ballot_sync(kFull, idx < n && v < x1));
+    // answer for x in [(k-1)*step + 1, min(k*step, n)], or 0 when k == 0
+    lo0 = k0 == 0 ? 0 : (k0 - 1) * step + 1;
+    hi0 = k0 == 0 ? 0 : min(k0 * step, n);
+    lo1 = k1 == 0 ? 0 : (k1 - 1) * step + 1;
+    hi1 = k1 == 0 ? 0 : min(k1 * step, n);
+  }
+  const bool second = lane >= 16;
+  const int idx = (second ? lo1 : lo0) + (lane & 15);
+  const int hi = second ? hi1 : hi0;
+  const Key x = second ? x1 : x0;
+  const unsigned m = __ballot_sync(kFull, idx < hi && a[idx] < x);
+  r0 = lo0 + __popc(m & 0xffffu);
+  r1 = lo1 + __popc(m >> 16);
 }
 
 }  // namespace sbs
