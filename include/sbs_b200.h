@@ -328,9 +328,14 @@ int sbs_run_experiments(const sbs_experiment* points, int32_t n_points,
 /* Cache-aware mode (capacity_after, prefill_alloc.cpp:12-21): hit != NULL  */
 /* gives Len_hit(r, d) of every (request, DP) pair of window w, row-major   */
 /* from hit[hit_off[w]] (request-major, n_dp per row); NULL = Basic mode.   */
+/* max_requests / max_dp: optional bounds over the batch's windows (0 =     */
+/* unknown: the 1024 / 1024 envelope).  Windows of <= 32 requests and <= 32 */
+/* DP units (Basic mode, ids < 2^27) run on registers only; the bounds size */
+/* the shared-memory slice of the rest, so small batches run many warps per */
+/* SM.                                                                      */
 typedef struct sbs_window_batch {
   int32_t n_windows;
-  int32_t _pad;
+  int32_t max_requests;
   const int64_t* req_off;
   const int32_t* n_pending;
   const int64_t* dp_off;
@@ -345,6 +350,8 @@ typedef struct sbs_window_batch {
   uint8_t* flow;
   const int64_t* hit_off;
   const int64_t* hit;
+  int32_t max_dp;
+  int32_t _pad;
 } sbs_window_batch;
 int sbs_prefill_allocate(const sbs_window_batch* batch, void* stream);
 /* One window from HOST arrays, synchronous (the reference's one-call shape,
@@ -367,7 +374,8 @@ int sbs_prefill_allocate_async(const sbs_window_batch* batch, int32_t* error_out
 /* flag and the threshold Q3 + k(Q3-Q1).  DEVICE pointers.                  */
 typedef struct sbs_decode_batch {
   int32_t n_calls;
-  int32_t _pad;
+  int32_t max_units; /* optional bound over the calls (0 = unknown); calls of */
+                     /* <= 512 units are sorted in registers                  */
   const int64_t* unit_off;
   const int32_t* batch;
   const int64_t* kv;

@@ -140,16 +140,16 @@ class Histograms(C.Structure):
 
 
 class WindowBatch(C.Structure):
-    _fields_ = [("n_windows", C.c_int32), ("_pad", C.c_int32), ("req_off", C.c_void_p),
+    _fields_ = [("n_windows", C.c_int32), ("max_requests", C.c_int32), ("req_off", C.c_void_p),
                 ("n_pending", C.c_void_p), ("dp_off", C.c_void_p), ("n_limit", C.c_void_p),
                 ("req_id", C.c_void_p), ("prompt_len", C.c_void_p), ("wait_in", C.c_void_p),
                 ("caps", C.c_void_p), ("out_dp", C.c_void_p), ("out_rank", C.c_void_p),
                 ("wait_out", C.c_void_p), ("flow", C.c_void_p), ("hit_off", C.c_void_p),
-                ("hit", C.c_void_p)]
+                ("hit", C.c_void_p), ("max_dp", C.c_int32), ("_pad", C.c_int32)]
 
 
 class DecodeBatch(C.Structure):
-    _fields_ = [("n_calls", C.c_int32), ("_pad", C.c_int32), ("unit_off", C.c_void_p),
+    _fields_ = [("n_calls", C.c_int32), ("max_units", C.c_int32), ("unit_off", C.c_void_p),
                 ("batch", C.c_void_p), ("kv", C.c_void_p), ("k", C.c_double),
                 ("pos_out", C.c_void_p), ("fallback_out", C.c_void_p),
                 ("threshold_out", C.c_void_p)]

@@ -372,7 +372,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   uint32_t o_s = 0;
   int o_k = 0, o_i = 0;
 
-  // ---- counters (shared memory, lane 0)
+  // ---- counters (shared memory, lane 0; the per-admission ones in registers)
+  int64_t n_fb = 0, n_mask = 0, n_dsel = 0;
 #ifdef SBS_PROF
   long long prof_acc[24] = {0};
   const long long prof_t0 = clock64();
@@ -636,6 +637,14 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       lo75 = (int)floor(r75); hi75 = (int)ceil(r75); fr75 = __dsub_rn(r75, (double)lo75);
       pc_n = nul;
     }
+    // the lex-min over all units (fast path) is reduced while the quartile
+    // loads and the FP64 threshold chain are in flight
+    uint32_t gh = 0xffffffffu, gl = 0xffffffffu;
+    if (lmin_ok) {
+      gh = __reduce_min_sync(kFull, (uint32_t)(lmin >> 32));
+      gl = __reduce_min_sync(kFull, (uint32_t)(lmin >> 32) == gh ? (uint32_t)lmin : 0xffffffffu);
+    }
+    const uint32_t smin = s_S[0], smax = s_S[nul - 1];
     const double a1 = (double)s_S[lo25], b1 = (double)s_S[hi25];
     const double a3 = (double)s_S[lo75], b3 = (double)s_S[hi75];
     const double q1 = lo25 == hi25 ? a1 : __dadd_rn(a1, __dmul_rn(fr25, __dsub_rn(b1, a1)));
@@ -646,17 +655,15 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     const int64_t thi = fth >= 281474976710656.0 ? (int64_t)kKMask : (fth < 0.0 ? -1 : (int64_t)fth);
     // safe set empty <=> min K > th (fallback); a proper subset <=> max K > th
     // (mask): both read off the sorted multiset, so the scan needs no count
-    const bool fallback = (int64_t)s_S[0] > thi;
-    if (fallback) CNT(fb, 1);
-    else if ((int64_t)s_S[nul - 1] > thi) CNT(mask, 1);
+    const bool fallback = (int64_t)smin > thi;
+    n_fb += fallback ? 1 : 0;
+    n_mask += (!fallback && (int64_t)smax > thi) ? 1 : 0;
     // lexicographic (B, K, position) as one u64: B << 48 | K << 16 | position
-    // (K < 2^32, position < 2^16)
+    // (K < 2^32, position < 2^16).  Fast path: the lex-min over all units is
+    // the answer whenever it is safe (or the safe set is empty): the minimum
+    // over a superset that lies in the set.
     if (lmin_ok) {
-      // the lex-min over all units is the answer whenever it is safe (or the
-      // safe set is empty): the minimum over a superset that lies in the set
-      const uint32_t h = __reduce_min_sync(kFull, (uint32_t)(lmin >> 32));
-      const uint32_t l = __reduce_min_sync(kFull, (uint32_t)(lmin >> 32) == h ? (uint32_t)lmin : 0xffffffffu);
-      const uint64_t gm = ((uint64_t)h << 32) | l;
+      const uint64_t gm = ((uint64_t)gh << 32) | gl;
       if (SBS_LIKELY(fallback || (int64_t)((gm >> 16) & 0xffffffffull) <= thi)) {
         PROF_END(5);
         return (int)(gm & 0xffffu);
@@ -770,7 +777,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         pos = (int)(dec_rr % nul);
         dec_rr += 1;
       }
-      CNT(dsel, 1);
+      n_dsel += 1;
       const int u = ul_ident ? pos : s_ul[pos];
       const int j = Dn == 1 ? 0 : u / Dd;
       // admit_decode (engine_model.cpp:145-151): B += 1, K += prompt_len
@@ -973,11 +980,17 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         // one EndForward's keys must fit the ring whole, else run on one warp
         if (m && ndw + 32 > kChanKeys) { error = kErrSplitTie; break; }
         if (m) {
+#ifdef SBS_PROF
+          const long long pk0 = clock64();
+#endif
           for (;;) {
             const int kh = chL->khead;
             if (ktail + 32 - kh <= kChanKeys) break;
             __nanosleep(100);
           }
+#ifdef SBS_PROF
+          prof_acc[17] += clock64() - pk0;
+#endif
           chan_fence<CL>();
           if (wait) {
             int32_t prompt = __ldg(g_prompt + id);
@@ -1571,7 +1584,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         if (c == kInf64 && pdone == kInf64) break;  // all done
         if (pdone <= c) {  // an EndForward <= c may still come
 #ifdef SBS_PROF
-          prof_acc[16] += 1;
+          prof_acc[16] += 164;  // ~cycles of one wait round (nanosleep 64 + polling)
 #endif
           if (pub_head != rhead) {  // exact release before waiting on the prefill warp
             chan_fence<CL>();
@@ -1731,14 +1744,17 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       if (ROLE == 1) {
         // hand-off record for the decode warp (one per EndForward)
         const int32_t hidx = bcast(ef_hidx, p), hext = bcast(ef_hext, p);
+#ifdef SBS_PROF
+        const long long pw0 = clock64();
+#endif
         for (;;) {
           const int hd = chL->head;
           if (ch_tail - hd < kChanRecs) break;
-#ifdef SBS_PROF
-          prof_acc[17] += 1;
-#endif
           __nanosleep(100);
         }
+#ifdef SBS_PROF
+        prof_acc[17] += clock64() - pw0;  // cycles waiting for record room
+#endif
         chan_fence<CL>();
         if (lane == 0) {
           ChanRec& r = chR->rec[ch_tail % kChanRecs];
@@ -1873,6 +1889,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
 
   asm volatile("cp.async.wait_all;" ::: "memory");  // staged buckets: nothing in flight
   // ---- results (completion-derived fields: finalize_kernel)
+  if (lane == 0) { cn->fb += n_fb; cn->mask += n_mask; cn->dsel += n_dsel; }
+  __syncwarp();
 #ifdef SBS_PROF
   if (ROLE == 0) prof_acc[21] += clock64() - prof_t0;
 #endif
