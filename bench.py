@@ -255,6 +255,316 @@ def run_reference_arm(args, rank, world):
     return 0
 
 
+# --------------------------------------------------------------- allocation step alone
+ALLOC_SRC_DURATION = 100.0   # cfg2 replica the windows / decode calls are recorded from
+ALLOC_WINDOWS = 1 << 20      # windows per launch (the recorded ones, tiled)
+ALLOC_CALLS = 1 << 16        # decode placements per launch (tiled)
+
+
+def alloc_inputs():
+    """The allocation calls a cfg2 replica (32 prefill DP,
+    320 decode DP, Poisson 200 qps) makes, recorded by interposing on the
+    reference's allocate_batch / select_decode_unit (oracle/ref_harness.cpp):
+    flat records with the reference's own outputs."""
+    from oracle import ref
+    out = ref.run(cfg2(11, ALLOC_SRC_DURATION), windows=True, decodes=True, dec_cap=1 << 25)
+    return out["windows"], out["decodes"]
+
+
+def parse_windows(rec):
+    import numpy as np
+    rec = np.asarray(rec, np.int64)
+    w, i = [], 0
+    while i < len(rec):
+        np_, nn, D, nlim = (int(x) for x in rec[i:i + 4]); i += 4
+        rows = rec[i:i + 3 * (np_ + nn)].reshape(-1, 3); i += 3 * (np_ + nn)
+        caps = rec[i:i + D]; i += D
+        nm = int(rec[i]); mp = rec[i + 1:i + 1 + 2 * nm].reshape(-1, 2); i += 1 + 2 * nm
+        nd = int(rec[i]); i += 1 + 2 * nd
+        nt = int(rec[i]); i += 1 + nt
+        caps_out = rec[i:i + D]; i += D
+        flow = int(rec[i]); i += 1
+        w.append((np_, nlim, rows, caps, mp, caps_out, flow))
+    return w
+
+
+def parse_decodes(rec):
+    import numpy as np
+    rec = np.asarray(rec, np.int64)
+    c, i = [], 0
+    while i < len(rec):
+        U = int(rec[i]); bk = rec[i + 1:i + 1 + 2 * U].reshape(-1, 2); i += 1 + 2 * U
+        c.append((bk[:, 0].astype(np.int32), bk[:, 1].copy(), int(rec[i]), int(rec[i + 1]))); i += 2
+    return c
+
+
+def run_alloc(args, rank, world):
+    """`--workload alloc`: the allocation step on its own — batched PBAA windows
+    (sbs_prefill_allocate, allocate_batch prefill_alloc.cpp:61-88) and batched
+    IQR decode placements (sbs_decode_select, select_decode_unit
+    decode_alloc.cpp:38-81) over the calls a cfg2 replica makes, recorded from
+    the reference and tiled to 2^20 windows / 2^16 placements per launch;
+    the reference's own functions timed on all host cores on the same calls."""
+    import ctypes
+    import numpy as np
+    threads = os.cpu_count() or 1
+    wrec, drec = alloc_inputs()
+    wins, calls = parse_windows(wrec), parse_decodes(drec)
+    desc = (f"alloc: the {len(wins)} PBAA windows and {len(calls)} IQR decode placements of a cfg2 "
+            f"replica ({ALLOC_SRC_DURATION:g} s; prefill 4xDP8, decode 1xDP320), recorded from the "
+            f"reference, tiled to {ALLOC_WINDOWS} windows and {ALLOC_CALLS} placements per launch")
+    qs = np.array([len(w[2]) for w in wins]); ds = np.array([len(w[3]) for w in wins])
+    us = np.array([len(c[0]) for c in calls])
+
+    def cpu_arm():
+        # bounded samples (~2-5 s each) of the reference's allocate_batch / select_decode_unit
+        from oracle import ref
+        ref.lib()
+        w_wall, w_n, _ = ref.bench_allocate(wrec, threads, 1)
+        reps = max(1, int(2.0 / max(w_wall, 1e-4)))
+        w_wall, w_n, _ = ref.bench_allocate(wrec, threads, reps)
+        d_wall, d_n, _ = ref.bench_select(drec, 1.5, threads, 1)
+        dreps = max(1, int(2.0 / max(d_wall, 1e-4)))
+        d_wall, d_n, _ = ref.bench_select(drec, 1.5, threads, dreps)
+        return {"windows_per_s": w_n / w_wall, "windows": w_n, "windows_wall_s": w_wall,
+                "selects_per_s": d_n / d_wall, "selects": d_n, "selects_wall_s": d_wall}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        vals = []
+        for i in range(args.warmup + args.steps):
+            c = cpu_arm()
+            if i >= args.warmup:
+                vals.append(c)
+        v = statistics.mean(c["windows_per_s"] for c in vals)
+        sample = (f"allocate_batch over the recorded windows ({vals[0]['windows']} calls per step) and "
+                  f"select_decode_unit over the recorded placements ({vals[0]['selects']} calls per "
+                  f"step), {threads}-thread std::thread pool")
+        print(json.dumps({
+            "impl": "reference", "metric": "allocations_per_s", "value": v, "unit": "windows/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * statistics.mean(c["windows_wall_s"] for c in vals),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic", "config": {"workload": desc, "sample": sample},
+            "decode_selects_per_s": statistics.mean(c["selects_per_s"] for c in vals),
+            "cpu_baseline": {"value": v, "unit": "windows/s", "cores": threads, "kind": "reference",
+                             "sample": sample, "cpu_model": cpu_model()},
+            "e2e": {"value": v, "unit": "windows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+            flush=True)
+        return 0
+
+    import torch
+    import paper_2512_16134_b200 as P
+    from paper_2512_16134_b200 import api
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    L = api.lib()
+
+    # ---- windows: CSR arrays of one tile, tiled ALLOC_WINDOWS / len(wins) times
+    T = max(1, ALLOC_WINDOWS // len(wins))
+    nw = T * len(wins)
+    np_ = np.array([w[0] for w in wins], np.int32)
+    nl = np.array([w[1] for w in wins], np.int32)
+    rows = np.concatenate([w[2] for w in wins])
+    caps = np.concatenate([w[3] for w in wins])
+    roff1 = np.concatenate([[0], np.cumsum(qs)]).astype(np.int64)
+    doff1 = np.concatenate([[0], np.cumsum(ds)]).astype(np.int64)
+    nr1, nd1 = int(roff1[-1]), int(doff1[-1])
+    host = {
+        "req_off": np.concatenate([roff1[:-1] + t * nr1 for t in range(T)] + [[T * nr1]]).astype(np.int64),
+        "dp_off": np.concatenate([doff1[:-1] + t * nd1 for t in range(T)] + [[T * nd1]]).astype(np.int64),
+        "n_pending": np.tile(np_, T), "n_limit": np.tile(nl, T),
+        "req_id": np.tile(rows[:, 0], T), "prompt_len": np.tile(rows[:, 1], T),
+        "wait_in": np.tile(rows[:, 2].astype(np.int32), T), "caps": np.tile(caps, T)}
+    hp = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in host.items()}
+    g = {k: v.to(dev) for k, v in hp.items()}
+    caps0 = g["caps"].clone()
+    nreq = T * nr1
+    o = {"out_dp": torch.empty(nreq, dtype=torch.int32, device=dev),
+         "out_rank": torch.empty(nreq, dtype=torch.int32, device=dev),
+         "wait_out": torch.empty(nreq, dtype=torch.int32, device=dev),
+         "flow": torch.empty(nw, dtype=torch.uint8, device=dev)}
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    wb = api.WindowBatch(n_windows=nw, max_requests=int(qs.max()), max_dp=int(ds.max()),
+                         req_off=g["req_off"].data_ptr(), n_pending=g["n_pending"].data_ptr(),
+                         dp_off=g["dp_off"].data_ptr(), n_limit=g["n_limit"].data_ptr(),
+                         req_id=g["req_id"].data_ptr(), prompt_len=g["prompt_len"].data_ptr(),
+                         wait_in=g["wait_in"].data_ptr(), caps=g["caps"].data_ptr(),
+                         out_dp=o["out_dp"].data_ptr(), out_rank=o["out_rank"].data_ptr(),
+                         wait_out=o["wait_out"].data_ptr(), flow=o["flow"].data_ptr(),
+                         hit_off=None, hit=None)
+    st = ctypes.c_void_p(stream.cuda_stream)
+    eptr = ctypes.c_void_p(err.data_ptr())
+
+    def launch_windows():
+        g["caps"].copy_(caps0)  # every step starts from the recorded c_avail snapshots
+        api._check(L.sbs_prefill_allocate_async(ctypes.byref(wb), eptr, st))
+
+    # ---- decode placements: tiled calls of 320 units
+    Tc = max(1, ALLOC_CALLS // len(calls))
+    ncall = Tc * len(calls)
+    uo1 = np.concatenate([[0], np.cumsum(us)]).astype(np.int64)
+    nu1 = int(uo1[-1])
+    dh = {"unit_off": np.concatenate([uo1[:-1] + t * nu1 for t in range(Tc)] + [[Tc * nu1]]).astype(np.int64),
+          "batch": np.tile(np.concatenate([c[0] for c in calls]), Tc),
+          "kv": np.tile(np.concatenate([c[1] for c in calls]), Tc)}
+    dhp = {k: torch.from_numpy(np.ascontiguousarray(v)).pin_memory() for k, v in dh.items()}
+    dg = {k: v.to(dev) for k, v in dhp.items()}
+    d_pos = torch.empty(ncall, dtype=torch.int32, device=dev)
+    d_fb = torch.empty(ncall, dtype=torch.uint8, device=dev)
+    d_th = torch.empty(ncall, dtype=torch.float64, device=dev)
+    db = api.DecodeBatch(n_calls=ncall, max_units=int(us.max()), unit_off=dg["unit_off"].data_ptr(),
+                         batch=dg["batch"].data_ptr(), kv=dg["kv"].data_ptr(), k=1.5,
+                         pos_out=d_pos.data_ptr(), fallback_out=d_fb.data_ptr(),
+                         threshold_out=d_th.data_ptr())
+
+    def launch_calls():
+        api._check(L.sbs_decode_select_async(ctypes.byref(db), eptr, st))
+
+    # ---- parity of the first tile against the reference's recorded outputs
+    launch_windows(); launch_calls()
+    torch.cuda.synchronize()
+    if int(err.item()):
+        raise SystemExit(f"allocation kernels reported error {int(err.item())}")
+    odp, ork = o["out_dp"][:nr1].cpu().numpy(), o["out_rank"][:nr1].cpu().numpy()
+    ocaps = g["caps"][:nd1].cpu().numpy()
+    bad = 0
+    for i, w in enumerate(wins):
+        r0, r1 = roff1[i], roff1[i + 1]
+        pl = np.nonzero(odp[r0:r1] >= 0)[0]
+        pl = pl[np.argsort(ork[r0:r1][pl], kind="stable")]
+        got = np.stack([w[2][pl, 0], odp[r0:r1][pl]], 1) if len(pl) else np.zeros((0, 2), np.int64)
+        if not (np.array_equal(got, w[4]) and np.array_equal(ocaps[doff1[i]:doff1[i + 1]], w[5])):
+            bad += 1
+    pos1, fb1 = d_pos[:len(calls)].cpu().numpy(), d_fb[:len(calls)].cpu().numpy()
+    bad_d = int(sum(int(pos1[i]) != c[2] or int(fb1[i]) != c[3] for i, c in enumerate(calls)))
+    if bad or bad_d:
+        raise SystemExit(f"allocation parity failed: {bad} windows, {bad_d} placements")
+
+    def timed(fn, steps):
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ts = []
+        for _ in range(steps):
+            if dist:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            fn()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(ev0.elapsed_time(ev1))
+        return statistics.mean(ts)
+
+    for _ in range(args.warmup):
+        launch_windows(); launch_calls()
+    gpu = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local]) \
+        if os.environ.get("CUDA_VISIBLE_DEVICES") else local
+    with ClockSampler(gpu) as clk:
+        w_ms = timed(launch_windows, args.steps)
+        d_ms = timed(launch_calls, args.steps)
+    clocks = clk.summary()
+    if int(err.item()):
+        raise SystemExit("allocation kernels reported an error")
+    if dist:
+        t = torch.tensor([w_ms, d_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        w_ms, d_ms = float(t[0].item()), float(t[1].item())
+
+    # ---- e2e: host (pinned) inputs -> device -> kernel -> outputs back, per step
+    n_e = max(2, min(args.steps, 4))
+    hcaps = hp["caps"]
+    out_h = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in o.items()}
+    caps_h = torch.empty_like(hcaps).pin_memory()
+    in_keys = ["req_off", "dp_off", "n_pending", "n_limit", "req_id", "prompt_len", "wait_in", "caps"]
+    h2d = sum(hp[k].numel() * hp[k].element_size() for k in in_keys)
+    d2h = sum(v.numel() * v.element_size() for v in o.values()) + caps_h.numel() * 8
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_a = time.perf_counter()
+    for _ in range(n_e):
+        for k in in_keys:
+            g[k].copy_(hp[k], non_blocking=True)
+        api._check(L.sbs_prefill_allocate_async(ctypes.byref(wb), eptr, st))
+        for k, v in o.items():
+            out_h[k].copy_(v, non_blocking=True)
+        caps_h.copy_(g["caps"], non_blocking=True)
+        torch.cuda.synchronize()
+    e_s = (time.perf_counter() - t_a) / n_e
+    if dist:
+        t = torch.tensor([e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_s = float(t[0].item())
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            c = cpu_arm()
+            cpu = {"value": c["windows_per_s"], "unit": "windows/s", "cores": threads,
+                   "kind": "reference", "cpu_model": cpu_model(),
+                   "selects_per_s": c["selects_per_s"],
+                   "sample": f"allocate_batch x {c['windows']} and select_decode_unit x {c['selects']} "
+                             f"(the recorded calls, repeated) on {threads} threads"}
+        except Exception as e:
+            cpu = {"value": None, "unit": "windows/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    peaks = {}
+    try:
+        peaks = json.load(open(ROOT / "MEASURED_PEAKS.json"))
+    except Exception:
+        pass
+    peak = peaks.get("hbm_gbs", 6650.0)
+    # algorithmic bytes (SURVEY §8d): 12*Q + 16*D per window, 12*U + 4 per placement
+    wbytes = T * float((12 * qs + 16 * ds).sum())
+    dbytes = Tc * float((12 * us + 4).sum())
+    w_ach = wbytes / (w_ms / 1000.0) / 1e9
+    d_ach = dbytes / (d_ms / 1000.0) / 1e9
+    value = world * nw / (w_ms / 1000.0)
+    line = {
+        "metric": "allocations_per_s", "value": value, "unit": "windows/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": w_ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": desc, "windows_per_launch": nw, "requests_per_window_mean": float(qs.mean()),
+                   "requests_per_window_max": int(qs.max()), "dp_units": int(ds.max()),
+                   "placements_per_launch": ncall, "units_per_placement": int(us.max()),
+                   "l2": f"{(h2d + dbytes / Tc * Tc) / 1e6:.0f} MB of inputs per launch pair (> L2)",
+                   "parity": f"first tile equal to the reference's recorded outputs ({len(wins)} windows, "
+                             f"{len(calls)} placements)"},
+        "decode_selects_per_s": {"value": world * ncall / (d_ms / 1000.0), "unit": "placements/s",
+                                 "ms_per_launch": d_ms,
+                                 "roofline": {"bound": "hbm", "achieved": d_ach, "peak": peak,
+                                              "unit": "GB/s", "frac": d_ach / peak,
+                                              "bytes": "12*U + 4 per placement"},
+                                 "cpu_baseline": (cpu or {}).get("selects_per_s")},
+        "gpu_launches": args.steps * 2,
+        "roofline": {"bound": "hbm", "achieved": w_ach, "peak": peak, "unit": "GB/s",
+                     "frac": w_ach / peak, "traffic": None, "kernel_ms": w_ms,
+                     "kernel_share_of_step": 1.0,
+                     "note": "algorithmic bytes = 12*Q + 16*D per window (SURVEY §8d); the C-ABI "
+                             "format moves 32 B per request + 16 B per DP unit"},
+        "clocks": clocks,
+        "e2e": {"value": world * nw / e_s, "unit": "windows/s", "h2d_bytes_per_step": h2d * world,
+                "d2h_bytes_per_step": d2h * world, "ms_per_step": e_s * 1000.0, "steps": n_e,
+                "what": "per step: every window input H2D from pinned memory, the PBAA kernel, "
+                        "every output D2H"},
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 def relaunch(n):
     """`bench.py --gpus N` outside torchrun: one rank per GPU via
     torch.distributed.run on 127.0.0.1 (rank 0 prints the line)."""
@@ -275,7 +585,8 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+    ap.add_argument("--workload", default="cfg5",
+                    choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "alloc"])
     ap.add_argument("--replicas", type=int, default=None, help="dev override (not a bench line)")
     ap.add_argument("--duration", type=float, default=None, help="dev override (not a bench line)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -290,6 +601,8 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.workload == "alloc":
+        return run_alloc(args, rank, world)
     if args.impl == "reference":
         return run_reference_arm(args, rank, world)
 

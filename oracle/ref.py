@@ -78,6 +78,9 @@ def lib():
         L.ref_outlier_threshold.restype = C.c_double
         L.ref_run_batch.argtypes = [C.POINTER(C.c_char_p), C.c_int64, C.c_int, _f64p,
                                     _i64p, _f64p]
+        L.ref_bench_allocate.argtypes = [_i64p, C.c_int64, C.c_int, C.c_int, _f64p, _i64p, _i64p]
+        L.ref_bench_select.argtypes = [_i64p, C.c_int64, C.c_double, C.c_int, C.c_int, _f64p,
+                                       _i64p, _i64p]
         _lib = L
     return _lib
 
@@ -231,3 +234,23 @@ def run_batch(cfgs, threads):
     _check(L.ref_run_batch(arr, len(cfgs), int(threads), _p(agg, _f64p), _p(meta),
                            C.byref(wall)))
     return wall.value, agg, meta
+
+
+def bench_allocate(window_records, threads, reps):
+    """CPU baseline: the reference's allocate_batch over recorded windows
+    (Recorder records), `reps` passes on `threads` threads.  Returns
+    (wall_s, calls, checksum)."""
+    rec = np.ascontiguousarray(window_records, np.int64)
+    wall, n, cs = np.zeros(1), np.zeros(1, np.int64), np.zeros(1, np.int64)
+    _check(lib().ref_bench_allocate(_p(rec), len(rec), int(threads), int(reps), _p(wall, _f64p),
+                                    _p(n), _p(cs)))
+    return float(wall[0]), int(n[0]) * max(1, int(reps)), int(cs[0])
+
+
+def bench_select(decode_records, k, threads, reps):
+    """CPU baseline: the reference's select_decode_unit over recorded calls."""
+    rec = np.ascontiguousarray(decode_records, np.int64)
+    wall, n, cs = np.zeros(1), np.zeros(1, np.int64), np.zeros(1, np.int64)
+    _check(lib().ref_bench_select(_p(rec), len(rec), float(k), int(threads), int(reps),
+                                  _p(wall, _f64p), _p(n), _p(cs)))
+    return float(wall[0]), int(n[0]) * max(1, int(reps)), int(cs[0])

@@ -520,4 +520,124 @@ int ref_run_batch(const char* const* json_texts, std::int64_t n, int threads,
   return rc.load();
 }
 
+// CPU baseline of the allocation step alone: the reference's allocate_batch
+// (Basic mode) over `n` recorded windows (flat Recorder records, see above),
+// `reps` passes per window, on a pool of `threads` std::threads.  Each call
+// starts from the recorded inputs (c_avail snapshot, wait_cycles), as the
+// Runner's perform_dispatch does (simulation.cpp:277-289).  Returns wall
+// seconds; *checksum folds the placements (so nothing is optimised away).
+int ref_bench_allocate(const std::int64_t* rec, std::int64_t rec_len, int threads, int reps,
+                       double* wall_s, std::int64_t* n_windows, std::int64_t* checksum) {
+  struct Win {
+    std::vector<Request> req;
+    std::vector<Request*> pend, fresh;
+    std::vector<std::int64_t> caps;
+    std::vector<int> waits;
+    int n_limit = 0;
+  };
+  std::vector<Win> wins;
+  std::int64_t i = 0;
+  while (i < rec_len) {
+    const std::int64_t np = rec[i], nn = rec[i + 1], D = rec[i + 2];
+    Win w;
+    w.n_limit = static_cast<int>(rec[i + 3]);
+    i += 4;
+    w.req.resize(static_cast<std::size_t>(np + nn));
+    for (std::int64_t r = 0; r < np + nn; ++r) {
+      Request& q = w.req[static_cast<std::size_t>(r)];
+      q.id = static_cast<std::uint64_t>(rec[i]);
+      q.prompt_len = rec[i + 1];
+      q.wait_cycles = static_cast<int>(rec[i + 2]);
+      w.waits.push_back(q.wait_cycles);
+      i += 3;
+    }
+    for (std::int64_t r = 0; r < np + nn; ++r)
+      (r < np ? w.pend : w.fresh).push_back(&w.req[static_cast<std::size_t>(r)]);
+    for (std::int64_t d = 0; d < D; ++d) w.caps.push_back(rec[i + d]);
+    i += D;
+    const std::int64_t nm = rec[i];
+    i += 1 + 2 * nm;
+    const std::int64_t nd = rec[i];
+    i += 1 + 2 * nd;
+    const std::int64_t nt = rec[i];
+    i += 1 + nt + D + 1;
+    wins.push_back(std::move(w));
+  }
+  *n_windows = static_cast<std::int64_t>(wins.size());
+  std::atomic<std::int64_t> next{0}, sum{0};
+  const std::int64_t total = static_cast<std::int64_t>(wins.size()) * std::max(1, reps);
+  auto worker = [&]() {
+    std::vector<DpPlan> dps;
+    std::int64_t local = 0;
+    for (;;) {
+      const std::int64_t j = next.fetch_add(64);
+      if (j >= total) break;
+      for (std::int64_t t = j; t < std::min(total, j + 64); ++t) {
+        Win& w = wins[static_cast<std::size_t>(t % static_cast<std::int64_t>(wins.size()))];
+        // (per-thread copies of the mutable request state)
+        std::vector<Request> req = w.req;
+        std::vector<Request*> pv, nv;
+        for (std::size_t r = 0; r < req.size(); ++r)
+          (r < w.pend.size() ? pv : nv).push_back(&req[r]);
+        dps.resize(w.caps.size());
+        for (std::size_t d = 0; d < w.caps.size(); ++d) {
+          dps[d].dp_index = static_cast<int>(d);
+          dps[d].c_avail = w.caps[d];
+          dps[d].cache = nullptr;
+        }
+        AllocationResult res = ref_impl_allocate_batch({pv.data(), pv.size()}, {nv.data(), nv.size()},
+                                                       dps, w.n_limit, AllocMode::kBasic);
+        local += static_cast<std::int64_t>(res.mapping.size()) + (res.flow_control ? 1 : 0);
+      }
+    }
+    sum += local;
+  };
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> pool;
+  for (int t = 0; t < std::max(1, threads); ++t) pool.emplace_back(worker);
+  for (auto& th : pool) th.join();
+  *wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  *checksum = sum.load();
+  return 0;
+}
+
+// CPU baseline of the decode placement alone: the reference's
+// select_decode_unit over `n` recorded calls (Recorder decode records), `reps`
+// passes, on `threads` threads.
+int ref_bench_select(const std::int64_t* rec, std::int64_t rec_len, double k, int threads, int reps,
+                     double* wall_s, std::int64_t* n_calls, std::int64_t* checksum) {
+  std::vector<std::vector<DecodeUnitPlan>> calls;
+  std::int64_t i = 0;
+  while (i < rec_len) {
+    const std::int64_t U = rec[i];
+    std::vector<DecodeUnitPlan> u(static_cast<std::size_t>(U));
+    for (std::int64_t x = 0; x < U; ++x)
+      u[static_cast<std::size_t>(x)] =
+          DecodeUnitPlan{static_cast<int>(x), static_cast<int>(rec[i + 1 + 2 * x]), rec[i + 2 + 2 * x]};
+    i += 1 + 2 * U + 2;
+    calls.push_back(std::move(u));
+  }
+  *n_calls = static_cast<std::int64_t>(calls.size());
+  std::atomic<std::int64_t> next{0}, sum{0};
+  const std::int64_t total = static_cast<std::int64_t>(calls.size()) * std::max(1, reps);
+  auto worker = [&]() {
+    std::int64_t local = 0;
+    for (;;) {
+      const std::int64_t j = next.fetch_add(64);
+      if (j >= total) break;
+      for (std::int64_t t = j; t < std::min(total, j + 64); ++t)
+        local += ref_impl_select_decode_unit(
+            calls[static_cast<std::size_t>(t % static_cast<std::int64_t>(calls.size()))], k, 0, nullptr);
+    }
+    sum += local;
+  };
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> pool;
+  for (int t = 0; t < std::max(1, threads); ++t) pool.emplace_back(worker);
+  for (auto& th : pool) th.join();
+  *wall_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  *checksum = sum.load();
+  return 0;
+}
+
 }  // extern "C"

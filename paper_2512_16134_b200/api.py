@@ -812,7 +812,9 @@ def allocate_batch(windows, device="cuda"):
                     caps=t_caps.data_ptr(), out_dp=t_dp.data_ptr(), out_rank=t_rank.data_ptr(),
                     wait_out=t_wout.data_ptr(), flow=t_flow.data_ptr(),
                     hit_off=t_hoff.data_ptr() if t_hoff is not None else None,
-                    hit=t_hit.data_ptr() if t_hit is not None else None)
+                    hit=t_hit.data_ptr() if t_hit is not None else None,
+                    max_requests=max(np.diff(req_off).max(initial=0), 1),
+                    max_dp=max(np.diff(dp_off).max(initial=0), 1))
     stream = torch.cuda.current_stream(dev).cuda_stream
     _check(lib().sbs_prefill_allocate(C.byref(b), C.c_void_p(stream)))
     o_dp, o_rank, o_w = t_dp.cpu().numpy(), t_rank.cpu().numpy(), t_wout.cpu().numpy()
@@ -854,7 +856,8 @@ def select_decode_unit(calls, k=1.5, device="cuda"):
     t_pos = torch.empty(n, dtype=torch.int32, device=dev)
     t_fb = torch.empty(n, dtype=torch.uint8, device=dev)
     t_th = torch.empty(n, dtype=torch.float64, device=dev)
-    b = DecodeBatch(n_calls=n, unit_off=t_off.data_ptr(), batch=t_b.data_ptr(), kv=t_k.data_ptr(),
+    b = DecodeBatch(n_calls=n, max_units=max(np.diff(off).max(initial=0), 1),
+                    unit_off=t_off.data_ptr(), batch=t_b.data_ptr(), kv=t_k.data_ptr(),
                     k=float(k), pos_out=t_pos.data_ptr(), fallback_out=t_fb.data_ptr(),
                     threshold_out=t_th.data_ptr())
     stream = torch.cuda.current_stream(dev).cuda_stream

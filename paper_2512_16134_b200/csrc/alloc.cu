@@ -1,16 +1,20 @@
 // Batched allocation kernels — the allocation step as its own sm_100a kernel.
 //
 //  pbaa_kernel   : allocate_batch (prefill_alloc.cpp:61-88) over a CSR batch
-//                  of cluster-windows, one warp per window.  Each queue is
-//                  sorted by (prompt_len desc, id asc) with a warp bitonic
-//                  sort in shared memory, then placed greedily: a warp max
-//                  over capacity_after = c_avail - (prompt - hit) for the DP
-//                  capacities staged in shared memory (hit = 0 in Basic
-//                  mode), lowest index on ties, guarded by c_avail > 0 on the
-//                  chosen unit.
+//                  of cluster-windows, one warp per window.  Windows of <= 32
+//                  requests and <= 32 DP units (Basic mode) run on registers:
+//                  lane i holds request i and DP unit i, one in-register
+//                  bitonic sort orders (phase, prompt_len desc, id asc, input
+//                  position) — pending before new, stable like std::stable_sort
+//                  — and each placement is a REDUX argmax over the lanes'
+//                  capacities (lowest index on ties), guarded by c_avail > 0.
+//                  Larger or cache-aware windows sort in a shared-memory slice
+//                  sized from the batch's bounds and take a warp max over
+//                  capacity_after = c_avail - (prompt - hit).
 //  iqr_kernel    : select_decode_unit (decode_alloc.cpp:38-81), one warp per
-//                  call: K staged and sorted in shared memory, Q1/Q3 by the
-//                  reference's FP64 interpolation, IQR mask, lex-min (B, K).
+//                  call: for <= 512 units K is sorted in registers (16 per
+//                  lane), else in shared memory; Q1/Q3 by the reference's
+//                  FP64 interpolation, IQR mask, lex-min (B, K).
 //  sched_kernel  : schedule_decode_batch (decode_alloc.cpp:83-106), one warp
 //                  per candidate batch: stable order (sort_len desc, id asc),
 //                  then one select_decode_unit per candidate on units kept in
@@ -61,6 +65,7 @@ __device__ void warp_sort_pairs(uint64_t* a, uint64_t* b, int* idx, int n) {
 
 struct PbaaArgs {
   int32_t n_windows;
+  int32_t max_req, max_dp;  // slice bounds of the shared-memory path (<= 1024 each)
   const int64_t* req_off;
   const int32_t* n_pending;
   const int64_t* dp_off;
@@ -78,14 +83,27 @@ struct PbaaArgs {
   const int64_t* hit;
 };
 
+// Shared-memory slice of one warp on the general path: sort keys (2 x u64),
+// positions (i32) for a power-of-two padded queue, then the DP capacities.
+__host__ __device__ inline int pbaa_pow2(int n) {
+  int m = 1;
+  while (m < n) m <<= 1;
+  return m;
+}
+__host__ __device__ inline size_t pbaa_slice_bytes(int max_req, int max_dp) {
+  const size_t q = (size_t)pbaa_pow2(max_req < 1 ? 1 : max_req);
+  return ((q * 20 + 15) & ~(size_t)15) + 8 * (size_t)(max_dp < 1 ? 1 : max_dp);
+}
+
 // One cluster-window by one warp; `my` is its shared-memory slice
-// (kAllocMaxReq * 20 + kAllocMaxDp * 8 bytes).
+// (pbaa_slice_bytes(A.max_req, A.max_dp)).
 __device__ void pbaa_window(const PbaaArgs& A, int w, unsigned char* my) {
   const int lane = lane_id();
+  const int QP = pbaa_pow2(A.max_req < 1 ? 1 : A.max_req);
   uint64_t* ka = (uint64_t*)my;
-  uint64_t* kb = ka + kAllocMaxReq;
-  int* ki = (int*)(kb + kAllocMaxReq);
-  int64_t* cap = (int64_t*)(ki + kAllocMaxReq);
+  uint64_t* kb = ka + QP;
+  int* ki = (int*)(kb + QP);
+  int64_t* cap = (int64_t*)(my + ((QP * 20 + 15) & ~15));
 
   const int64_t r0 = A.req_off[w], r1 = A.req_off[w + 1];
   const int n = (int)(r1 - r0);
@@ -93,7 +111,7 @@ __device__ void pbaa_window(const PbaaArgs& A, int w, unsigned char* my) {
   const int64_t c0 = A.dp_off[w];
   const int D = (int)(A.dp_off[w + 1] - c0);
   const int nlim = A.n_limit[w];
-  if (n > kAllocMaxReq || D > kAllocMaxDp || npend > n || D < 1) {
+  if (n > A.max_req || D > A.max_dp || npend > n || D < 1) {
     if (lane == 0) atomicExch(A.error, 4);
     return;
   }
@@ -162,12 +180,89 @@ __device__ void pbaa_window(const PbaaArgs& A, int w, unsigned char* my) {
   if (lane == 0) A.flow[w] = any_thr ? 1 : 0;
 }
 
-__global__ void __launch_bounds__(32 * kAllocWarps) pbaa_kernel(PbaaArgs A) {
+// Register path: <= 32 requests, <= 32 DP units, Basic mode, 0 <= id < 2^27,
+// 0 <= prompt_len < 2^31.  Lane i loads request i and DP unit i.  One u64 key
+// per request — phase (pending 0 / new 1) | 0x7fffffff - prompt | id | input
+// position — sorts both queues at once in the order greedy_dispatch visits
+// them (prefill_alloc.cpp:28-35, std::stable_sort: the position breaks full
+// ties).  In Basic mode argmax(c_avail - prompt) == argmax c_avail, and once
+// the maximum is <= 0 nothing later fits (capacities only fall), so the loop
+// stops there; every unplaced request is deferred or throttled
+// (prefill_alloc.cpp:71-86).  Returns false (nothing written) when the window
+// is outside this envelope.
+__device__ bool pbaa_window_reg(const PbaaArgs& A, int w, int lane) {
+  const int64_t r0 = A.req_off[w];
+  const int n = (int)(A.req_off[w + 1] - r0);
+  const int npend = A.n_pending[w];
+  const int64_t c0 = A.dp_off[w];
+  const int D = (int)(A.dp_off[w + 1] - c0);
+  if (n > 32 || D > 32 || D < 1 || npend > n || A.hit != nullptr) return false;
+  const bool has = lane < n;
+  const int64_t id = has ? A.req_id[r0 + lane] : 0;
+  const int64_t len = has ? A.prompt_len[r0 + lane] : 0;
+  const int64_t cap0 = lane < D ? A.caps[c0 + lane] : 0;
+  const bool ok = !has || (id >= 0 && id < (1ll << 27) && len >= 0 && len < (1ll << 31));
+  if (!__all_sync(kFull, ok)) return false;
+  uint64_t key = has ? ((uint64_t)(lane >= npend) << 63) | ((uint64_t)(0x7fffffffu - (uint32_t)len) << 32) |
+                           ((uint64_t)id << 5) | (uint64_t)lane
+                     : UINT64_MAX;
+  key = warp_sort32<true>(key, lane);  // lane j: the j-th request visited
+  const int src = (int)(key & 31u);
+  const int64_t my_len = (int64_t)(0x7fffffffu - (uint32_t)((key >> 32) & 0x7fffffffu));
+  // capacities: 32-bit REDUX when they fit (a placed unit keeps c - len >
+  // -2^31 because c > 0 and len < 2^31, so they keep fitting), else 64-bit
+  const bool small = __all_sync(kFull, lane >= D || (cap0 >= INT32_MIN && cap0 <= INT32_MAX));
+  int64_t cap = lane < D ? cap0 : INT64_MIN;
+  int my_dp = -1, my_rank = -1, rank = 0;
+  for (int j = 0; j < n; ++j) {
+    const int64_t L = __shfl_sync(kFull, my_len, j);
+    int64_t mv;
+    int best;
+    if (small) {
+      const uint32_t bv = (uint32_t)(int32_t)(lane < D ? cap : (int64_t)INT32_MIN) ^ 0x80000000u;
+      const uint32_t m = __reduce_max_sync(kFull, bv);
+      best = (int)__reduce_min_sync(kFull, bv == m ? (uint32_t)lane : 32u);
+      mv = (int64_t)(int32_t)(m ^ 0x80000000u);
+    } else {
+      const uint64_t bv = (uint64_t)cap ^ 0x8000000000000000ull;
+      const uint32_t h = __reduce_max_sync(kFull, (uint32_t)(bv >> 32));
+      const uint32_t l = __reduce_max_sync(kFull, (uint32_t)(bv >> 32) == h ? (uint32_t)bv : 0u);
+      const uint64_t m = ((uint64_t)h << 32) | l;
+      best = (int)__reduce_min_sync(kFull, bv == m ? (uint32_t)lane : 32u);
+      mv = (int64_t)(m ^ 0x8000000000000000ull);
+    }
+    if (mv <= 0) break;  // guard on the chosen unit fails here and for everything after
+    if (lane == best) cap -= L;
+    if (lane == j) { my_dp = best; my_rank = rank; }
+    rank += 1;
+  }
+  bool thr = false;
+  if (has) {
+    const int32_t wv = A.wait_in[r0 + src];
+    if (my_dp >= 0) {
+      A.out_dp[r0 + src] = my_dp;
+      A.out_rank[r0 + src] = my_rank;
+      A.wait_out[r0 + src] = wv;
+    } else {
+      thr = wv + 1 > A.n_limit[w];
+      A.out_dp[r0 + src] = thr ? -2 : -1;
+      A.out_rank[r0 + src] = -1;
+      A.wait_out[r0 + src] = wv + 1;
+    }
+  }
+  if (lane < D) A.caps[c0 + lane] = cap;
+  thr = __any_sync(kFull, thr);
+  if (lane == 0) A.flow[w] = thr ? 1 : 0;
+  return true;
+}
+
+__global__ void __launch_bounds__(256) pbaa_kernel(PbaaArgs A, int slice) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int warp = threadIdx.x >> 5;
-  const int w = blockIdx.x * kAllocWarps + warp;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int w = blockIdx.x * (blockDim.x >> 5) + warp;
   if (w >= A.n_windows) return;
-  pbaa_window(A, w, smem + warp * (kAllocMaxReq * 20 + kAllocMaxDp * 8));
+  if (pbaa_window_reg(A, w, lane)) return;
+  pbaa_window(A, w, smem + (size_t)warp * slice);
 }
 
 // A single small window passed by value in the kernel parameters (no input
@@ -182,7 +277,7 @@ struct PbaaOne {
   int32_t* out;  // mapped host: dp[n], rank[n], wait[n], flow, error; then caps (int64, 8-aligned)
 };
 __global__ void __launch_bounds__(32) pbaa_one_kernel(PbaaOne P) {
-  __shared__ __align__(16) unsigned char slice[kAllocMaxReq * 20 + kAllocMaxDp * 8];
+  __shared__ __align__(16) unsigned char slice[kOneMax * 20 + kOneMax * 8];
   __shared__ int64_t s_id[kOneMax], s_len[kOneMax], s_caps[kOneMax], s_off[4];
   __shared__ int32_t s_wait[kOneMax], s_dp[kOneMax], s_rank[kOneMax], s_wout[kOneMax], s_misc[4];
   __shared__ uint8_t s_flow;
@@ -200,9 +295,9 @@ __global__ void __launch_bounds__(32) pbaa_one_kernel(PbaaOne P) {
     s_err = 0;
   }
   __syncwarp();
-  PbaaArgs A{1, s_off, s_misc, s_off + 2, s_misc + 1, s_id, s_len, s_wait, s_caps,
+  PbaaArgs A{1, kOneMax, kOneMax, s_off, s_misc, s_off + 2, s_misc + 1, s_id, s_len, s_wait, s_caps,
              s_dp, s_rank, s_wout, &s_flow, &s_err, nullptr, nullptr};
-  pbaa_window(A, 0, slice);
+  if (!pbaa_window_reg(A, 0, lane)) pbaa_window(A, 0, slice);
   __syncwarp();
   int32_t* o = P.out;
   for (int i = lane; i < P.n; i += 32) {
@@ -220,6 +315,7 @@ __global__ void __launch_bounds__(32) pbaa_one_kernel(PbaaOne P) {
 
 struct IqrArgs {
   int32_t n_calls;
+  int32_t max_units;  // bound over the calls (<= 2048); <= 512: no shared memory
   const int64_t* unit_off;
   const int32_t* batch;
   const int64_t* kv;
@@ -239,18 +335,73 @@ __device__ __forceinline__ double pct_sorted_f(const int64_t* S, int n, double p
   return __dadd_rn(vlo, __dmul_rn(frac, __dsub_rn((double)S[hi], vlo)));
 }
 
-__global__ void __launch_bounds__(32 * kAllocWarps) iqr_kernel(IqrArgs A) {
+// Safe-set lex-min (B, K) with the first position on ties over the call's
+// units (decode_alloc.cpp:46-68), given the threshold; writes the outputs.
+__device__ __forceinline__ void iqr_finish(const IqrArgs& A, int c, int lane, int64_t u0, int n, double th,
+                                           bool fallback) {
+  int32_t bb = 0x7fffffff;
+  int64_t bk = kInf64;
+  int bp = 0x7fffffff;
+  for (int i = lane; i < n; i += 32) {
+    const int64_t kv = A.kv[u0 + i];
+    if (!fallback && !((double)kv <= th)) continue;
+    const int32_t b = A.batch[u0 + i];
+    if (b < bb || (b == bb && kv < bk)) { bb = b; bk = kv; bp = i; }
+  }
+  const uint32_t ob = (uint32_t)bb ^ 0x80000000u;
+  const uint32_t mb = __reduce_min_sync(kFull, ob);
+  const int64_t mk = warp_min_i64(ob == mb ? bk : kInf64);
+  const int pos = (int)__reduce_min_sync(kFull, (ob == mb && bk == mk) ? (uint32_t)bp : 0xffffffffu);
+  if (lane == 0) {
+    A.pos_out[c] = pos;
+    if (A.fallback_out) A.fallback_out[c] = fallback ? 1 : 0;
+    if (A.threshold_out) A.threshold_out[c] = th;
+  }
+}
+
+// <= 512 units: K (offset by 2^63, so signed order == unsigned order) sorted
+// in registers, 16 per lane; quartiles read by shuffles; no shared memory.
+__device__ void iqr_call_reg(const IqrArgs& A, int c, int lane, int64_t u0, int n) {
+  constexpr int KP = 16;
+  uint64_t x[KP];
+#pragma unroll
+  for (int i = 0; i < KP; ++i) {
+    const int p = KP * lane + i;
+    x[i] = p < n ? (uint64_t)A.kv[u0 + p] ^ 0x8000000000000000ull : UINT64_MAX;
+  }
+  warp_bitonic_regs<uint64_t, KP>(x, lane);
+  auto at = [&](int p) -> double {
+    return (double)(int64_t)(warp_regs_at<uint64_t, KP>(x, p) ^ 0x8000000000000000ull);
+  };
+  auto pct = [&](double p) -> double {  // percentile (decode_alloc.cpp:13-23) on the sorted K
+    const double rank = __ddiv_rn(__dmul_rn((double)n - 1.0, p), 100.0);
+    const int lo = (int)floor(rank), hi = (int)ceil(rank);
+    const double vlo = at(lo);
+    if (lo == hi) return vlo;
+    return __dadd_rn(vlo, __dmul_rn(__dsub_rn(rank, (double)lo), __dsub_rn(at(hi), vlo)));
+  };
+  const double q1 = pct(25.0), q3 = pct(75.0);
+  const double th = __dadd_rn(q3, __dmul_rn(A.k, __dsub_rn(q3, q1)));
+  const bool fallback = !(at(0) <= th);  // no K <= th
+  iqr_finish(A, c, lane, u0, n, th, fallback);
+}
+
+__global__ void __launch_bounds__(256) iqr_kernel(IqrArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int warp = threadIdx.x >> 5, lane = lane_id();
-  const int c = blockIdx.x * kAllocWarps + warp;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (blockDim.x >> 5) + warp;
   if (c >= A.n_calls) return;
-  int64_t* S = (int64_t*)(smem + warp * kIqrMaxUnits * 8);
   const int64_t u0 = A.unit_off[c];
   const int n = (int)(A.unit_off[c + 1] - u0);
-  if (n < 1 || n > kIqrMaxUnits) {
+  if (n < 1 || n > A.max_units) {
     if (lane == 0) atomicExch(A.error, n < 1 ? 3 : 4);
     return;
   }
+  if (n <= 512) {
+    iqr_call_reg(A, c, lane, u0, n);
+    return;
+  }
+  int64_t* S = (int64_t*)(smem + warp * kIqrMaxUnits * 8);
   // K -> double is monotone, so sorting int64 K == sorting the doubles.
   // Keys are offset by 2^63 so negative K would also order correctly.
   for (int i = lane; i < n; i += 32) S[i] = A.kv[u0 + i];
@@ -267,28 +418,7 @@ __global__ void __launch_bounds__(32 * kAllocWarps) iqr_kernel(IqrArgs A) {
   int nsafe = 0;
   for (int i = lane; i < n; i += 32) nsafe += ((double)A.kv[u0 + i] <= th) ? 1 : 0;
   nsafe = __reduce_add_sync(kFull, nsafe);
-  const bool fallback = nsafe == 0;
-  int32_t bb = 0x7fffffff;
-  int64_t bk = kInf64;
-  int bp = 0x7fffffff;
-  for (int i = lane; i < n; i += 32) {
-    int64_t kv = A.kv[u0 + i];
-    if (!fallback && !((double)kv <= th)) continue;
-    int32_t b = A.batch[u0 + i];
-    if (b < bb || (b == bb && kv < bk)) { bb = b; bk = kv; bp = i; }
-  }
-  // B >= 0 in the reference (core.h:145); order B as signed via offset
-  uint32_t ob = (uint32_t)bb ^ 0x80000000u;
-  uint32_t mb = __reduce_min_sync(kFull, ob);
-  int64_t ck = (ob == mb) ? bk : kInf64;
-  int64_t mk = warp_min_i64(ck);
-  uint32_t cp = (ob == mb && bk == mk) ? (uint32_t)bp : 0xffffffffu;
-  int pos = (int)__reduce_min_sync(kFull, cp);
-  if (lane == 0) {
-    A.pos_out[c] = pos;
-    if (A.fallback_out) A.fallback_out[c] = fallback ? 1 : 0;
-    if (A.threshold_out) A.threshold_out[c] = th;
-  }
+  iqr_finish(A, c, lane, u0, n, th, nsafe == 0);
 }
 
 struct SchedArgs {
@@ -468,35 +598,40 @@ cudaError_t launch_pbaa_one(const int64_t* rows, int n_pending, int n_new, const
   return cudaGetLastError();
 }
 
-cudaError_t launch_pbaa(const PbaaArgs& a, cudaStream_t st) {
-  const int smem = kAllocWarps * (kAllocMaxReq * 20 + kAllocMaxDp * 8);
-  static thread_local int configured = -1;  // attribute set once per device
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (configured != dev) {
+cudaError_t launch_pbaa(const PbaaArgs& a0, cudaStream_t st) {
+  PbaaArgs a = a0;
+  if (a.n_windows <= 0) return cudaSuccess;
+  // bounds: 0 = unknown -> the envelope.  Every warp keeps a slice sized from
+  // them: a window inside the register envelope by shape can still need the
+  // shared-memory path (ids >= 2^27, prompt lengths >= 2^31).
+  a.max_req = a.max_req > 0 ? std::min(a.max_req, kAllocMaxReq) : kAllocMaxReq;
+  a.max_dp = a.max_dp > 0 ? std::min(a.max_dp, kAllocMaxDp) : kAllocMaxDp;
+  const int slice = (int)pbaa_slice_bytes(a.max_req, a.max_dp);
+  int warps = 8;  // per CTA
+  while (warps > 1 && (size_t)warps * slice > 200 * 1024) warps >>= 1;
+  const int smem = warps * slice;
+  if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(pbaa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    configured = dev;
   }
-  int blocks = (a.n_windows + kAllocWarps - 1) / kAllocWarps;
-  if (blocks == 0) return cudaSuccess;
-  pbaa_kernel<<<blocks, 32 * kAllocWarps, smem, st>>>(a);
+  const int blocks = (a.n_windows + warps - 1) / warps;
+  pbaa_kernel<<<blocks, 32 * warps, smem, st>>>(a, slice);
   return cudaGetLastError();
 }
 
-cudaError_t launch_iqr(const IqrArgs& a, cudaStream_t st) {
-  const int smem = kAllocWarps * kIqrMaxUnits * 8;
-  static thread_local int configured = -1;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (configured != dev) {
+cudaError_t launch_iqr(const IqrArgs& a0, cudaStream_t st) {
+  IqrArgs a = a0;
+  if (a.n_calls <= 0) return cudaSuccess;
+  a.max_units = a.max_units > 0 ? std::min(a.max_units, kIqrMaxUnits) : kIqrMaxUnits;
+  // <= 512 units: registers only, 8 warps per CTA; else a 16 KB slice per warp
+  const int warps = a.max_units <= 512 ? 8 : kAllocWarps;
+  const int smem = a.max_units <= 512 ? 0 : warps * kIqrMaxUnits * 8;
+  if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(iqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    configured = dev;
   }
-  int blocks = (a.n_calls + kAllocWarps - 1) / kAllocWarps;
-  if (blocks == 0) return cudaSuccess;
-  iqr_kernel<<<blocks, 32 * kAllocWarps, smem, st>>>(a);
+  const int blocks = (a.n_calls + warps - 1) / warps;
+  iqr_kernel<<<blocks, 32 * warps, smem, st>>>(a);
   return cudaGetLastError();
 }
 

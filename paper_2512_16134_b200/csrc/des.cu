@@ -778,6 +778,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         dec_rr += 1;
       }
       n_dsel += 1;
+#ifdef SBS_PROF
+      const long long pa0 = clock64();
+#endif
       const int u = ul_ident ? pos : s_ul[pos];
       const int j = Dn == 1 ? 0 : u / Dd;
       // admit_decode (engine_model.cpp:145-151): B += 1, K += prompt_len
@@ -832,6 +835,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         if (lane == ntouched) order_lane = j;
         ntouched += 1;
       }
+#ifdef SBS_PROF
+      prof_acc[19] += clock64() - pa0;  // admission bookkeeping (incl. S_update)
+#endif
       wi += 1;
     }
     // keep unadmitted waiters (still sorted)
@@ -855,7 +861,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       if (lane == ntouched) order_lane = then_j;
       ntouched += 1;
     }
+    PROF_BEGIN(10);
     for (int t = 0; t < ntouched; ++t) try_begin_step(bcast(order_lane, t));
+    PROF_END(10);
   };
 
   // try_begin_prefill_pass (engine_model.cpp:51-116) + record_pass
@@ -1372,15 +1380,21 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     uint32_t mx = 0, ovf = 0;
     uint64_t s1 = 0, s2lo = 0, s2hi = 0;  // sum K, sum K^2 (128-bit)
     const bool band_fast = !LOG && Dn == 1 && now >= warmup;
-    double worst = 0.0;
+    // step-time maximum over non-negative doubles == maximum of their bit
+    // patterns (u64 compare: no FP64 compare on the loop-carried chain)
+    uint64_t worst_b = 0;
     uint64_t lm = UINT64_MAX;
     const uint32_t tps32 = (uint32_t)tps;
+    // the next unit's words are loaded one iteration ahead
+    uint64_t k_n = 0, r_n = 0;
+    uint32_t st_n = 0;
+    if (lane < Dd) { k_n = s_PK[u0 + lane]; r_n = s_R[u0 + lane]; st_n = (uint32_t)s_nst[u0 + lane]; }
 #pragma unroll 1
     for (int d = lane; d < Dd; d += 32) {
       const int u = u0 + d;
-      const uint64_t k = s_PK[u];
-      const uint64_t r = s_R[u];
-      const uint32_t st = (uint32_t)s_nst[u];
+      const uint64_t k = k_n, r = r_n;
+      const uint32_t st = st_n;
+      if (d + 32 < Dd) { k_n = s_PK[u + 32]; r_n = s_R[u + 32]; st_n = (uint32_t)s_nst[u + 32]; }
       const uint32_t kk = (uint32_t)k, rk = (uint32_t)r;
       const uint32_t grown = kk + tps32 * st;
       ovf |= grown < kk;
@@ -1397,10 +1411,12 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       const uint64_t k2 = (uint64_t)K * K;
       s2lo += k2;
       s2hi += s2lo < k2;
-      double t = __dadd_rn(__dmul_rn(dc_req, (double)B), __dmul_rn(dc_kv, (double)K));
-      worst = t > worst ? t : worst;
+      const double t = __dadd_rn(__dmul_rn(dc_req, (double)B), __dmul_rn(dc_kv, (double)K));
+      const uint64_t tb = (uint64_t)__double_as_longlong(t);
+      worst_b = tb > worst_b ? tb : worst_b;
     }
     if (SBS_UNLIKELY(__any_sync(kFull, ovf != 0))) error = kErrEnvelope;
+    double worst;
     PROF_END(12);
     PROF_BEGIN(13);
     // per-step reductions as independent 32-bit REDUX: the step time's max
@@ -1408,7 +1424,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     // sums are split into chunks whose 32-lane sums cannot overflow 32 bits
     // (lane partials: sum K < 2^36, sum K^2 < 2^68)
     {
-      const uint64_t wb = (uint64_t)__double_as_longlong(worst);
+      const uint64_t wb = worst_b;
       const uint32_t wh = __reduce_max_sync(kFull, (uint32_t)(wb >> 32));
       const uint32_t wl = __reduce_max_sync(kFull, (uint32_t)(wb >> 32) == wh ? (uint32_t)wb : 0u);
       worst = __longlong_as_double((long long)(((uint64_t)wh << 32) | wl));

@@ -47,6 +47,7 @@ struct CopySeg {
 cudaError_t launch_gather(const CopySeg* d_segs, int n_segs, int64_t n_blocks, cudaStream_t st);
 struct PbaaArgs {
   int32_t n_windows;
+  int32_t max_req, max_dp;
   const int64_t* req_off;
   const int32_t* n_pending;
   const int64_t* dp_off;
@@ -65,6 +66,7 @@ struct PbaaArgs {
 };
 struct IqrArgs {
   int32_t n_calls;
+  int32_t max_units;
   const int64_t* unit_off;
   const int32_t* batch;
   const int64_t* kv;
@@ -1720,9 +1722,9 @@ int sbs_prefill_allocate(const sbs_window_batch* b, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     Scratch& sc = scratch();
     CUDA_OR_THROW(cudaMemsetAsync(sc.d_err, 0, sizeof(int32_t), st));
-    sbs::PbaaArgs a{b->n_windows, b->req_off, b->n_pending, b->dp_off, b->n_limit, b->req_id,
-                    b->prompt_len, b->wait_in, b->caps, b->out_dp, b->out_rank, b->wait_out,
-                    b->flow, sc.d_err, b->hit_off, b->hit};
+    sbs::PbaaArgs a{b->n_windows, b->max_requests, b->max_dp, b->req_off, b->n_pending, b->dp_off,
+                    b->n_limit, b->req_id, b->prompt_len, b->wait_in, b->caps, b->out_dp,
+                    b->out_rank, b->wait_out, b->flow, sc.d_err, b->hit_off, b->hit};
     CUDA_OR_THROW(sbs::launch_pbaa(a, st));
     CUDA_OR_THROW(cudaMemcpyAsync(sc.h_err, sc.d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
     CUDA_OR_THROW(cudaStreamSynchronize(st));
@@ -1814,7 +1816,7 @@ int sbs_prefill_allocate_one(const int64_t* rows, int32_t n_pending, int32_t n_n
     *(int32_t*)(h + o_err) = 0;
     unsigned char* g = w.dev;
     CUDA_OR_THROW(cudaMemcpyAsync(g, h, off, cudaMemcpyHostToDevice, w.stream));
-    sbs::PbaaArgs a{1, (const int64_t*)(g + o_roff), (const int32_t*)(g + o_np),
+    sbs::PbaaArgs a{1, n, n_dp, (const int64_t*)(g + o_roff), (const int32_t*)(g + o_np),
                     (const int64_t*)(g + o_doff), (const int32_t*)(g + o_nl),
                     (const int64_t*)(g + o_id), (const int64_t*)(g + o_len),
                     (const int32_t*)(g + o_win), (int64_t*)(g + o_caps), (int32_t*)(g + o_dp),
@@ -1841,7 +1843,7 @@ int sbs_decode_select(const sbs_decode_batch* b, void* stream) {
     cudaStream_t st = (cudaStream_t)stream;
     Scratch& sc = scratch();
     CUDA_OR_THROW(cudaMemsetAsync(sc.d_err, 0, sizeof(int32_t), st));
-    sbs::IqrArgs a{b->n_calls, b->unit_off, b->batch, b->kv, b->k, b->pos_out,
+    sbs::IqrArgs a{b->n_calls, b->max_units, b->unit_off, b->batch, b->kv, b->k, b->pos_out,
                    b->fallback_out, b->threshold_out, sc.d_err};
     CUDA_OR_THROW(sbs::launch_iqr(a, st));
     CUDA_OR_THROW(cudaMemcpyAsync(sc.h_err, sc.d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -1854,9 +1856,9 @@ int sbs_decode_select(const sbs_decode_batch* b, void* stream) {
 
 int sbs_prefill_allocate_async(const sbs_window_batch* b, int32_t* error_out, void* stream) {
   return guarded([&] {
-    sbs::PbaaArgs a{b->n_windows, b->req_off, b->n_pending, b->dp_off, b->n_limit, b->req_id,
-                    b->prompt_len, b->wait_in, b->caps, b->out_dp, b->out_rank, b->wait_out,
-                    b->flow, error_out, b->hit_off, b->hit};
+    sbs::PbaaArgs a{b->n_windows, b->max_requests, b->max_dp, b->req_off, b->n_pending, b->dp_off,
+                    b->n_limit, b->req_id, b->prompt_len, b->wait_in, b->caps, b->out_dp,
+                    b->out_rank, b->wait_out, b->flow, error_out, b->hit_off, b->hit};
     CUDA_OR_THROW(sbs::launch_pbaa(a, (cudaStream_t)stream));
     return SBS_OK;
   });
@@ -1864,7 +1866,7 @@ int sbs_prefill_allocate_async(const sbs_window_batch* b, int32_t* error_out, vo
 
 int sbs_decode_select_async(const sbs_decode_batch* b, int32_t* error_out, void* stream) {
   return guarded([&] {
-    sbs::IqrArgs a{b->n_calls, b->unit_off, b->batch, b->kv, b->k, b->pos_out,
+    sbs::IqrArgs a{b->n_calls, b->max_units, b->unit_off, b->batch, b->kv, b->k, b->pos_out,
                    b->fallback_out, b->threshold_out, error_out};
     CUDA_OR_THROW(sbs::launch_iqr(a, (cudaStream_t)stream));
     return SBS_OK;

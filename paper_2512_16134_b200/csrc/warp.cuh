@@ -223,17 +223,11 @@ __device__ __forceinline__ void warp_radix_sort(Key* a, Key* t, uint32_t* hist, 
 // so every compare-exchange is a plain min/max pair.  Replaces two 8-bit
 // radix passes (smem histogram + match_any scatter per 32 keys) for the
 // sorted-K multiset of <= 512 decode units.
-template <int KP>
-__device__ __forceinline__ void warp_sort_reg_u32(uint32_t* a, int n, int lane) {
+template <typename Key, int KP>
+__device__ __forceinline__ void warp_bitonic_regs(Key (&x)[KP], int lane) {
   static_assert(KP >= 2 && KP <= 16 && (KP & (KP - 1)) == 0, "KP: power of two in [2, 16]");
-  uint32_t x[KP];
-#pragma unroll
-  for (int i = 0; i < KP; ++i) {
-    const int p = KP * lane + i;
-    x[i] = p < n ? a[p] : 0xffffffffu;
-  }
-  auto cas_up = [&](uint32_t& lo, uint32_t& hi) {
-    const uint32_t a0 = lo, b0 = hi;
+  auto cas_up = [&](Key& lo, Key& hi) {
+    const Key a0 = lo, b0 = hi;
     lo = a0 < b0 ? a0 : b0;
     hi = a0 < b0 ? b0 : a0;
   };
@@ -252,7 +246,7 @@ __device__ __forceinline__ void warp_sort_reg_u32(uint32_t* a, int n, int lane) 
   // stages (j >= KP), then the in-lane ones
 #pragma unroll 1
   for (int k = KP; k <= 32 * KP; k <<= 1) {
-    const uint32_t flip = ((KP * lane) & k) ? 0xffffffffu : 0u;
+    const Key flip = ((KP * lane) & k) ? (Key)~(Key)0 : (Key)0;
 #pragma unroll
     for (int i = 0; i < KP; ++i) x[i] ^= flip;
 #pragma unroll 1
@@ -261,7 +255,7 @@ __device__ __forceinline__ void warp_sort_reg_u32(uint32_t* a, int n, int lane) 
       const bool lower = (lane & m) == 0;
 #pragma unroll
       for (int i = 0; i < KP; ++i) {
-        const uint32_t y = __shfl_xor_sync(kFull, x[i], m);
+        const Key y = __shfl_xor_sync(kFull, x[i], m);
         x[i] = lower ? (x[i] < y ? x[i] : y) : (x[i] < y ? y : x[i]);
       }
     }
@@ -273,6 +267,28 @@ __device__ __forceinline__ void warp_sort_reg_u32(uint32_t* a, int n, int lane) 
 #pragma unroll
     for (int i = 0; i < KP; ++i) x[i] ^= flip;
   }
+}
+
+// Register i of lane o holds position KP*o + i after warp_bitonic_regs:
+// the key at position p (warp-uniform p), every lane gets it.
+template <typename Key, int KP>
+__device__ __forceinline__ Key warp_regs_at(const Key (&x)[KP], int p) {
+  const int r = p % KP;
+  Key v = x[0];
+#pragma unroll
+  for (int i = 1; i < KP; ++i) v = i == r ? x[i] : v;
+  return __shfl_sync(kFull, v, p / KP);
+}
+
+template <int KP>
+__device__ __forceinline__ void warp_sort_reg_u32(uint32_t* a, int n, int lane) {
+  uint32_t x[KP];
+#pragma unroll
+  for (int i = 0; i < KP; ++i) {
+    const int p = KP * lane + i;
+    x[i] = p < n ? a[p] : 0xffffffffu;
+  }
+  warp_bitonic_regs<uint32_t, KP>(x, lane);
   __syncwarp();
 #pragma unroll
   for (int i = 0; i < KP; ++i) {

@@ -16,7 +16,7 @@ n = sum(r["generated"] for r in res)
 names = ["select", "arrival", "finish_pass", "finish_step", "drain", "iqr_select", "S_update",
          "rebuild_S", "try_start_pass", "dispatch_chain", "begin_step", "fs.completers",
          "fs.unit_loop", "fs.reduce", "fs.band", "D.n_drains_with_waiters", "D.wait_P(~cyc)", "P.wait_recroom(cyc)",
-         "D.n_sorts", "P.consume", "D.total", "P.total", "sum_np_per_dispatch", "sum_nn"]
+         "D.n_sorts", "D.admit_book(incl S_upd)", "D.total", "P.total", "sum_np_per_dispatch", "sum_nn"]
 ev = sum(r["events"] for r in res)
 steps = sum(r["decode_steps"] for r in res)
 print("steps/request %.3f (post-warmup)" % (steps / n))

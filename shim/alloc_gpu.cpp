@@ -203,6 +203,7 @@ double outlier_threshold(std::span<const Tokens> kv_loads, double k) {
   Staging::check(cudaMemcpyAsync(g, h, o_pos, cudaMemcpyHostToDevice, g_st.stream));
   sbs_decode_batch b{};
   b.n_calls = 1;
+  b.max_units = (int32_t)std::min<size_t>(U, 1 << 30);
   b.unit_off = (const int64_t*)(g + o_off);
   b.batch = (const int32_t*)(g + o_b);
   b.kv = (const int64_t*)(g + o_k);
@@ -243,6 +244,7 @@ int select_decode_unit(const std::vector<DecodeUnitPlan>& units, double k,
   Staging::check(cudaMemcpyAsync(g, h, o_pos, cudaMemcpyHostToDevice, g_st.stream));
   sbs_decode_batch b{};
   b.n_calls = 1;
+  b.max_units = (int32_t)std::min<size_t>(U, 1 << 30);
   b.unit_off = (const int64_t*)(g + o_off);
   b.batch = (const int32_t*)(g + o_b);
   b.kv = (const int64_t*)(g + o_k);

@@ -45,7 +45,7 @@ def test_struct_sizes_match_header():
     assert ctypes.sizeof(P.api.Cluster) == 144
     assert ctypes.sizeof(P.api.LengthSpec) == 48
     assert ctypes.sizeof(P.api.Trace) == 56
-    assert ctypes.sizeof(P.api.WindowBatch) == 8 + 14 * 8
+    assert ctypes.sizeof(P.api.WindowBatch) == 8 + 14 * 8 + 8
     assert ctypes.sizeof(P.api.Experiment) == ctypes.sizeof(P.api.Cluster) + \
         ctypes.sizeof(P.api.Workload) + 4 * 4 + 8 + 8 + 3 * 8 + 8
 

@@ -230,3 +230,63 @@ def test_shim_schedule_decode_batch_vs_reference(tmp_path):
         assert np.array_equal(pl, w_pl), f"batch {i}"
         assert np.array_equal(th, w_th) and np.array_equal(fb, w_fb), f"batch {i}: observer"
         assert np.array_equal(un[:, 0], w_b) and np.array_equal(un[:, 1], w_kv), f"batch {i}: units"
+
+
+def test_pbaa_register_path_edges_vs_reference():
+    """Windows of <= 32 requests x <= 32 DP units take the register path: full
+    (prompt, id) ties keep input order (std::stable_sort), capacities beyond
+    32 bits take the 64-bit argmax, ids >= 2^27 fall back to the shared-memory
+    path; checked against the compiled reference (else the pinned C oracle)."""
+    rng = np.random.default_rng(2027)
+    check = ref.allocate_batch if ref.available() else orc.allocate_batch
+    wins = []
+    for t in range(3000):
+        D = int(rng.integers(1, 33))
+        k = int(rng.integers(0, 33))
+        if t % 5 == 0:
+            ids = rng.integers(0, 4, k)                      # duplicate ids
+            lens = rng.integers(1, 4, k)                     # -> full ties
+        elif t % 5 == 1:
+            ids = rng.permutation(1 << 20)[:k] + (1 << 27) - (1 << 19)  # straddles 2^27
+            lens = rng.integers(1, 5000, k)
+        else:
+            ids = rng.permutation(10 * k + 10)[:k]
+            lens = np.where(rng.random(k) < 0.2, 1, rng.integers(1, 1 << 30, k))
+        waits = rng.integers(0, 6, k)
+        rows = [[int(a), int(b), int(c)] for a, b, c in zip(ids, lens, waits)]
+        split = int(rng.integers(0, k + 1))
+        if t % 3 == 0:
+            caps = rng.integers(-(1 << 40), 1 << 41, D)     # 64-bit capacities
+        else:
+            caps = rng.integers(-4000, 1 << 31, D) if t % 3 == 1 else rng.integers(-50, 50, D)
+        wins.append({"pending": rows[:split], "new": rows[split:], "caps": caps.tolist(),
+                     "n_limit": int(rng.integers(0, 6))})
+    got = P.allocate_batch(wins)
+    for w, g in zip(wins, got):
+        e = check(w["pending"], w["new"], w["caps"], w["n_limit"])
+        for key in ("mapping", "deferred", "throttled", "caps"):
+            assert np.array_equal(g[key], e[key]), key
+        assert g["flow"] == e["flow"]
+
+
+def test_iqr_register_path_signed_and_wide_kv():
+    """<= 512 units are sorted in registers with K offset by 2^63: negative and
+    > 2^32 KV loads order exactly as the reference's doubles."""
+    rng = np.random.default_rng(77)
+    calls = []
+    for t in range(2000):
+        U = int(rng.integers(1, 513))
+        B = rng.integers(0, 5, U)
+        if t % 3 == 0:
+            K = rng.integers(-(1 << 45), 1 << 45, U)
+        elif t % 3 == 1:
+            K = rng.integers(0, 3, U)
+        else:
+            K = rng.integers(0, 1 << 33, U)
+        calls.append((B, K))
+    for k in (0.0, 1.5):
+        pos, fb, th = P.select_decode_unit(calls, k=k)
+        for i, (B, K) in enumerate(calls):
+            e = (ref.select_decode_unit(B, K, k) if ref.available()
+                 else orc.select_decode_unit(B, K, k))
+            assert (pos[i], fb[i], th[i]) == tuple(e), i
