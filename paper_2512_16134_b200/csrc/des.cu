@@ -1385,16 +1385,12 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     uint64_t worst_b = 0;
     uint64_t lm = UINT64_MAX;
     const uint32_t tps32 = (uint32_t)tps;
-    // the next unit's words are loaded one iteration ahead
-    uint64_t k_n = 0, r_n = 0;
-    uint32_t st_n = 0;
-    if (lane < Dd) { k_n = s_PK[u0 + lane]; r_n = s_R[u0 + lane]; st_n = (uint32_t)s_nst[u0 + lane]; }
 #pragma unroll 1
     for (int d = lane; d < Dd; d += 32) {
       const int u = u0 + d;
-      const uint64_t k = k_n, r = r_n;
-      const uint32_t st = st_n;
-      if (d + 32 < Dd) { k_n = s_PK[u + 32]; r_n = s_R[u + 32]; st_n = (uint32_t)s_nst[u + 32]; }
+      const uint64_t k = s_PK[u];
+      const uint64_t r = s_R[u];
+      const uint32_t st = (uint32_t)s_nst[u];
       const uint32_t kk = (uint32_t)k, rk = (uint32_t)r;
       const uint32_t grown = kk + tps32 * st;
       ovf |= grown < kk;
