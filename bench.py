@@ -298,7 +298,7 @@ def parse_decodes(rec):
     return c
 
 
-def run_alloc(args, rank, world):
+def run_alloc(args, rank, world, ctx=None, steps=None, warmup=None):
     """`--workload alloc`: the allocation step on its own — batched PBAA windows
     (sbs_prefill_allocate, allocate_batch prefill_alloc.cpp:61-88) and batched
     IQR decode placements (sbs_decode_select, select_decode_unit
@@ -308,6 +308,8 @@ def run_alloc(args, rank, world):
     import ctypes
     import numpy as np
     threads = os.cpu_count() or 1
+    steps = steps or steps
+    warmup = warmup if warmup is not None else warmup
     wrec, drec = alloc_inputs()
     wins, calls = parse_windows(wrec), parse_decodes(drec)
     desc = (f"alloc: the {len(wins)} PBAA windows and {len(calls)} IQR decode placements of a cfg2 "
@@ -329,13 +331,13 @@ def run_alloc(args, rank, world):
         return {"windows_per_s": w_n / w_wall, "windows": w_n, "windows_wall_s": w_wall,
                 "selects_per_s": d_n / d_wall, "selects": d_n, "selects_wall_s": d_wall}
 
-    if args.impl == "reference":
+    if args.impl == "reference" and ctx is None:
         if rank != 0:
             return 0
         vals = []
-        for i in range(args.warmup + args.steps):
+        for i in range(warmup + steps):
             c = cpu_arm()
-            if i >= args.warmup:
+            if i >= warmup:
                 vals.append(c)
         v = statistics.mean(c["windows_per_s"] for c in vals)
         sample = (f"allocate_batch over the recorded windows ({vals[0]['windows']} calls per step) and "
@@ -343,7 +345,7 @@ def run_alloc(args, rank, world):
                   f"step), {threads}-thread std::thread pool")
         print(json.dumps({
             "impl": "reference", "metric": "allocations_per_s", "value": v, "unit": "windows/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "n_gpus": world, "steps": steps, "warmup": warmup,
             "ms_per_step": 1000.0 * statistics.mean(c["windows_wall_s"] for c in vals),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic", "config": {"workload": desc, "sample": sample},
@@ -355,16 +357,18 @@ def run_alloc(args, rank, world):
         return 0
 
     import torch
-    import paper_2512_16134_b200 as P
     from paper_2512_16134_b200 import api
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    stream = torch.cuda.current_stream(dev)
+    if ctx is None:
+        torch.cuda.set_device(local)
+        dist = None
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dev = torch.device("cuda", local)
+        stream = torch.cuda.current_stream(dev)
+    else:
+        dist, dev, stream = ctx
     L = api.lib()
 
     # ---- windows: CSR arrays of one tile, tiled ALLOC_WINDOWS / len(wins) times
@@ -462,13 +466,13 @@ def run_alloc(args, rank, world):
             ts.append(ev0.elapsed_time(ev1))
         return statistics.mean(ts)
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         launch_windows(); launch_calls()
     gpu = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local]) \
         if os.environ.get("CUDA_VISIBLE_DEVICES") else local
     with ClockSampler(gpu) as clk:
-        w_ms = timed(launch_windows, args.steps)
-        d_ms = timed(launch_calls, args.steps)
+        w_ms = timed(launch_windows, steps)
+        d_ms = timed(launch_calls, steps)
     clocks = clk.summary()
     if int(err.item()):
         raise SystemExit("allocation kernels reported an error")
@@ -480,7 +484,7 @@ def run_alloc(args, rank, world):
     # ---- e2e: host (pinned) inputs -> device -> kernel -> outputs back, per
     # step, in chunks of windows pipelined over two copy streams (H2D of chunk
     # c+1 and D2H of chunk c-1 overlap the kernel on chunk c; PCIe is full duplex)
-    n_e = max(2, min(args.steps, 4))
+    n_e = max(2, min(steps, 4))
     out_h = {k: torch.empty(v.shape, dtype=v.dtype).pin_memory() for k, v in o.items()}
     caps_h = torch.empty_like(hp["caps"]).pin_memory()
     in_keys = ["req_off", "dp_off", "n_pending", "n_limit", "req_id", "prompt_len", "wait_in", "caps"]
@@ -571,7 +575,7 @@ def run_alloc(args, rank, world):
     value = world * nw / (w_ms / 1000.0)
     line = {
         "metric": "allocations_per_s", "value": value, "unit": "windows/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": w_ms, "higher_is_better": True,
+        "steps": steps, "warmup": warmup, "ms_per_step": w_ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
         "config": {"workload": desc, "windows_per_launch": nw, "requests_per_window_mean": float(qs.mean()),
                    "requests_per_window_max": int(qs.max()), "dp_units": int(ds.max()),
@@ -585,7 +589,7 @@ def run_alloc(args, rank, world):
                                               "unit": "GB/s", "frac": d_ach / peak,
                                               "bytes": "12*U + 4 per placement"},
                                  "cpu_baseline": (cpu or {}).get("selects_per_s")},
-        "gpu_launches": args.steps * 2,
+        "gpu_launches": steps * 2,
         "roofline": {"bound": "hbm", "achieved": w_ach, "peak": peak, "unit": "GB/s",
                      "frac": w_ach / peak, "traffic": None, "kernel_ms": w_ms,
                      "kernel_share_of_step": 1.0,
@@ -598,6 +602,8 @@ def run_alloc(args, rank, world):
                         "every output D2H; 16 chunks pipelined over two copy streams"},
         "cpu_baseline": cpu,
     }
+    if ctx is not None:
+        return line
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist:
@@ -633,6 +639,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-host-traces", action="store_true", help="skip the host-trace e2e leg")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="default cfg5 run: skip the compact cfg1-4 / alloc lines")
     args = ap.parse_args()
 
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -659,14 +667,57 @@ def main():
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
 
-    desc, cfgs = workload_points(args.workload, rank, world, args.replicas, args.duration)
+    line = measure(args, args.workload, rank, world, local, dev, stream, dist, args.steps, args.warmup,
+                   True, args.replicas, args.duration)
+    if args.workload == "cfg5" and not args.no_extras and args.replicas is None and args.duration is None:
+        # the other SURVEY §8d workloads and the allocation step alone, each a
+        # compact line (2 timed steps) carried inside the headline line so the
+        # driver's run records them beside their CPU baselines
+        extras = {}
+        for w in ("cfg1", "cfg2", "cfg3", "cfg4"):
+            extras[w] = compact(measure(args, w, rank, world, local, dev, stream, dist, 2, 1, False))
+        extras["alloc"] = compact(run_alloc(args, rank, world, ctx=(dist, dev, stream), steps=5, warmup=2))
+        line["workloads"] = extras
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def compact(line):
+    """The fields of a workload line that the headline carries for it."""
+    keep = ("metric", "value", "unit", "ms_per_step", "steps", "warmup", "config", "allocations_per_s",
+            "decode_placements_per_s", "decode_selects_per_s", "roofline", "e2e", "cpu_baseline",
+            "gpu_launches", "clocks")
+    out = {k: line[k] for k in keep if k in line and line[k] is not None}
+    cpu = (line.get("cpu_baseline") or {}).get("value")
+    if cpu:
+        out["ratio_vs_cpu"] = line["value"] / cpu
+        e = (line.get("e2e") or {}).get("value")
+        if e:
+            out["e2e_ratio_vs_cpu"] = e / cpu
+    return out
+
+
+
+def measure(args, workload, rank, world, local, dev, stream, dist, steps, warmup, full,
+            replicas=None, duration=None):
+    """One workload's bench line (dict): device-timed value, e2e legs, roofline,
+    CPU baseline.  full=False skips the host-trace e2e leg (extra lines)."""
+    import numpy as np  # noqa: F401
+    import torch
+    import paper_2512_16134_b200 as P
+
+    desc, cfgs = workload_points(workload, rank, world, replicas, duration)
     points = [P.experiment_from_config(c) for c in cfgs]
     # traces are generated on the device (bit-identical to generate_workload)
     sim = P.Simulator(points, None, device=local)
     R = len(points)
 
     # warm-up (also grows any arena that overflowed)
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         sim.launch(stream=stream.cuda_stream)
         res = sim.results(stream=stream.cuda_stream)
     errs = [r["error"] for r in res if r["error"]]
@@ -682,7 +733,7 @@ def main():
         if os.environ.get("CUDA_VISIBLE_DEVICES") else local
     times, des_times = [], []
     with ClockSampler(gpu) as clk:
-        for _ in range(args.steps):
+        for _ in range(steps):
             if dist:
                 dist.barrier()
             torch.cuda.synchronize()
@@ -716,7 +767,7 @@ def main():
     # come back.  Step k+1's generation is queued behind step k on one stream.
     e2e = None
     if not args.no_e2e:
-        n_e = max(2, min(args.steps, 4))
+        n_e = max(2, min(steps, 4))
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
@@ -747,7 +798,7 @@ def main():
 
     # ---- e2e with host-generated traces uploaded every step (the r01 path)
     e2e_host = None
-    if not args.no_e2e and not args.no_host_traces:
+    if not args.no_e2e and not args.no_host_traces and full:
         t0 = time.time()
         from concurrent.futures import ThreadPoolExecutor
         with ThreadPoolExecutor(max_workers=max(1, (os.cpu_count() or 2) // max(1, world))) as ex:
@@ -755,7 +806,7 @@ def main():
         gen_s = time.time() - t0
         hsim = P.Simulator(points, traces, device=local)
         h2d_bytes = 16 * sum(t.n for t in traces)
-        n_e = max(2, min(args.steps, 4))
+        n_e = max(2, min(steps, 4))
         hsim.launch(stream=stream.cuda_stream)  # warm-up
         hsim.results(stream=stream.cuda_stream)
         hsim.enable_trace_slots(2)
@@ -810,7 +861,7 @@ def main():
     if tf.exists():
         try:
             tj = json.load(open(tf))
-            traffic = tj.get(args.workload)
+            traffic = tj.get(workload)
         except Exception:
             traffic = None
 
@@ -818,12 +869,12 @@ def main():
     if rank == 0 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
-            spec = cpu_sample_spec(args.workload)
+            spec = cpu_sample_spec(workload)
             nrep = min(len(cfgs), threads * spec["replicas_per_core"])
             wall, gen, allocs, dsel, n = cpu_reference(cfgs, threads, nrep, spec["duration"])
             cpu = {"value": gen / wall, "unit": "sim-req/s", "cores": threads, "kind": "reference",
                    "cpu_model": cpu_model(),
-                   "sample": f"{n} replicas of {args.workload}"
+                   "sample": f"{n} replicas of {workload}"
                              + (f" at duration {spec['duration']:g} s" if spec["duration"] else "")
                              + f" ({gen:.0f} simulated requests) on {threads} threads, "
                                f"{wall:.1f} s wall"}
@@ -833,7 +884,7 @@ def main():
 
     line = {
         "metric": "simulated_requests_per_s", "value": value, "unit": "sim-req/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "n_gpus": world, "steps": steps, "warmup": warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
         "data": "synthetic",
         "config": {"workload": desc, "replicas_per_gpu": len(points),
@@ -844,7 +895,7 @@ def main():
         "summary": {"completed": summary["completed"], "window_requests": summary["window_requests"],
                     "ttft_mean_s": summary.get("ttft_mean_s"), "events": summary["events"]},
         "decode_placements_per_s": total_dsel / (ms / 1000.0),
-        "gpu_launches": args.steps * sim.launches_per_run,
+        "gpu_launches": steps * sim.launches_per_run,
         "gpu_launches_e2e_step": 1 + sim.launches_per_run,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "kernel_ms": des_ms,
@@ -856,13 +907,9 @@ def main():
         "e2e_host_traces": e2e_host,
         "cpu_baseline": cpu,
     }
-    if rank == 0:
-        print(json.dumps(line), flush=True)
     sim.close()
-    if dist:
-        dist.barrier()
-        dist.destroy_process_group()
-    return 0
+    return line
+
 
 
 if __name__ == "__main__":

@@ -531,13 +531,10 @@ void build_point(sbs_sim& s, PointHost& p) {
   {
     const char* e = std::getenv("SBS_SPLIT");
     const bool allow = e == nullptr || std::atoi(e) != 0;
-    // the decode warp only pays off when the trace has decode work
-    // (completion-ring entries carry times in 48 bits)
-    // (cache-aware points run on the one-warp kernels that compile the cache in)
-    const bool ca = x.prefill_mode == SBS_ALLOC_CACHE_AWARE && c.cache_enabled && t.pool != nullptr;
-    (void)ca;
-    d.split = (allow && p.split && !(s.flags & SBS_FLAG_LOGS) && t.max_output > 1 &&
-               seconds_to_ns(x.workload.duration_s) < (int64_t(1) << 47)) ? 1 : 0;
+    // two-warp replicas (cache-aware points included: kernel variants 10/11
+    // compile the cache into the prefill warp) whenever the trace has decode
+    // work; run records (SBS_FLAG_LOGS) are kept by the one-warp kernels only
+    d.split = (allow && p.split && !(s.flags & SBS_FLAG_LOGS) && t.max_output > 1) ? 1 : 0;
   }
   d.c_chunk = c.c_chunk;
   d.t_default = seconds_to_ns(c.t_default_s);
