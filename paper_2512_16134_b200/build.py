@@ -15,7 +15,8 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "lib"
 PROF = os.environ.get("SBS_PROF") == "1"   # development: clock64 region counters
-LIB = LIB_DIR / ("libsbs_b200_prof.so" if PROF else "libsbs_b200.so")
+CHECK = os.environ.get("SBS_CHECK") == "1"  # development: device bounds checks (trap)
+LIB = LIB_DIR / ("libsbs_b200_prof.so" if PROF else "libsbs_b200_check.so" if CHECK else "libsbs_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["des.cu", "alloc.cu", "gen.cu"]
@@ -34,13 +35,14 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
     LIB_DIR.mkdir(exist_ok=True)
-    obj_dir = LIB_DIR / ("obj_prof" if PROF else "obj")
+    obj_dir = LIB_DIR / ("obj_prof" if PROF else "obj_check" if CHECK else "obj")
     obj_dir.mkdir(exist_ok=True)
     objs = []
     common = ["-O3", "-std=c++17", "-lineinfo", f"-I{PKG.parent / 'include'}"]
     for src in CU_SOURCES:
         obj = obj_dir / (src + ".o")
-        cmd = [NVCC, *ARCH, *common, *(["-DSBS_PROF"] if PROF else []), "-fmad=false", "-Xptxas", "-v", "-Xcompiler",
+        cmd = [NVCC, *ARCH, *common, *(["-DSBS_PROF"] if PROF else []), *(["-DSBS_CHECK"] if CHECK else []),
+               "-fmad=false", "-Xptxas", "-v", "-Xcompiler",
                "-fPIC,-ffp-contract=off", "-c", str(CSRC / src), "-o", str(obj)]
         _run(cmd, verbose)
         objs.append(obj)

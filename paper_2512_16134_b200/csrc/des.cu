@@ -50,6 +50,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "des_types.h"
 #include "mt19937.cuh"
@@ -119,6 +120,17 @@ struct Counters {
 // Branch hints: cold paths leave the hot instruction stream (block layout).
 #define SBS_LIKELY(x) __builtin_expect(!!(x), 1)
 #define SBS_UNLIKELY(x) __builtin_expect(!!(x), 0)
+
+// Checked build (-DSBS_CHECK, build.py SBS_CHECK=1): every index into the
+// per-replica shared-memory and HBM arrays is bounds-checked on the device;
+// a violation prints the site and traps (the run fails loudly).  Compiled out
+// of the product build.
+#ifdef SBS_CHECK
+#define SBS_ASSERT(c) \
+  do { if (!(c)) { printf("SBS_CHECK %s:%d: %s\n", __FILE__, __LINE__, #c); __trap(); } } while (0)
+#else
+#define SBS_ASSERT(c) do { } while (0)
+#endif
 
 #ifdef SBS_PROF
 #define PROF_BEGIN(r) const long long _pt##r = clock64()
@@ -518,6 +530,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   //      accounting: no gathers on the event chains).
   auto complete_req = [&](bool has, int64_t id, int64_t t_done) {
     if (has) {
+      SBS_ASSERT(id >= 0 && id < N);
       o_comp[id] = t_done;
       if (per_req) o_status[id] = kStCompleted;
     }
@@ -616,6 +629,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       const int bb = j * R + (int)(s1 & (R - 1));
       const int nb = s_bcnt[bb];
       if (lane < nb && lane < kStageEntries) {
+        SBS_ASSERT(j >= 0 && j < Dn && bb >= 0 && bb < Dn * R);
         const unsigned dst = (unsigned)__cvta_generic_to_shared(s_stage + j * kStageEntries + lane);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst),
                      "l"(g_buckets + (int64_t)bb * BC + lane) : "memory");
@@ -701,6 +715,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     const uint32_t o = (uint32_t)oldv, nv = (uint32_t)newv;
     int c_old, c_new;
     warp_lower_bound2<uint32_t>(s_S, nul, o, nv, lane, c_old, c_new);
+    SBS_ASSERT(c_old >= 0 && c_old < c_new && c_new <= nul && s_S[c_old] == o);
     // shift S[c_old+1 .. c_new-1] left by one (128 per round: every load of a
     // round is issued before its stores), then S[c_new-1] = newv
 #pragma unroll 1
@@ -784,6 +799,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       const int u = ul_ident ? pos : s_ul[pos];
       const int j = Dn == 1 ? 0 : u / Dd;
       // admit_decode (engine_model.cpp:145-151): B += 1, K += prompt_len
+      SBS_ASSERT(u >= 0 && u < U && j >= 0 && j < Dn && id >= 0 && id < N && prompt >= 1 && out > 1);
       const uint64_t k0 = s_PK[u];
       const uint64_t K0 = k0 & kKMask, B0 = k0 >> 48;
       const uint64_t K1 = K0 + (uint64_t)prompt;
@@ -825,6 +841,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       const int cnt = s_bcnt[b];
       if (SBS_UNLIKELY(cnt >= BC)) { error = kErrOverflow; return; }
       if (lane == 0) {
+        SBS_ASSERT(b >= 0 && b < Dn * R && cnt >= 0 && cnt < BC && u >= 0 && u < U);
         g_buckets[(int64_t)b * BC + cnt] =
             make_int4((int)id, u, (int)(prompt + target + excess), (int)excess);
         s_bcnt[b] = (uint16_t)(cnt + 1);
@@ -975,6 +992,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       int32_t out = 0;
       if (has) {
         id = g_fifo[(int64_t)(g0 + d) * F + (idx & Fm)].x;
+        SBS_ASSERT(g0 + d < PD && id >= 0 && id < N);
         idx += 1;
         out = __ldg(g_output + id);
         o_ftok[id] = now;
@@ -1010,6 +1028,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       } else {
         if (wait) {
           int32_t prompt = __ldg(g_prompt + id);
+          SBS_ASSERT(ndw + __popc(m & lt_mask) < QD);
           g_dwait[ndw + __popc(m & lt_mask)] = wait_key(prompt, out, id);
         }
         ndw += __popc(m);
@@ -1024,6 +1043,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   auto fifo_push = [&](int g, int64_t id, int32_t tokens) -> bool {
     int32_t t = s_tail[g];
     if (t - s_rel[g] >= F) return false;
+    SBS_ASSERT(g >= 0 && g < PD && id >= 0 && id < N);
     g_fifo[(int64_t)g * F + (t & Fm)] = make_int2((int)id, tokens);
     s_tail[g] = t + 1;
     s_out[g] += tokens;
@@ -1188,6 +1208,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     int na = 0, thr = 0;
     for (int base = k1; base < np; base += 32) {
       int i = base + lane;
+      SBS_ASSERT(np <= QP);
       uint64_t key = i < np ? pk[i] : 0;
       bool valid = i < np && key != kPlaced;
       int32_t w = valid ? pw[i] + 1 : 0;
@@ -1353,6 +1374,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     const int b = j * R + (int)(s & (R - 1));
     const int n = s_bcnt[b];
     const int4* ent = g_buckets + (int64_t)b * BC;
+    SBS_ASSERT(j >= 0 && j < Dn && b >= 0 && b < Dn * R && n <= BC);
     const int4* stg = s_stage + j * kStageEntries;  // entries < kStageEntries (lane-owned copies)
     asm volatile("cp.async.wait_all;" ::: "memory");
     int64_t exc = 0;
@@ -1362,6 +1384,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       const int e = base + lane;
       if (e < n) {
         const int4 v = e < kStageEntries ? stg[e] : ent[e];
+        SBS_ASSERT(v.y >= u0 && v.y < u0 + Dd && v.x >= 0 && v.x < N);
         complete_req(true, v.x, now);
         atomicAdd((unsigned long long*)&s_R[v.y], (unsigned long long)(kBOne | (uint64_t)(uint32_t)v.z));
         exc += v.w;
@@ -1645,7 +1668,10 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
           wreg = true;
         } else {
 #pragma unroll 1
-          for (int i = lane; i < nk; i += 32) g_dwait[ndw + i] = chL->keys[(k0 + i) % kChanKeys];
+          for (int i = lane; i < nk; i += 32) {
+            SBS_ASSERT(ndw + i < QD);
+            g_dwait[ndw + i] = chL->keys[(k0 + i) % kChanKeys];
+          }
         }
         ndw += nk;
         rhead += 1;
