@@ -93,6 +93,7 @@ __device__ __forceinline__ int hist_bin(int64_t v) {
 
 __device__ __noinline__ void mt_twist_ool(uint64_t* mt) { mt_twist(mt); }
 
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -385,7 +386,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   int o_k = 0, o_i = 0;
 
   // ---- counters (shared memory, lane 0; the per-admission ones in registers)
-  int64_t n_fb = 0, n_mask = 0, n_dsel = 0;
+  int64_t n_fb = 0, n_mask = 0, n_dsel = 0, n_events = 0, n_steps = 0, n_outtok = 0;
 #ifdef SBS_PROF
   long long prof_acc[24] = {0};
   const long long prof_t0 = clock64();
@@ -1479,8 +1480,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     if (cap_batch > 0 && n > 0) ul_dirty = true;
     __syncwarp();
     if (now >= warmup) {
-      CNT(steps, 1);
-      CNT(outtok, gen);
+      if constexpr (ROLE == 2) { n_steps += 1; n_outtok += gen; }
+      else { CNT(steps, 1); CNT(outtok, gen); }
     }
     if (g_log) log_rec(LOG_STEP, 2, now, gen, 0, 0, 0);  // record_step (simulation.cpp:507)
     PROF_END(13);
@@ -1679,7 +1680,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       } else if (kind == 1) {
         // ---- on_decode_step (simulation.cpp:497-512)
         now = td;
-        CNT(events, 1);
+        n_events += 1;  // (ROLE 2: a register, flushed at the end)
         const int j = o_i;
         if (lane == j) ds_t = kInf64;
         odirty = true;
@@ -1927,7 +1928,10 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
 
   asm volatile("cp.async.wait_all;" ::: "memory");  // staged buckets: nothing in flight
   // ---- results (completion-derived fields: finalize_kernel)
-  if (lane == 0) { cn->fb += n_fb; cn->mask += n_mask; cn->dsel += n_dsel; }
+  if (lane == 0) {
+    cn->fb += n_fb; cn->mask += n_mask; cn->dsel += n_dsel;
+    if constexpr (ROLE == 2) { cn->events += n_events; cn->steps += n_steps; cn->outtok += n_outtok; }
+  }
   __syncwarp();
 #ifdef SBS_PROF
   if (ROLE == 0) prof_acc[21] += clock64() - prof_t0;
