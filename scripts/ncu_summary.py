@@ -42,4 +42,11 @@ with open(f"profiles/{tag}_ncu_des_summary.txt", "w") as f:
                       for x, k in sorted(st, reverse=True)[:10]) + "\n")
     f.write(f"# shared-memory bank conflicts: {float(d['l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum']) / 1e6:.1f} M"
             f" over {float(d['smsp__sass_inst_executed_op_shared_ld.sum']) / 1e6:.1f} M shared loads\n")
+    # the two CTAs of a cluster run different roles: the busiest SMs are the
+    # decode SMs (the critical path), the least busy the prefill SMs
+    f.write("# issue slots busy per SM (sm__issue_active.{avg,max,min}): "
+            f"avg {float(d['sm__issue_active.avg.pct_of_peak_sustained_elapsed']):.1f} %, "
+            f"max {float(d['sm__issue_active.max.pct_of_peak_sustained_elapsed']):.1f} % (decode SMs), "
+            f"min {float(d['sm__issue_active.min.pct_of_peak_sustained_elapsed']):.1f} % (prefill SMs); "
+            f"warp-instructions per request {float(d['smsp__inst_executed.sum']) / nreq:.0f}\n")
 print(f"{(rb + wb) * 1e6 / nreq:.2f} B/request")
