@@ -120,6 +120,11 @@ def workload_points(name, rank, world, replicas=None, duration=None):
         R = replicas or 512
         cfgs = [short3k(seed=7 + rank + world * i) for i in range(R)]
         return (f"cfg1: short_3k @ 23.25 s (~10k requests), SBS, {R} replicas per GPU", cfgs)
+    if name in ("cfg1_single_sbs", "cfg1_single_immediate"):
+        # the literal config-1 comparison: ONE replica (seed 7), SBS or immediate
+        pol = "sbs" if name.endswith("sbs") else "immediate"
+        return (f"cfg1 single replica: short_3k @ 23.25 s (~10k requests), policy {pol}, seed 7",
+                [short3k(seed=7, policy=pol)])
     raise SystemExit(f"unknown workload {name}")
 
 
@@ -633,7 +638,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg5",
-                    choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "alloc"])
+                    choices=["cfg1", "cfg1_single_sbs", "cfg1_single_immediate", "cfg2", "cfg3", "cfg4", "cfg5", "alloc"])
     ap.add_argument("--replicas", type=int, default=None, help="dev override (not a bench line)")
     ap.add_argument("--duration", type=float, default=None, help="dev override (not a bench line)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -674,7 +679,7 @@ def main():
         # compact line (2 timed steps) carried inside the headline line so the
         # driver's run records them beside their CPU baselines
         extras = {}
-        for w in ("cfg1", "cfg2", "cfg3", "cfg4"):
+        for w in ("cfg1", "cfg1_single_sbs", "cfg1_single_immediate", "cfg2", "cfg3", "cfg4"):
             extras[w] = compact(measure(args, w, rank, world, local, dev, stream, dist, 2, 1, False))
         extras["alloc"] = compact(run_alloc(args, rank, world, ctx=(dist, dev, stream), steps=5, warmup=2))
         line["workloads"] = extras
