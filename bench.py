@@ -803,7 +803,7 @@ def measure(args, workload, rank, world, local, dev, stream, dist, steps, warmup
 
     # ---- e2e with host-generated traces uploaded every step (the r01 path)
     e2e_host = None
-    if not args.no_e2e and not args.no_host_traces and full:
+    if not args.no_e2e and not args.no_host_traces and full and world == 1:  # (N>1: host generation would dominate the run)
         t0 = time.time()
         from concurrent.futures import ThreadPoolExecutor
         with ThreadPoolExecutor(max_workers=max(1, (os.cpu_count() or 2) // max(1, world))) as ex:
