@@ -313,8 +313,8 @@ def run_alloc(args, rank, world, ctx=None, steps=None, warmup=None):
     import ctypes
     import numpy as np
     threads = os.cpu_count() or 1
-    steps = steps or steps
-    warmup = warmup if warmup is not None else warmup
+    steps = steps or args.steps
+    warmup = warmup if warmup is not None else args.warmup
     wrec, drec = alloc_inputs()
     wins, calls = parse_windows(wrec), parse_decodes(drec)
     desc = (f"alloc: the {len(wins)} PBAA windows and {len(calls)} IQR decode placements of a cfg2 "

@@ -6,6 +6,7 @@ import sys
 from collections import Counter
 from pathlib import Path
 
+import numpy as np
 import pytest
 
 from oracle import ref
@@ -58,3 +59,33 @@ def test_cpu_arm_is_same_config():
     """The CPU arm runs full-size replicas of the GPU arm's workload."""
     for w in ("cfg5", "cfg2", "cfg3", "cfg1"):
         assert bench.cpu_sample_spec(w)["duration"] is None
+
+
+@pytest.mark.skipif(not ref.available(), reason="compiled reference unavailable")
+def test_alloc_reference_arm_and_inputs():
+    """`--workload alloc --impl reference`: the reference's allocate_batch /
+    select_decode_unit over the calls a cfg2 replica makes (recorded from the
+    reference), timed on the host cores; the parsed windows replay to the
+    recorded outputs through the C oracle."""
+    from oracle import orc
+    wrec, drec = bench.alloc_inputs()
+    wins, calls = bench.parse_windows(wrec), bench.parse_decodes(drec)
+    assert len(wins) > 500 and len(calls) > 10000 and all(len(c[0]) == 320 for c in calls)
+    for np_, nlim, rows, caps, mapping, caps_out, flow in wins[:200]:
+        e = orc.allocate_batch(rows[:np_], rows[np_:], caps, nlim)
+        assert np.array_equal(e["mapping"], mapping) and np.array_equal(e["caps"], caps_out)
+        assert e["flow"] == bool(flow)
+    p = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--workload", "alloc",
+                        "--steps", "1", "--warmup", "0"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["metric"] == "allocations_per_s" and line["value"] > 0
+    assert line["decode_selects_per_s"] > 0 and line["unit"] == "windows/s"
+
+
+def test_compact_extra_lines():
+    line = {"metric": "m", "value": 10.0, "unit": "u", "ms_per_step": 1.0, "config": {},
+            "cpu_baseline": {"value": 2.0}, "e2e": {"value": 5.0}, "clocks": None}
+    c = bench.compact(line)
+    assert c["ratio_vs_cpu"] == 5.0 and c["e2e_ratio_vs_cpu"] == 2.5 and "clocks" not in c
