@@ -386,7 +386,7 @@ typedef struct sbs_decode_batch {
 } sbs_decode_batch;
 int sbs_decode_select(const sbs_decode_batch* batch, void* stream);
 /* Asynchronous form (see sbs_prefill_allocate_async); error 3 = empty call,
- * 4 = more than 2048 units. */
+ * 4 = more units than max_units (2048 when 0; at most 16384). */
 int sbs_decode_select_async(const sbs_decode_batch* batch, int32_t* error_out, void* stream);
 
 /* Batched schedule_decode_batch (decode_alloc.cpp:83-106): batch b places

@@ -34,7 +34,8 @@ namespace sbs {
 constexpr int kAllocWarps = 4;
 constexpr int kAllocMaxReq = 1024;  // per window (shared-memory sort)
 constexpr int kAllocMaxDp = 1024;
-constexpr int kIqrMaxUnits = 2048;
+constexpr int kIqrMaxUnits = 16384;     // = the simulator's decode-unit envelope
+constexpr int kIqrDefaultUnits = 2048;  // bound assumed when the caller gives none
 constexpr int kOneMax = 32;  // pbaa_one_kernel: requests / DP units by value
 
 // Lexicographic ascending sort of (a, b) pairs in shared memory by a warp.
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__(32) pbaa_one_kernel(PbaaOne P) {
 
 struct IqrArgs {
   int32_t n_calls;
-  int32_t max_units;  // bound over the calls (<= 2048); <= 512: no shared memory
+  int32_t max_units;  // bound over the calls (<= 16384); <= 512: no shared memory
   const int64_t* unit_off;
   const int32_t* batch;
   const int64_t* kv;
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(256) iqr_kernel(IqrArgs A) {
     iqr_call_reg(A, c, lane, u0, n);
     return;
   }
-  int64_t* S = (int64_t*)(smem + warp * kIqrMaxUnits * 8);
+  int64_t* S = (int64_t*)(smem + (size_t)warp * pbaa_pow2(A.max_units) * 8);
   // K -> double is monotone, so sorting int64 K == sorting the doubles.
   // Keys are offset by 2^63 so negative K would also order correctly.
   for (int i = lane; i < n; i += 32) S[i] = A.kv[u0 + i];
@@ -622,10 +623,13 @@ cudaError_t launch_pbaa(const PbaaArgs& a0, cudaStream_t st) {
 cudaError_t launch_iqr(const IqrArgs& a0, cudaStream_t st) {
   IqrArgs a = a0;
   if (a.n_calls <= 0) return cudaSuccess;
-  a.max_units = a.max_units > 0 ? std::min(a.max_units, kIqrMaxUnits) : kIqrMaxUnits;
-  // <= 512 units: registers only, 8 warps per CTA; else a 16 KB slice per warp
-  const int warps = a.max_units <= 512 ? 8 : kAllocWarps;
-  const int smem = a.max_units <= 512 ? 0 : warps * kIqrMaxUnits * 8;
+  a.max_units = a.max_units > 0 ? std::min(a.max_units, kIqrMaxUnits) : kIqrDefaultUnits;
+  // <= 512 units: registers only, 8 warps per CTA; else one power-of-two
+  // shared-memory slice per warp (the bitonic sort pads to it), <= 4 per CTA
+  const size_t slice = a.max_units <= 512 ? 0 : (size_t)pbaa_pow2(a.max_units) * 8;
+  int warps = slice == 0 ? 8 : kAllocWarps;
+  while (warps > 1 && (size_t)warps * slice > 200 * 1024) warps >>= 1;
+  const int smem = (int)(warps * slice);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(iqr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;

@@ -180,12 +180,8 @@ double outlier_threshold(std::span<const Tokens> kv_loads, double k) {
   // Q3 + k (Q3 - Q1) from the IQR kernel (the threshold it masks with)
   const size_t U = kv_loads.size();
   if (U == 0) throw std::logic_error("percentile: empty input");
-  if (U > 2048) {  // beyond the kernel's staging envelope: the same formula on the host
-    std::vector<double> v(kv_loads.begin(), kv_loads.end());
-    double q1 = percentile(v, 25.0);
-    double q3 = percentile(std::move(v), 75.0);
-    return q3 + k * (q3 - q1);
-  }
+  if (U > 16384)  // the IQR kernel's envelope (= the simulator's decode-unit limit); no host fallback
+    throw std::runtime_error("outlier_threshold: more than 16384 decode units (GPU envelope)");
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off = align8(off + bytes); return o; };
   const size_t o_off = take(16), o_b = take(4 * U), o_k = take(8 * U), o_err = take(8),

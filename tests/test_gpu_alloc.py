@@ -290,3 +290,17 @@ def test_iqr_register_path_signed_and_wide_kv():
             e = (ref.select_decode_unit(B, K, k) if ref.available()
                  else orc.select_decode_unit(B, K, k))
             assert (pos[i], fb[i], th[i]) == tuple(e), i
+
+
+def test_iqr_large_unit_lists():
+    """Calls above 2,048 units (up to the simulator's 16,384-unit envelope) take
+    one power-of-two shared-memory slice per warp; beyond it the call fails
+    loudly (no host fallback)."""
+    rng = np.random.default_rng(8)
+    calls = [(rng.integers(0, 4, U), rng.integers(0, 10**6, U)) for U in (2049, 3000, 9000, 16384)]
+    pos, fb, th = P.select_decode_unit(calls, k=1.5)
+    for i, (B, K) in enumerate(calls):
+        e = ref.select_decode_unit(B, K, 1.5) if ref.available() else orc.select_decode_unit(B, K, 1.5)
+        assert (pos[i], fb[i], th[i]) == tuple(e), i
+    with pytest.raises(P.api.SbsError):
+        P.select_decode_unit([(np.zeros(16385, np.int64), np.arange(16385))])

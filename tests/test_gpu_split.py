@@ -120,25 +120,32 @@ def test_multi_instance_decode_with_faults_vs_reference():
 def test_oversized_handoff_falls_back_to_one_warp():
     """An EndForward that finishes more decode-bound requests than the hand-off
     key ring holds (here > 1,024: one-token prompts, a 100k-token chunk) makes
-    the replica rerun on one warp instead of blocking; result unchanged.
-    Run in a subprocess with a timeout so a regression cannot hang the suite."""
+    the replica rerun on one warp instead of blocking; the result equals the
+    one-warp run and, per request, the compiled reference.  Run in a
+    subprocess with a timeout so a regression cannot hang the suite."""
+    import copy
     import json
     import os
     import subprocess
     import sys
-    code = ("import copy,json,sys; sys.path.insert(0,'.'); import paper_2512_16134_b200 as P; "
-            "from tests.common import CASES; c=copy.deepcopy(CASES['decode_dp32']); "
-            "c['cluster'].update({'c_chunk':100000,'dp_degree':1,'n_instances_prefill':1,"
-            "'t_default_s':0.5}); c['workload'].update({'rate_qps':3000.0,'duration_s':3.0,"
-            "'initial_burst':2000,'prompt':{'dist':'constant','value':1},"
-            "'output':{'dist':'uniform','min':2,'max':20}}); "
-            "g=P.run_experiment(c, per_request=True); "
+    from oracle import ref
+    from tests.common import CASES
+    c = copy.deepcopy(CASES["decode_dp32"])
+    c["cluster"].update({"c_chunk": 100000, "dp_degree": 1, "n_instances_prefill": 1, "t_default_s": 0.5})
+    c["workload"].update({"rate_qps": 3000.0, "duration_s": 3.0, "initial_burst": 2000,
+                          "prompt": {"dist": "constant", "value": 1},
+                          "output": {"dist": "uniform", "min": 2, "max": 20}})
+    code = ("import json,sys; sys.path.insert(0,'.'); import paper_2512_16134_b200 as P; "
+            "c=json.loads(sys.argv[1]); g=P.run_experiment(c, per_request=True); "
             "print(json.dumps(g['requests']['completion'].tolist()))")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
     for mode in ("2", "0"):
-        p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=root,
-                           env=dict(os.environ, SBS_SPLIT=mode), timeout=300)
+        p = subprocess.run([sys.executable, "-c", code, json.dumps(c)], capture_output=True, text=True,
+                           cwd=root, env=dict(os.environ, SBS_SPLIT=mode), timeout=300)
         assert p.returncode == 0, p.stderr[-2000:]
         outs.append(json.loads(p.stdout.strip().splitlines()[-1]))
     assert outs[0] == outs[1]
+    if ref.available():
+        want = ref.run(copy.deepcopy(c), per_request=True)["requests"][:, 7].tolist()
+        assert outs[0] == want
