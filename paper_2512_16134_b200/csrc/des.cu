@@ -49,6 +49,7 @@
 //    32-bit REDUX where the operands allow.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 
@@ -141,18 +142,22 @@ struct Counters {
 #define PROF_END(r)
 #endif
 
-// Ordering of the two-warp channel: CTA scope within one CTA, cluster scope
-// when the two warps of a replica sit in the two CTAs of a cluster.
-template <bool CL>
+// Ordering of the two-warp channel (CM = channel mode): 0 = both warps in one
+// CTA (CTA scope), 1 = the two CTAs of a cluster (cluster scope, DSMEM),
+// 2 = the two warps in different kernels (GPU scope, the channel in HBM).
+template <int CM>
 __device__ __forceinline__ void chan_fence() {
-  if constexpr (CL) asm volatile("fence.acq_rel.cluster;" ::: "memory");
+  if constexpr (CM == 2) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  else if constexpr (CM == 1) asm volatile("fence.acq_rel.cluster;" ::: "memory");
   else __threadfence_block();
 }
 // acquire load of a channel word from this warp's own copy
-template <bool CL>
+template <int CM>
 __device__ __forceinline__ long long chan_ld(const volatile long long* p) {
   long long v;
-  if constexpr (CL) {
+  if constexpr (CM == 2) {
+    asm volatile("ld.acquire.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  } else if constexpr (CM == 1) {
     const unsigned a = (unsigned)__cvta_generic_to_shared((const void*)p);
     asm volatile("ld.acquire.cluster.shared::cta.b64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
   } else {
@@ -161,10 +166,12 @@ __device__ __forceinline__ long long chan_ld(const volatile long long* p) {
   }
   return v;
 }
-template <bool CL>
+template <int CM>
 __device__ __forceinline__ int chan_ld(const volatile int* p) {
   int v;
-  if constexpr (CL) {
+  if constexpr (CM == 2) {
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  } else if constexpr (CM == 1) {
     const unsigned a = (unsigned)__cvta_generic_to_shared((const void*)p);
     asm volatile("ld.acquire.cluster.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
   } else {
@@ -237,7 +244,7 @@ __device__ __noinline__ void kv_band_general_ool(const uint64_t* s_PK, int U, in
 // LOG: keep run records (compiled out of the sweep kernel).
 // ROLE: 0 = the whole replica on one warp; 1 = the prefill warp and 2 = the
 // decode warp of a two-warp replica (see the channel notes at the event loop).
-template <int KD, bool LOG, int ROLE, bool CL, bool CA = false>
+template <int KD, bool LOG, int ROLE, int CL, bool CA = false>
 __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* sm,
                             unsigned char* sm_peer) {
   static_assert(!(LOG && ROLE != 0), "run records are kept by the one-warp replica only");
@@ -298,8 +305,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   // two-warp replicas: every channel word is read from this warp's own copy
   // (chL) and written into the peer's (chR); one CTA (CL false): the same
   // struct; a CTA pair of a cluster (CL true): the peer CTA's shared memory
-  Chan* const chL = (Chan*)(sm + pt.sm_chan);
-  Chan* const chR = (Chan*)((CL ? sm_peer : sm) + pt.sm_chan);
+  Chan* const chL = CL == 2 ? pt.gchan : (Chan*)(sm + pt.sm_chan);
+  Chan* const chR = CL == 2 ? pt.gchan : (Chan*)((CL ? sm_peer : sm) + pt.sm_chan);
   if (lane == 0) {
     long long* z = (long long*)cn;
     for (int i = 0; i < (int)(sizeof(Counters) / 8); ++i) z[i] = 0;
@@ -534,6 +541,19 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       SBS_ASSERT(id >= 0 && id < N);
       o_comp[id] = t_done;
       if (per_req) o_status[id] = kStCompleted;
+    }
+  };
+
+  // Pair mode 3 (the two warps in different kernels): a hand-off wait that
+  // exceeds ~8 s of clock means the partner cannot make progress; the replica
+  // stops with an invariant error instead of hanging the GPU.
+  auto wait_expired = [&](long long& t0) -> bool {
+    if constexpr (CL != 2) {
+      return false;
+    } else {
+      const long long t = clock64();
+      if (t0 == 0) { t0 = t; return false; }
+      return t - t0 > 16000000000ll;
     }
   };
 
@@ -1010,9 +1030,11 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
 #ifdef SBS_PROF
           const long long pk0 = clock64();
 #endif
+          long long w0 = 0;
           for (;;) {
             const int kh = chL->khead;
             if (ktail + 32 - kh <= kChanKeys) break;
+            if (SBS_UNLIKELY(wait_expired(w0))) { error = kErrInvariant; break; }
             __nanosleep(100);
           }
 #ifdef SBS_PROF
@@ -1585,6 +1607,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     // process, so a decode event at time c is safe once p_done > c.
     // ===================================================================
     int rhead = 0, khead = 0, dtopo = 0, pub_head = 0;
+    int tail_seen = 0;  // records known published (re-read only once all are consumed)
+    long long dwait0 = 0;  // start of the current wait on the prefill warp (pair mode 3 guard)
     bool aborted = false;
     auto next_dtopo = [&]() -> int64_t {
       while (dtopo < n_topo && pt.topo_inst[dtopo] < P) ++dtopo;
@@ -1596,10 +1620,18 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       if (odirty) recompute_other();
       const int64_t td = o_t <= horizon ? o_t : kInf64;
       const int64_t tt = dt_t <= horizon ? dt_t : kInf64;
-      // progress first, then the queue (one shared load per word: warp-uniform)
-      const long long pdone = chan_ld<CL>(&chL->p_done);
-      const int tail = chan_ld<CL>(&chL->tail);
-      const bool have = rhead < tail;
+      // The queue first: a published record later than the next decode
+      // event already proves that event safe (records come in time order),
+      // so the progress word is read only when no record is known; then
+      // progress before the queue (a record below the progress seen is
+      // published before it).  Each acquire load is a round trip (HBM in
+      // pair mode 3).
+      long long pdone = 0;
+      if (rhead >= tail_seen) {
+        pdone = chan_ld<CL>(&chL->p_done);
+        tail_seen = chan_ld<CL>(&chL->tail);
+      }
+      const bool have = rhead < tail_seen;
       const ChanRec* rc = &chL->rec[rhead % kChanRecs];
       const int64_t th = have ? rc->t : kInf64;
       if (SBS_UNLIKELY(aborted)) {  // keep the prefill warp unblocked until it finishes
@@ -1612,6 +1644,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
           continue;
         }
         if (pdone == kInf64) break;
+        if (SBS_UNLIKELY(wait_expired(dwait0))) break;
         __nanosleep(128);
         continue;
       }
@@ -1628,10 +1661,12 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
             if (lane == 0) { chR->head = rhead; chR->khead = khead; }
             pub_head = rhead;
           }
+          if (SBS_UNLIKELY(wait_expired(dwait0))) { error = kErrInvariant; aborted = true; }
           __nanosleep(64);
           continue;
         }
       }
+      dwait0 = 0;
       int kind;  // 0 record, 1 step, 2 topology
       if (tt <= th && tt <= td) {
         kind = 2;
@@ -1786,9 +1821,11 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
 #ifdef SBS_PROF
         const long long pw0 = clock64();
 #endif
+        long long w0 = 0;
         for (;;) {
           const int hd = chL->head;
           if (ch_tail - hd < kChanRecs) break;
+          if (SBS_UNLIKELY(wait_expired(w0))) { error = kErrInvariant; break; }
           __nanosleep(100);
         }
 #ifdef SBS_PROF
@@ -1940,6 +1977,12 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   if (ROLE != 0) {
     if (lane == 0) {
       cn->err = error;
+      if constexpr (CL == 2) {  // two kernels: finalize_kernel combines the counters from HBM
+        const long long* src = (const long long*)cn;
+        long long* dst = (long long*)(pt.gcnt + (ROLE == 1 ? 0 : 32));
+        for (int i = 0; i < (int)(sizeof(Counters) / 8); ++i) dst[i] = src[i];
+        if (ROLE == 1) pt.gcnt[63] = 3;  // marker: finalize_kernel combines this replica
+      }
 #ifdef SBS_PROF
       for (int i = 0; i < 24; ++i) atomicAdd((unsigned long long*)&res.prof[i], (unsigned long long)prof_acc[i]);
 #endif
@@ -2122,6 +2165,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256)
   }
 }
 
+// Two-kernel pairs (pair mode 3): the prefill warps of all replicas in one
+// kernel on a minority of SMs (the prefill role idles about half the time, so
+// many share an SM), their decode warps in another on the rest (fewer decode
+// warps per SM: each runs faster), the hand-off channel in HBM (GPU-scope
+// acquire/release).  Slot s of both kernels runs replicas s, s + S, s + 2S...
+// in the same order, so a warp only ever waits on the partner working on the
+// same replica.  The pair must be co-resident: every CTA checks in on entry
+// and waits (bounded) until all CTAs of both kernels have; otherwise both
+// kernels give up (sync[1] = 1) and the host reruns the replicas as clusters.
+__device__ bool pair3_checkin(int* sync, int total) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    atomicAdd(sync, 1);
+    const long long t0 = clock64();
+    int v = 0;
+    for (;;) {
+      v = *(volatile int*)sync;
+      if (v >= total || *(volatile int*)(sync + 1) != 0) break;
+      if (clock64() - t0 > 4000000000ll) { atomicExch(sync + 1, 1); break; }  // ~2 s
+      __nanosleep(1000);
+    }
+    ok = v >= total && *(volatile int*)(sync + 1) == 0;
+  }
+  __syncthreads();
+  return ok != 0;
+}
+
+template <int KD, bool CA = false>
+__global__ void __launch_bounds__(384) des_pf_kernel(const DevPoint* __restrict__ pts, int n_pts, int S,
+                                                     int* __restrict__ sync, int total,
+                                                     DevResult* __restrict__ res, int slice) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  if (!pair3_checkin(sync, total)) return;
+  const int warp = threadIdx.x >> 5;
+  const int slot = warp * gridDim.x + blockIdx.x;
+  if (slot >= S) return;
+  unsigned char* my = smem + (size_t)warp * slice;
+  for (int pi = slot; pi < n_pts; pi += S) run_replica<KD, false, 1, 2, CA>(pts[pi], res[pi], my, my);
+}
+
+template <int KD>
+__global__ void __launch_bounds__(256) des_dc_kernel(const DevPoint* __restrict__ pts, int n_pts, int S,
+                                                     int* __restrict__ sync, int total,
+                                                     DevResult* __restrict__ res, int slice) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  if (!pair3_checkin(sync, total)) return;
+  const int warp = threadIdx.x >> 5;
+  const int slot = warp * gridDim.x + blockIdx.x;
+  if (slot >= S) return;
+  unsigned char* my = smem + (size_t)warp * slice;
+  for (int pi = slot; pi < n_pts; pi += S) {
+    // the decode fields sit at [sm_dec_begin, sm_dec_end) of the replica layout
+    unsigned char* base = my - pts[pi].sm_dec_begin;
+    run_replica<KD, false, 2, 2>(pts[pi], res[pi], base, base);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Finalize (MetricsCollector::finalize, metrics.cpp:103-190), one CTA per
 // replica, after the event loops.  Deferred accounting: the loops only stamp
@@ -2148,6 +2248,12 @@ __global__ void __launch_bounds__(256) reset_kernel(const DevPoint* __restrict__
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
       c[i] = make_int4(-1, -1, -1, -1);
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) pt.o_comp[n - 1] = -1;
+    if (pt.gcnt != nullptr && blockIdx.x == 0 && threadIdx.x == 0) pt.gcnt[63] = 0;
+    if (pt.gchan != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {  // pair mode 3's channel
+      Chan* ch = pt.gchan;
+      ch->p_done = 0;
+      ch->tail = 0; ch->head = 0; ch->ktail = 0; ch->khead = 0; ch->abort = 0;
+    }
   }
 }
 
@@ -2166,6 +2272,9 @@ __global__ void __launch_bounds__(256) finalize_kernel(const DevPoint* __restric
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   if (tid < kHistBins) { hbin[tid] = 0; tbin[tid] = 0; }
   if (tid == 0) n_win = 0;
+  // two-kernel pairs: fold the two warps' counters into the replica's result
+  if (pt.gcnt != nullptr && pt.split && *(const volatile int*)&pt.gcnt[63] == 3 && tid < 32)
+    combine_pair(pt, r, (const Counters*)pt.gcnt, (const Counters*)(pt.gcnt + 32));
   __syncthreads();
 
   // ---- pass 1: completion-derived sums (deferred accounting)
@@ -2364,6 +2473,47 @@ cudaError_t launch_des_cluster(int variant, const DevPoint* d_pts, int n_pts, De
   size_t smem = (size_t)w * smem_per_rep;
   if (smem < (size_t)kOnePerSm) smem = kOnePerSm;
   k<<<2 * ncl, 32 * w, smem, st>>>(d_pts, n_pts, nullptr, d_res, smem_per_rep);
+  return cudaGetLastError();
+}
+
+// Two-kernel pairs (variant 4|5|10|11 points, pair mode 3).  Geometry: the
+// prefill kernel on n_psm SMs with wp warps each, the decode kernel on the
+// other n_dsm with wd warps each, one CTA per SM (reserved shared memory
+// above half an SM), S = min(n_psm * wp, n_dsm * wd) slots.  `sync` is two
+// device ints (zeroed here).  Returns cudaErrorInvalidValue when the
+// geometry does not fit (the caller then uses cluster pairs).
+cudaError_t launch_des_pair3(int variant, const DevPoint* d_pts, int n_pts, DevResult* d_res, int slice_pf,
+                             int slice_dc, int n_psm, int wp, int n_dsm, int wd, int* sync,
+                             cudaStream_t st_pf, cudaStream_t st_dc) {
+  void (*kp)(const DevPoint*, int, int, int*, int, DevResult*, int) =
+      variant == 4 ? des_pf_kernel<1> : variant == 5 ? des_pf_kernel<4>
+    : variant == 10 ? des_pf_kernel<1, true> : des_pf_kernel<4, true>;
+  void (*kd)(const DevPoint*, int, int, int*, int, DevResult*, int) =
+      (variant == 4 || variant == 10) ? des_dc_kernel<1> : des_dc_kernel<4>;
+  constexpr int kMaxSmem = 227 * 1024, kOnePerSm = 120 * 1024;
+  if (wp < 1 || wp > 12 || wd < 1 || wd > 8 || n_psm < 1 || n_dsm < 1) return cudaErrorInvalidValue;
+  const size_t sp = std::max<size_t>((size_t)wp * slice_pf, kOnePerSm);
+  const size_t sd = std::max<size_t>((size_t)wd * slice_dc, kOnePerSm);
+  // (the kernels' own static shared memory - the check-in flag - leaves 1 KB)
+  if (sp > (size_t)kMaxSmem - 1024 || sd > (size_t)kMaxSmem - 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sp);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(kd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sd);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(sync, 0, 2 * sizeof(int), st_pf);
+  if (e != cudaSuccess) return e;
+  cudaEvent_t ev;
+  e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  if (e != cudaSuccess) return e;
+  cudaEventRecord(ev, st_pf);
+  cudaStreamWaitEvent(st_dc, ev, 0);  // the decode kernel after the zeroed check-in counter
+  cudaEventDestroy(ev);
+  const int S = std::min(n_psm * wp, n_dsm * wd);
+  const int total = n_psm + n_dsm;
+  kp<<<n_psm, 32 * wp, sp, st_pf>>>(d_pts, n_pts, S, sync, total, d_res, slice_pf);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  kd<<<n_dsm, 32 * wd, sd, st_dc>>>(d_pts, n_pts, S, sync, total, d_res, slice_dc);
   return cudaGetLastError();
 }
 

@@ -116,6 +116,10 @@ struct DevPoint {
   uint64_t* dwait;
   uint64_t* mt;
   int64_t* tpot_hist;  // kHistBins
+  // two-kernel pairs (pair mode 3): the hand-off channel in HBM and each
+  // warp's counters (2 x 256 B) for finalize_kernel to combine
+  struct Chan* gchan;
+  int64_t* gcnt;
   int64_t* log;        // optional run records (parity / report files), LOG_* below
   int64_t log_cap;     // words
   int32_t QP, QW, F, R, BC, QD;
@@ -124,6 +128,9 @@ struct DevPoint {
   int32_t sm_dPK, sm_dR, sm_dS, sm_dT, sm_dnst, sm_ulist, sm_bcnt, sm_hist, sm_wring, sm_wkeys, sm_cnt, sm_cnt2, sm_chan;
   int32_t sm_stage;  // per decode instance: the completion bucket of its step in progress
   int32_t sm_bytes;
+  // the prefill warp's fields come first, [0, sm_dec_begin); the decode
+  // warp's are [sm_dec_begin, sm_dec_end); the channel follows
+  int32_t sm_dec_begin, sm_dec_end;
   int32_t _pad1;
 };
 

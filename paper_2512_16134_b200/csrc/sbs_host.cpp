@@ -35,6 +35,9 @@ namespace sbs {
 cudaError_t launch_des(int variant, const DevPoint* d_pts, int n_pts, int* d_counter,
                        DevResult* d_res, int smem_per_warp, int warps_per_block, int n_blocks,
                        int min_smem, cudaStream_t st);
+cudaError_t launch_des_pair3(int variant, const DevPoint* d_pts, int n_pts, DevResult* d_res, int slice_pf,
+                             int slice_dc, int n_psm, int wp, int n_dsm, int wd, int* sync,
+                             cudaStream_t st_pf, cudaStream_t st_dc);
 cudaError_t launch_des_cluster(int variant, const DevPoint* d_pts, int n_pts, DevResult* d_res,
                                int smem_per_rep, cudaStream_t st);
 cudaError_t launch_finalize(const DevPoint* d_pts, int n_pts, DevResult* d_res, cudaStream_t st);
@@ -420,10 +423,16 @@ struct sbs_sim {
   int n_launches = 0;
   int64_t device_bytes = 0;
   int sm_count = 148;
-  int pair_mode = 2;  // two-warp replicas: 1 = one CTA, 2 = a 2-CTA cluster (SBS_SPLIT)
+  // two-warp replicas: 1 = one CTA, 2 = a 2-CTA cluster, 3 = two kernels
+  // (default; clusters when the group shares the launch or overflows one
+  // round, or when the kernels turn out not co-resident) — SBS_SPLIT
+  int pair_mode = 3;
+  int* d_sync = nullptr;  // pair mode 3: [0] CTAs checked in, [1] gave up (not co-resident)
+  int pair3_used = 0;     // the last launch ran a two-kernel group
   cudaEvent_t ev_des[2] = {nullptr, nullptr};  // around the DES kernels of the last launch
   // one stream per kernel variant: the variant groups run side by side
   cudaStream_t vstream[kVariants] = {};
+  cudaStream_t vstream2[kVariants] = {};  // pair mode 3: the decode kernel's stream
   cudaEvent_t ev_join[kVariants] = {};
   // trace re-upload in one gather launch (segment table, pinned host + device)
   sbs::CopySeg* h_segs = nullptr;
@@ -459,11 +468,17 @@ void layout_smem(sbs::DevPoint& d) {
     off = align_up(off + bytes, 16);
     return (int32_t)o;
   };
+  // prefill warp's fields first (a prefix: the slice of a prefill-only CTA)
   d.sm_pf_out = take(8 * PD);
   d.sm_pf_head = take(4 * PD);
   d.sm_pf_tail = take(4 * PD);
   d.sm_pf_rel = take(4 * PD);
   d.sm_pf_part = take(PD);
+  d.sm_wring = take(8 * (size_t)d.w_size);
+  d.sm_wkeys = take(8 * (size_t)sbs::kSmemWinKeys);
+  d.sm_cnt = take(256);
+  // then the decode warp's (the slice of a decode-only CTA)
+  d.sm_dec_begin = (int32_t)off;
   d.sm_dPK = take(8 * U);
   d.sm_dR = take(8 * U);
   d.sm_dS = take(4 * U);
@@ -473,10 +488,8 @@ void layout_smem(sbs::DevPoint& d) {
   d.sm_bcnt = take(2 * (size_t)d.Dn * d.R);
   d.sm_hist = take(4 * 256);
   d.sm_stage = take(16 * (size_t)sbs::kStageEntries * d.Dn);
-  d.sm_wring = take(8 * (size_t)d.w_size);
-  d.sm_wkeys = take(8 * (size_t)sbs::kSmemWinKeys);
-  d.sm_cnt = take(256);
   d.sm_cnt2 = take(256);
+  d.sm_dec_end = (int32_t)off;
   d.sm_chan = take(sizeof(sbs::Chan));
   d.sm_bytes = (int32_t)off;
 }
@@ -677,6 +690,10 @@ void build_point(sbs_sim& s, PointHost& p) {
   size_t o_dw = carve(8 * (size_t)p.QD);
   size_t o_mt = carve(8 * 312);
   size_t o_th = carve(8 * sbs::kHistBins);
+  // two-warp replicas: the hand-off channel and the two warps' counters in HBM
+  // (used when the pair runs as two kernels, pair mode 3)
+  size_t o_gch = d.split ? carve(sizeof(sbs::Chan)) : 0;
+  size_t o_gcn = d.split ? carve(512) : 0;
   const size_t n_keys = d.cache_on ? (size_t)d.n_pools * d.n_probes : 0;
   size_t o_cs = d.cache_on ? carve(4 * (size_t)PD * n_keys) : 0;
   size_t o_cu = d.cache_on ? carve(8 * (size_t)PD) : 0;
@@ -706,6 +723,8 @@ void build_point(sbs_sim& s, PointHost& p) {
   d.dwait = (uint64_t*)(b + o_dw);
   d.mt = (uint64_t*)(b + o_mt);
   d.tpot_hist = (int64_t*)(b + o_th);
+  d.gchan = d.split ? (sbs::Chan*)(b + o_gch) : nullptr;
+  d.gcnt = d.split ? (int64_t*)(b + o_gcn) : nullptr;
   d.c_stamp = d.cache_on ? (int32_t*)(b + o_cs) : nullptr;
   d.c_used = d.cache_on ? (int64_t*)(b + o_cu) : nullptr;
   d.c_clock = d.cache_on ? (int32_t*)(b + o_cc) : nullptr;
@@ -781,14 +800,68 @@ void order_points(sbs_sim& s) {
 // Kernel variants whose replicas are warp pairs (prefill warp + decode warp).
 bool is_pair_variant(int v) { return v == 4 || v == 5 || v == 10 || v == 11; }
 
+// Pair mode 3: the group's prefill warps in one kernel on n_psm SMs (wp warps
+// each: the prefill role idles about half the time), their decode warps in
+// another on the remaining SMs (fewer decode warps per SM than a 2-CTA
+// cluster gives), the channel in HBM.  Only when the group is the whole
+// launch (the two kernels must be co-resident on every SM) and the slices
+// fit; else the caller falls back to clusters.
+bool launch_pair3(sbs_sim& s, int v, const sbs::DevPoint* dp, int b, int e, cudaStream_t vs) {
+  for (int w = 0; w < sbs_sim::kVariants; ++w)
+    if (w != v && s.group_begin[w + 1] > s.group_begin[w]) {
+      if (std::getenv("SBS_DEBUG")) std::fprintf(stderr, "sbs: pair mode 3: other kernel groups, clusters\n");
+      return false;
+    }
+  const int n = e - b;
+  int slice_pf = 0, slice_dc = 0;
+  for (int i = b; i < e; ++i) {
+    const sbs::DevPoint& d = s.pts[s.order[i]].dp;
+    slice_pf = std::max(slice_pf, d.sm_dec_begin);
+    slice_dc = std::max(slice_dc, d.sm_dec_end - d.sm_dec_begin);
+  }
+  slice_pf = (int)align_up((size_t)slice_pf, 128);
+  slice_dc = (int)align_up((size_t)slice_dc, 128);
+  const char* ew = std::getenv("SBS_WP");
+  // 8 prefill warps per SM measured best on the cfg5 slice (512 pairs: 154.7 vs
+  // 146.3 M sim-req/s as clusters; 12 per SM makes the prefill side the limit)
+  int wp = ew ? std::atoi(ew) : 8;
+  while (wp > 1 && (size_t)wp * slice_pf > 227 * 1024) --wp;
+  int n_psm = (n + wp - 1) / wp;
+  if (n_psm >= s.sm_count) return false;
+  const int n_dsm = s.sm_count - n_psm;
+  int wd = std::min(8, (n + n_dsm - 1) / n_dsm);
+  while (wd > 1 && (size_t)wd * slice_dc > 227 * 1024) --wd;
+  if (s.d_sync == nullptr) CUDA_OR_THROW(cudaMalloc(&s.d_sync, 2 * sizeof(int)));
+  cudaStream_t st2 = s.vstream2[v];
+  CUDA_OR_THROW(cudaStreamWaitEvent(st2, s.ev_des[0], 0));
+  const cudaError_t err = sbs::launch_des_pair3(v, dp + b, n, s.d_res + b, slice_pf, slice_dc, n_psm, wp,
+                                                n_dsm, wd, s.d_sync, vs, st2);
+  if (std::getenv("SBS_DEBUG"))
+    std::fprintf(stderr, "sbs: pair mode 3: %d replicas, prefill %d SMs x %d warps (slice %d B), decode %d SMs x %d warps (slice %d B): %s\n",
+                 n, n_psm, wp, slice_pf, n_dsm, wd, slice_dc, cudaGetErrorString(err));
+  if (err == cudaErrorInvalidValue) return false;
+  CUDA_OR_THROW(err);
+  // join the decode kernel's stream into the group's
+  cudaEvent_t ev;
+  CUDA_OR_THROW(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CUDA_OR_THROW(cudaEventRecord(ev, st2));
+  CUDA_OR_THROW(cudaStreamWaitEvent(vs, ev, 0));
+  CUDA_OR_THROW(cudaEventDestroy(ev));
+  s.pair3_used = 1;
+  s.n_launches += 1;  // (two kernels for the group)
+  return true;
+}
+
 void launch_all(sbs_sim& s, cudaStream_t st) {
   s.n_launches = 0;
+  s.pair3_used = 0;
   const sbs::DevPoint* dp = s.cur_slot ? s.d_pts1 : s.d_pts;
   if (s.ev_des[0] == nullptr) {
     CUDA_OR_THROW(cudaEventCreate(&s.ev_des[0]));
     CUDA_OR_THROW(cudaEventCreate(&s.ev_des[1]));
     for (int v = 0; v < sbs_sim::kVariants; ++v) {
       CUDA_OR_THROW(cudaStreamCreateWithFlags(&s.vstream[v], cudaStreamNonBlocking));
+      CUDA_OR_THROW(cudaStreamCreateWithFlags(&s.vstream2[v], cudaStreamNonBlocking));
       CUDA_OR_THROW(cudaEventCreateWithFlags(&s.ev_join[v], cudaEventDisableTiming));
     }
   }
@@ -798,7 +871,7 @@ void launch_all(sbs_sim& s, cudaStream_t st) {
   int total_blocks = 0;
   for (int v = 0; v < sbs_sim::kVariants; ++v) {
     const int n = s.group_begin[v + 1] - s.group_begin[v];
-    if (n <= 0 || (is_pair_variant(v) && s.pair_mode == 2)) continue;
+    if (n <= 0 || (is_pair_variant(v) && s.pair_mode >= 2)) continue;
     const int per = is_pair_variant(v) ? std::max(1, std::min(4, (n + s.sm_count - 1) / s.sm_count))
                                        : s.warps_per_block;
     total_blocks += (n + per - 1) / per;
@@ -818,7 +891,11 @@ void launch_all(sbs_sim& s, cudaStream_t st) {
     CUDA_OR_THROW(cudaStreamWaitEvent(vs, s.ev_des[0], 0));
     used[v] = 1;
     int wpb = s.warps_per_block, per_block = wpb;
-    if (is_pair_variant(v) && s.pair_mode == 2) {  // replica = a CTA pair of a 2-CTA cluster
+    bool done = false;
+    if (is_pair_variant(v) && s.pair_mode == 3) done = launch_pair3(s, v, dp, b, e, vs);
+    if (done) {
+      // (launched)
+    } else if (is_pair_variant(v) && s.pair_mode >= 2) {  // replica = a CTA pair of a 2-CTA cluster
       CUDA_OR_THROW(sbs::launch_des_cluster(v, dp + b, e - b, s.d_res + b, s.smem_per_warp, vs));
     } else {
       if (is_pair_variant(v)) {  // two warps per replica; up to four replicas per block
@@ -1194,7 +1271,10 @@ void open_device(sbs_sim* s, const sbs_experiment* points, int32_t n_points, uin
   s->flags = flags;
   CUDA_OR_THROW(cudaSetDevice(device));
   CUDA_OR_THROW(cudaDeviceGetAttribute(&s->sm_count, cudaDevAttrMultiProcessorCount, device));
-  if (const char* e = std::getenv("SBS_SPLIT")) s->pair_mode = std::atoi(e) == 1 ? 1 : 2;
+  if (const char* e = std::getenv("SBS_SPLIT")) {
+    const int m = std::atoi(e);
+    s->pair_mode = m == 1 ? 1 : m == 2 ? 2 : 3;
+  }
 }
 
 void alloc_trace(sbs_sim* s, TraceDev& t, bool prefixes) {
@@ -1516,6 +1596,17 @@ int sbs_sim_results(sbs_sim* s, sbs_aggregates* out, sbs_histograms* hist, void*
                                    sizeof(sbs_gen_stats), cudaMemcpyDeviceToHost));
         s->gen_slot_valid[s->cur_slot] = 1;
       }
+      if (s->pair3_used) {  // the two kernels were not co-resident: rerun the launch as clusters
+        int sync[2] = {0, 0};
+        CUDA_OR_THROW(cudaMemcpy(sync, s->d_sync, sizeof(sync), cudaMemcpyDeviceToHost));
+        if (sync[1] != 0) {
+          if (std::getenv("SBS_DEBUG")) std::fprintf(stderr, "sbs: pair mode 3 not co-resident, clusters\n");
+          s->pair_mode = 2;
+          for (auto& p : s->pts) reset_point(p, st);
+          launch_all(*s, st);
+          continue;
+        }
+      }
       bool overflow = false;
       for (int i = 0; i < n; ++i) {
         const int err = s->h_res[i].error;
@@ -1643,10 +1734,12 @@ void sbs_sim_destroy(sbs_sim* s) {
   if (s->d_pts1) cudaFree(s->d_pts1);
   if (s->d_res) cudaFree(s->d_res);
   if (s->d_counter) cudaFree(s->d_counter);
+  if (s->d_sync) cudaFree(s->d_sync);
   for (auto& e : s->ev_des)
     if (e) cudaEventDestroy(e);
   for (int v = 0; v < sbs_sim::kVariants; ++v) {
     if (s->vstream[v]) cudaStreamDestroy(s->vstream[v]);
+    if (s->vstream2[v]) cudaStreamDestroy(s->vstream2[v]);
     if (s->ev_join[v]) cudaEventDestroy(s->ev_join[v]);
   }
   if (s->h_segs) cudaFreeHost(s->h_segs);

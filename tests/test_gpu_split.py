@@ -34,13 +34,13 @@ def _same(a, b, name):
             assert v == w, f"{name}: {k} {v!r} vs {w!r}"
 
 
-@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("mode", [1, 2, 3])
 @pytest.mark.parametrize("name", ["decode_dp32", "cfg2_20s", "short_3k", "oracle_n8", "cache_pd", "cache_pd_dp33"])
 def test_split_equals_serial(name, mode, monkeypatch):
     _same(_run(CASES[name], mode, monkeypatch), _run(CASES[name], 0, monkeypatch), name)
 
 
-@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("mode", [1, 2, 3])
 def test_split_equals_serial_random(mode, monkeypatch):
     rng = np.random.default_rng(77)
     for t in range(16):
@@ -140,12 +140,12 @@ def test_oversized_handoff_falls_back_to_one_warp():
             "print(json.dumps(g['requests']['completion'].tolist()))")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outs = []
-    for mode in ("2", "0"):
+    for mode in ("2", "3", "0"):
         p = subprocess.run([sys.executable, "-c", code, json.dumps(c)], capture_output=True, text=True,
                            cwd=root, env=dict(os.environ, SBS_SPLIT=mode), timeout=300)
         assert p.returncode == 0, p.stderr[-2000:]
         outs.append(json.loads(p.stdout.strip().splitlines()[-1]))
-    assert outs[0] == outs[1]
+    assert outs[0] == outs[1] == outs[2]
     if ref.available():
         want = ref.run(copy.deepcopy(c), per_request=True)["requests"][:, 7].tolist()
         assert outs[0] == want
