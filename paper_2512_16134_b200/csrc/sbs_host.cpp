@@ -822,11 +822,17 @@ bool launch_pair3(sbs_sim& s, int v, const sbs::DevPoint* dp, int b, int e, cuda
   slice_pf = (int)align_up((size_t)slice_pf, 128);
   slice_dc = (int)align_up((size_t)slice_dc, 128);
   const char* ew = std::getenv("SBS_WP");
-  // 8 prefill warps per SM measured best on the cfg5 slice (512 pairs: 154.7 vs
-  // 146.3 M sim-req/s as clusters; 12 per SM makes the prefill side the limit)
-  int wp = ew ? std::atoi(ew) : 8;
+  // 10 prefill warps per prefill SM measured best on the cfg5 slice (512 pairs
+  // on 52 + 96 SMs: 155.7 vs 146.3 M sim-req/s as clusters; 12 per SM makes
+  // the prefill side the limit, `profiles/r02_pair3_geometry.txt`)
+  int wp = ew ? std::atoi(ew) : 10;
   while (wp > 1 && (size_t)wp * slice_pf > 227 * 1024) --wp;
   int n_psm = (n + wp - 1) / wp;
+  if (const char* es = std::getenv("SBS_PSM")) {  // (dev: explicit prefill SM count)
+    n_psm = std::max(1, std::atoi(es));
+    wp = (n + n_psm - 1) / n_psm;
+    if (wp > 12 || (size_t)wp * slice_pf > 227 * 1024) return false;
+  }
   if (n_psm >= s.sm_count) return false;
   const int n_dsm = s.sm_count - n_psm;
   int wd = std::min(8, (n + n_dsm - 1) / n_dsm);
