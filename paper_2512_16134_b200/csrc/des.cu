@@ -244,7 +244,11 @@ __device__ __noinline__ void kv_band_general_ool(const uint64_t* s_PK, int U, in
 // LOG: keep run records (compiled out of the sweep kernel).
 // ROLE: 0 = the whole replica on one warp; 1 = the prefill warp and 2 = the
 // decode warp of a two-warp replica (see the channel notes at the event loop).
-template <int KD, bool LOG, int ROLE, int CL, bool CA = false>
+// SD (decode warp only): the replica has one decode instance, the IQR
+// policy, no batch cap, one token per step and no decode faults; those
+// runtime parameters become constants, so the decode warp's code carries only
+// the paths it can take (a smaller instruction-cache working set).
+template <int KD, bool LOG, int ROLE, int CL, bool CA = false, bool SD = false>
 __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* sm,
                             unsigned char* sm_peer) {
   static_assert(!(LOG && ROLE != 0), "run records are kept by the one-warp replica only");
@@ -254,18 +258,19 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   const unsigned lt_mask = lanemask_lt();
 
   // ---- constants hoisted out of the (global) descriptor
-  const int P = pt.P, Dn = pt.Dn, D = pt.D, Dd = pt.Dd, U = pt.U;
+  static_assert(!SD || ROLE == 2, "SD specialises the decode warp");
+  const int P = pt.P, Dn = SD ? 1 : pt.Dn, D = pt.D, Dd = pt.Dd, U = SD ? pt.Dd : pt.U;
   const int PD = P * D;
   const bool sbs = pt.policy == kSbs;
-  const int policy = pt.policy, dec_policy = pt.decode_policy;
+  const int policy = pt.policy, dec_policy = SD ? (int)kIqr : pt.decode_policy;
   const int64_t c_chunk = pt.c_chunk;
   const int64_t N = pt.n_dev ? *pt.n_dev : pt.N;
   const int64_t horizon = pt.horizon, warmup = pt.warmup;
   const int F = pt.F, Fm = pt.F - 1, R = pt.R, BC = pt.BC;
-  const int n_limit = pt.n_limit, cap_batch = pt.cap_batch, n_drops = pt.n_drops;
+  const int n_limit = pt.n_limit, cap_batch = SD ? 0 : pt.cap_batch, n_drops = pt.n_drops;
   const int n_topo = pt.n_topo, w_size = pt.w_size, QD = pt.QD, QP = pt.QP, QW = pt.QW;
   const bool per_req = pt.per_request != 0;
-  const int64_t tps = pt.tps, t_default = pt.t_default;
+  const int64_t tps = SD ? 1 : pt.tps, t_default = pt.t_default;
   const double inv_dd = 1.0 / (double)(pt.Dd > 0 ? pt.Dd : 1);
   const double pf_base = pt.pf_base, pf_tok = pt.pf_tok, dc_base = pt.dc_base, dc_req = pt.dc_req,
                dc_kv = pt.dc_kv, iqr_k = pt.iqr_k, wd_mult = pt.wd_mult;
@@ -340,7 +345,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   int64_t d_step = 0;
   int64_t ds_t = kInf64;
   uint32_t ds_s = 0xffffffffu;
-  const int64_t d_death = (lane < Dn) ? pt.death[P + lane] : kInf64;
+  const int64_t d_death = (!SD && lane < Dn) ? pt.death[P + lane] : kInf64;
   int64_t d_res = 0;            // residents over the instance's units
   double d_worst = 0.0;         // max_u decode_per_request*B + decode_per_kv*K
   int64_t d_res_begin = 0;      // residents stamped at the running step
@@ -1614,7 +1619,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       while (dtopo < n_topo && pt.topo_inst[dtopo] < P) ++dtopo;
       return dtopo < n_topo ? pt.topo_time[dtopo] : kInf64;
     };
-    int64_t dt_t = next_dtopo();
+    int64_t dt_t = SD ? kInf64 : next_dtopo();  // (SD: no decode topology events)
     for (;;) {
       if (SBS_UNLIKELY(seq > kSeqLimit) && !aborted) { error = kErrEnvelope; aborted = true; }
       if (odirty) recompute_other();
@@ -2205,7 +2210,7 @@ __global__ void __launch_bounds__(384) des_pf_kernel(const DevPoint* __restrict_
   for (int pi = slot; pi < n_pts; pi += S) run_replica<KD, false, 1, 2, CA>(pts[pi], res[pi], my, my);
 }
 
-template <int KD>
+template <int KD, bool SD = false>
 __global__ void __launch_bounds__(256) des_dc_kernel(const DevPoint* __restrict__ pts, int n_pts, int S,
                                                      int* __restrict__ sync, int total,
                                                      DevResult* __restrict__ res, int slice) {
@@ -2218,7 +2223,7 @@ __global__ void __launch_bounds__(256) des_dc_kernel(const DevPoint* __restrict_
   for (int pi = slot; pi < n_pts; pi += S) {
     // the decode fields sit at [sm_dec_begin, sm_dec_end) of the replica layout
     unsigned char* base = my - pts[pi].sm_dec_begin;
-    run_replica<KD, false, 2, 2>(pts[pi], res[pi], base, base);
+    run_replica<KD, false, 2, 2, false, SD>(pts[pi], res[pi], base, base);
   }
 }
 
@@ -2484,12 +2489,13 @@ cudaError_t launch_des_cluster(int variant, const DevPoint* d_pts, int n_pts, De
 // geometry does not fit (the caller then uses cluster pairs).
 cudaError_t launch_des_pair3(int variant, const DevPoint* d_pts, int n_pts, DevResult* d_res, int slice_pf,
                              int slice_dc, int n_psm, int wp, int n_dsm, int wd, int* sync,
-                             cudaStream_t st_pf, cudaStream_t st_dc) {
+                             cudaStream_t st_pf, cudaStream_t st_dc, bool simple_decode) {
   void (*kp)(const DevPoint*, int, int, int*, int, DevResult*, int) =
       variant == 4 ? des_pf_kernel<1> : variant == 5 ? des_pf_kernel<4>
     : variant == 10 ? des_pf_kernel<1, true> : des_pf_kernel<4, true>;
   void (*kd)(const DevPoint*, int, int, int*, int, DevResult*, int) =
-      (variant == 4 || variant == 10) ? des_dc_kernel<1> : des_dc_kernel<4>;
+      (variant == 4 || variant == 10) ? (simple_decode ? des_dc_kernel<1, true> : des_dc_kernel<1>)
+                                      : (simple_decode ? des_dc_kernel<4, true> : des_dc_kernel<4>);
   constexpr int kMaxSmem = 227 * 1024, kOnePerSm = 120 * 1024;
   if (wp < 1 || wp > 12 || wd < 1 || wd > 8 || n_psm < 1 || n_dsm < 1) return cudaErrorInvalidValue;
   const size_t sp = std::max<size_t>((size_t)wp * slice_pf, kOnePerSm);
