@@ -373,7 +373,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   int32_t imm_next = 0;
   int64_t dec_rr = 0;
   int32_t mti = 312;
-  bool S_valid = false, ul_dirty = true, ul_ident = false;
+  // SD: every decode unit stays listed (no caps, deaths or topology)
+  bool S_valid = false, ul_dirty = !SD, ul_ident = SD;
   bool S_gathered = false;      // s_S holds the unit Ks (unsorted) after a step
   // IQR fast path (one decode instance, every unit listed, U <= 1024): lane l
   // keeps the minimum of (B << 48 | K << 16 | u) over its units u = l mod 32
@@ -383,7 +384,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   // percentile ranks (decode_alloc.cpp:17-20) depend only on the unit count
   int pc_n = -1, lo25 = 0, hi25 = 0, lo75 = 0, hi75 = 0;
   double fr25 = 0.0, fr75 = 0.0;
-  int32_t nul = 0;
+  int32_t nul = SD ? pt.U : 0;
   int error = 0;
   int32_t pidx = 0, cur_ext = 0;   // ROLE 1: prefill-warp event index, handler is arrival/topology
   int32_t d_hk = 1, d_hi = 0;      // ROLE 2: handler of the decode event being processed
@@ -443,6 +444,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     if (lane == p && !(pflags & F_DEAD) && now >= p_death) pflags |= F_DEAD;
   };
   auto maybe_die_d = [&](int j) {
+    if constexpr (SD) return;  // (no decode deaths)
     bool died = false;
     if (lane == j && !(dflags & G_DEAD) && now >= d_death) { dflags |= G_DEAD; died = true; }
     if (__any_sync(kFull, died)) { ul_dirty = true; S_valid = false; S_gathered = false; }
@@ -622,7 +624,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     S_gathered = false;
     __syncwarp();
     if (nul <= 64) warp_sort_reg_u32<2>(s_S, nul, lane);
-    else if (nul <= 512) warp_sort_reg_u32<16>(s_S, nul, lane);
+    else if (SD || nul <= 512) warp_sort_reg_u32<16>(s_S, nul, lane);  // (SD: U <= 512)
     else warp_radix_sort<uint32_t>(s_S, s_T, s_hist, nul, mx ? 64 - __clzll((long long)mx) : 0, lane, lt_mask);
     S_valid = true;
   };
@@ -1499,7 +1501,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     }
     S_valid = false;
     lmin = lm;
-    lmin_ok = dec_policy == kIqr && Dn == 1 && U <= 1024 && ul_ident && !ul_dirty;
+    lmin_ok = SD || (dec_policy == kIqr && Dn == 1 && U <= 1024 && ul_ident && !ul_dirty);
     if (gather) {
       S_gathered = true;
       S_mx = (uint64_t)__reduce_max_sync(kFull, mx);

@@ -822,7 +822,7 @@ bool launch_pair3(sbs_sim& s, int v, const sbs::DevPoint* dp, int b, int e, cuda
     // the specialised decode kernel: one decode instance, IQR, no cap, one
     // token per step, no decode topology events or deaths
     bool sd = d.Dn == 1 && d.decode_policy == sbs::kIqr && d.cap_batch <= 0 && d.tps == 1 &&
-              d.death[d.P] == INT64_MAX;
+              d.death[d.P] == INT64_MAX && d.U <= 512;
     for (const auto& f : s.pts[s.order[i]].topo) sd = sd && f.instance < d.P;
     simple = simple && sd;
   }
