@@ -248,7 +248,10 @@ __device__ __noinline__ void kv_band_general_ool(const uint64_t* s_PK, int U, in
 // policy, no batch cap, one token per step and no decode faults; those
 // runtime parameters become constants, so the decode warp's code carries only
 // the paths it can take (a smaller instruction-cache working set).
-template <int KD, bool LOG, int ROLE, int CL, bool CA = false, bool SD = false>
+// SP (prefill warp only): SBS policy, no EndForward drops, no topology
+// events and no prefill deaths, as constants (the prefill kernel's code
+// carries only the SBS paths).
+template <int KD, bool LOG, int ROLE, int CL, bool CA = false, bool SD = false, bool SP = false>
 __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* sm,
                             unsigned char* sm_peer) {
   static_assert(!(LOG && ROLE != 0), "run records are kept by the one-warp replica only");
@@ -259,16 +262,17 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
 
   // ---- constants hoisted out of the (global) descriptor
   static_assert(!SD || ROLE == 2, "SD specialises the decode warp");
+  static_assert(!SP || ROLE == 1, "SP specialises the prefill warp");
   const int P = pt.P, Dn = SD ? 1 : pt.Dn, D = pt.D, Dd = pt.Dd, U = SD ? pt.Dd : pt.U;
   const int PD = P * D;
-  const bool sbs = pt.policy == kSbs;
-  const int policy = pt.policy, dec_policy = SD ? (int)kIqr : pt.decode_policy;
+  const bool sbs = SP || pt.policy == kSbs;
+  const int policy = SP ? (int)kSbs : pt.policy, dec_policy = SD ? (int)kIqr : pt.decode_policy;
   const int64_t c_chunk = pt.c_chunk;
   const int64_t N = pt.n_dev ? *pt.n_dev : pt.N;
   const int64_t horizon = pt.horizon, warmup = pt.warmup;
   const int F = pt.F, Fm = pt.F - 1, R = pt.R, BC = pt.BC;
-  const int n_limit = pt.n_limit, cap_batch = SD ? 0 : pt.cap_batch, n_drops = pt.n_drops;
-  const int n_topo = pt.n_topo, w_size = pt.w_size, QD = pt.QD, QP = pt.QP, QW = pt.QW;
+  const int n_limit = pt.n_limit, cap_batch = SD ? 0 : pt.cap_batch, n_drops = SP ? 0 : pt.n_drops;
+  const int n_topo = SP ? 0 : pt.n_topo, w_size = pt.w_size, QD = pt.QD, QP = pt.QP, QW = pt.QW;
   const bool per_req = pt.per_request != 0;
   const int64_t tps = SD ? 1 : pt.tps, t_default = pt.t_default;
   const double inv_dd = 1.0 / (double)(pt.Dd > 0 ? pt.Dd : 1);
@@ -337,7 +341,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   int32_t p_td = 0;
   int64_t ef_t = kInf64, wd_t = kInf64;
   uint32_t ef_s = 0xffffffffu, wd_s = 0xffffffffu;
-  const int64_t p_death = (lane < P) ? pt.death[lane] : kInf64;
+  const int64_t p_death = (!SP && lane < P) ? pt.death[lane] : kInf64;
   int32_t imm_dp = 0;  // RotationCursor::next_dp (baselines.h:17-20)
   int32_t ef_hidx = 0, ef_hext = 0;  // ROLE 1: handler that scheduled the live EndForward
 
@@ -441,6 +445,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
 
   // maybe_die (simulation.cpp:122-126)
   auto maybe_die_p = [&](int p) {
+    if constexpr (SP) return;  // (no prefill deaths)
     if (lane == p && !(pflags & F_DEAD) && now >= p_death) pflags |= F_DEAD;
   };
   auto maybe_die_d = [&](int j) {
@@ -2199,7 +2204,7 @@ __device__ bool pair3_checkin(int* sync, int total) {
   return ok != 0;
 }
 
-template <int KD, bool CA = false>
+template <int KD, bool CA = false, bool SP = false>
 __global__ void __launch_bounds__(384) des_pf_kernel(const DevPoint* __restrict__ pts, int n_pts, int S,
                                                      int* __restrict__ sync, int total,
                                                      DevResult* __restrict__ res, int slice) {
@@ -2209,7 +2214,7 @@ __global__ void __launch_bounds__(384) des_pf_kernel(const DevPoint* __restrict_
   const int slot = warp * gridDim.x + blockIdx.x;
   if (slot >= S) return;
   unsigned char* my = smem + (size_t)warp * slice;
-  for (int pi = slot; pi < n_pts; pi += S) run_replica<KD, false, 1, 2, CA>(pts[pi], res[pi], my, my);
+  for (int pi = slot; pi < n_pts; pi += S) run_replica<KD, false, 1, 2, CA, false, SP>(pts[pi], res[pi], my, my);
 }
 
 template <int KD, bool SD = false>
@@ -2491,9 +2496,10 @@ cudaError_t launch_des_cluster(int variant, const DevPoint* d_pts, int n_pts, De
 // geometry does not fit (the caller then uses cluster pairs).
 cudaError_t launch_des_pair3(int variant, const DevPoint* d_pts, int n_pts, DevResult* d_res, int slice_pf,
                              int slice_dc, int n_psm, int wp, int n_dsm, int wd, int* sync,
-                             cudaStream_t st_pf, cudaStream_t st_dc, bool simple_decode) {
+                             cudaStream_t st_pf, cudaStream_t st_dc, bool simple_decode, bool simple_prefill) {
   void (*kp)(const DevPoint*, int, int, int*, int, DevResult*, int) =
-      variant == 4 ? des_pf_kernel<1> : variant == 5 ? des_pf_kernel<4>
+      variant == 4 ? (simple_prefill ? des_pf_kernel<1, false, true> : des_pf_kernel<1>)
+    : variant == 5 ? (simple_prefill ? des_pf_kernel<4, false, true> : des_pf_kernel<4>)
     : variant == 10 ? des_pf_kernel<1, true> : des_pf_kernel<4, true>;
   void (*kd)(const DevPoint*, int, int, int*, int, DevResult*, int) =
       (variant == 4 || variant == 10) ? (simple_decode ? des_dc_kernel<1, true> : des_dc_kernel<1>)

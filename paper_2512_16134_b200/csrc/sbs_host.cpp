@@ -37,7 +37,7 @@ cudaError_t launch_des(int variant, const DevPoint* d_pts, int n_pts, int* d_cou
                        int min_smem, cudaStream_t st);
 cudaError_t launch_des_pair3(int variant, const DevPoint* d_pts, int n_pts, DevResult* d_res, int slice_pf,
                              int slice_dc, int n_psm, int wp, int n_dsm, int wd, int* sync,
-                             cudaStream_t st_pf, cudaStream_t st_dc, bool simple_decode);
+                             cudaStream_t st_pf, cudaStream_t st_dc, bool simple_decode, bool simple_prefill);
 cudaError_t launch_des_cluster(int variant, const DevPoint* d_pts, int n_pts, DevResult* d_res,
                                int smem_per_rep, cudaStream_t st);
 cudaError_t launch_finalize(const DevPoint* d_pts, int n_pts, DevResult* d_res, cudaStream_t st);
@@ -815,6 +815,7 @@ bool launch_pair3(sbs_sim& s, int v, const sbs::DevPoint* dp, int b, int e, cuda
   const int n = e - b;
   int slice_pf = 0, slice_dc = 0;
   bool simple = std::getenv("SBS_NO_SD") == nullptr;
+  bool simple_p = std::getenv("SBS_NO_SP") == nullptr;
   for (int i = b; i < e; ++i) {
     const sbs::DevPoint& d = s.pts[s.order[i]].dp;
     slice_pf = std::max(slice_pf, d.sm_dec_begin);
@@ -825,6 +826,10 @@ bool launch_pair3(sbs_sim& s, int v, const sbs::DevPoint* dp, int b, int e, cuda
               d.death[d.P] == INT64_MAX && d.U <= 512;
     for (const auto& f : s.pts[s.order[i]].topo) sd = sd && f.instance < d.P;
     simple = simple && sd;
+    // the specialised prefill kernel: SBS, no drops, no topology events, no prefill deaths
+    bool sp = d.policy == SBS_POLICY_SBS && d.n_drops == 0 && d.n_topo == 0;
+    for (int q = 0; q < d.P; ++q) sp = sp && d.death[q] == INT64_MAX;
+    simple_p = simple_p && sp;
   }
   slice_pf = (int)align_up((size_t)slice_pf, 128);
   slice_dc = (int)align_up((size_t)slice_dc, 128);
@@ -848,7 +853,7 @@ bool launch_pair3(sbs_sim& s, int v, const sbs::DevPoint* dp, int b, int e, cuda
   cudaStream_t st2 = s.vstream2[v];
   CUDA_OR_THROW(cudaStreamWaitEvent(st2, s.ev_des[0], 0));
   const cudaError_t err = sbs::launch_des_pair3(v, dp + b, n, s.d_res + b, slice_pf, slice_dc, n_psm, wp,
-                                                n_dsm, wd, s.d_sync, vs, st2, simple);
+                                                n_dsm, wd, s.d_sync, vs, st2, simple, simple_p);
   if (std::getenv("SBS_DEBUG"))
     std::fprintf(stderr, "sbs: pair mode 3: %d replicas, prefill %d SMs x %d warps (slice %d B), decode %d SMs x %d warps (slice %d B): %s\n",
                  n, n_psm, wp, slice_pf, n_dsm, wd, slice_dc, cudaGetErrorString(err));
