@@ -1579,8 +1579,10 @@ int sbs_sim_enable_trace_slots(sbs_sim* s, int32_t n) {
 }
 
 int32_t sbs_sim_launches_per_run(const sbs_sim* s) {
-  // one des_kernel per variant group + finalize_kernel (memsets are not ours)
-  int n = 1;
+  // the kernels of the last launch: reset_kernel, the DES kernel(s) of each
+  // variant group (two for a two-kernel pair group), finalize_kernel
+  if (s->n_launches > 0) return s->n_launches;
+  int n = 2;
   for (int v = 0; v < sbs_sim::kVariants; ++v) n += s->group_begin[v + 1] > s->group_begin[v] ? 1 : 0;
   return n;
 }
