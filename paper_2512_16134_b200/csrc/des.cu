@@ -251,18 +251,23 @@ __device__ __noinline__ void kv_band_general_ool(const uint64_t* s_PK, int U, in
 // SP (prefill warp only): SBS policy, no EndForward drops, no topology
 // events and no prefill deaths, as constants (the prefill kernel's code
 // carries only the SBS paths).
-template <int KD, bool LOG, int ROLE, int CL, bool CA = false, bool SD = false, bool SP = false>
+// PO (one-warp replica only): a prefill-only trace (every output_len <= 1,
+// so no request ever reaches the decode side) with the SP constants: the
+// decode code is compiled out of the one-warp kernel.
+template <int KD, bool LOG, int ROLE, int CL, bool CA = false, bool SD = false, bool SP = false,
+          bool PO = false>
 __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* sm,
                             unsigned char* sm_peer) {
   static_assert(!(LOG && ROLE != 0), "run records are kept by the one-warp replica only");
   constexpr bool kPre = ROLE != 2;  // this warp runs the prefill side
-  constexpr bool kDec = ROLE != 1;  // this warp runs the decode side
+  constexpr bool kDec = ROLE == 2 || (ROLE == 0 && !PO);  // this warp runs the decode side
   const int lane = lane_id();
   const unsigned lt_mask = lanemask_lt();
 
   // ---- constants hoisted out of the (global) descriptor
   static_assert(!SD || ROLE == 2, "SD specialises the decode warp");
-  static_assert(!SP || ROLE == 1, "SP specialises the prefill warp");
+  static_assert(!SP || ROLE != 2, "SP specialises the prefill side");
+  static_assert(!PO || (ROLE == 0 && SP && !LOG), "PO: one-warp, simple, prefill-only");
   const int P = pt.P, Dn = SD ? 1 : pt.Dn, D = pt.D, Dd = pt.Dd, U = SD ? pt.Dd : pt.U;
   const int PD = P * D;
   const bool sbs = SP || pt.policy == kSbs;
@@ -1031,7 +1036,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         o_ftok[id] = now;
       }
       bool done = has && out <= 1;   // decode_target() == 0
-      bool wait = has && out > 1;
+      bool wait = !PO && has && out > 1;  // (PO: every output_len <= 1)
       complete_req(done, id, now);
       unsigned m = __ballot_sync(kFull, wait);
       if (ROLE == 1) {
@@ -1910,7 +1915,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     }
 
     // ---- decode hand-off: hand_off_finished / on_decode_step tail
-    if (ROLE == 0 && (kind == kEvEF || kind == kEvDS)) {
+    if (ROLE == 0 && !PO && (kind == kEvEF || kind == kEvDS)) {
       PROF_BEGIN(4);
       drain_decode(step_j);
       PROF_END(4);
@@ -2035,7 +2040,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
 // orders replicas by estimated cost, longest first).  One instantiation per
 // (prefill DP units per lane, run records) so each keeps its own registers and
 // instruction footprint.
-template <int KD, bool LOG, bool CA = false>
+template <int KD, bool LOG, bool CA = false, bool PO = false>
 __global__ void __launch_bounds__(128) des_kernel(const DevPoint* __restrict__ pts, int n_pts,
                                                   int* __restrict__ next_point,
                                                   DevResult* __restrict__ res, int smem_per_warp) {
@@ -2046,7 +2051,7 @@ __global__ void __launch_bounds__(128) des_kernel(const DevPoint* __restrict__ p
     if (lane_id() == 0) pi = atomicAdd(next_point, 1);
     pi = bcast(pi, 0);
     if (pi >= n_pts) return;
-    run_replica<KD, LOG, 0, false, CA>(pts[pi], res[pi], my, my);
+    run_replica<KD, LOG, 0, false, CA, false, PO, PO>(pts[pi], res[pi], my, my);
     __syncwarp();
   }
 }
@@ -2430,7 +2435,8 @@ cudaError_t launch_des(int variant, const DevPoint* d_pts, int n_pts, int* d_cou
     : variant == 6 ? des_kernel<1, false, true> : variant == 7 ? des_kernel<4, false, true>
     : variant == 8 ? des_kernel<1, true, true> : variant == 9 ? des_kernel<4, true, true>
     : variant == 4 ? des_split_kernel<1> : variant == 5 ? des_split_kernel<4>
-    : variant == 10 ? des_split_kernel<1, true> : des_split_kernel<4, true>;
+    : variant == 10 ? des_split_kernel<1, true> : variant == 11 ? des_split_kernel<4, true>
+    : variant == 12 ? des_kernel<1, false, false, true> : des_kernel<4, false, false, true>;
   if (min_smem > 0 && smem < (size_t)min_smem) smem = (size_t)min_smem;  // CTAs per SM cap
   e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

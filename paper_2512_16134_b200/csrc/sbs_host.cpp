@@ -394,6 +394,7 @@ struct PointHost {
   int32_t F = 0, QP = 0, QW = 0, BC = 0, QD = 0;
   int64_t LOG = 0;
   int32_t split = 1;  // two-warp replica (cleared for an exact one-warp rerun)
+  bool prefill_only = false;  // every output_len <= 1: no request reaches the decode side
   void* arena = nullptr;
   size_t arena_bytes = 0;
   void* fault_buf = nullptr;
@@ -411,7 +412,7 @@ struct sbs_sim {
   std::vector<PointHost> pts;
   std::vector<TraceDev> traces;
   std::vector<int> order;  // device slot -> point index (grouped by variant, cost-descending)
-  static constexpr int kVariants = 12;
+  static constexpr int kVariants = 14;
   int group_begin[kVariants + 1] = {};  // slots of kernel variant v: [group_begin[v], group_begin[v+1])
   sbs::DevPoint* d_pts = nullptr;
   sbs::DevResult* d_res = nullptr;
@@ -548,6 +549,7 @@ void build_point(sbs_sim& s, PointHost& p) {
     // compile the cache into the prefill warp) whenever the trace has decode
     // work; run records (SBS_FLAG_LOGS) are kept by the one-warp kernels only
     d.split = (allow && p.split && !(s.flags & SBS_FLAG_LOGS) && t.max_output > 1) ? 1 : 0;
+    p.prefill_only = t.max_output <= 1;
   }
   d.c_chunk = c.c_chunk;
   d.t_default = seconds_to_ns(c.t_default_s);
@@ -780,6 +782,14 @@ void grow_caps(PointHost& p) {
 
 int variant_of(const PointHost& p) {
   if (p.dp.split) return (4 | (p.dp.D > 32 ? 1 : 0)) + (p.dp.cache_on ? 6 : 0);
+  // prefill-only SBS replicas without faults: the one-warp kernel with the
+  // decode side and the baseline / fault paths compiled out (variants 12|13)
+  if (p.prefill_only && p.dp.log == nullptr && !p.dp.cache_on && p.dp.policy == SBS_POLICY_SBS &&
+      p.dp.n_drops == 0 && p.dp.n_topo == 0 && std::getenv("SBS_NO_PO") == nullptr) {
+    bool alive = true;
+    for (int q = 0; q < p.dp.P; ++q) alive = alive && p.dp.death[q] == INT64_MAX;
+    if (alive) return 12 + (p.dp.D > 32 ? 1 : 0);
+  }
   return (p.dp.D > 32 ? 1 : 0) + (p.dp.log != nullptr ? 2 : 0) + (p.dp.cache_on ? 6 : 0);
 }
 
