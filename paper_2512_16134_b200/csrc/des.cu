@@ -52,6 +52,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 
 #include "des_types.h"
 #include "mt19937.cuh"
@@ -2529,7 +2530,8 @@ cudaError_t launch_des_pair3(int variant, const DevPoint* d_pts, int n_pts, DevR
   cudaStreamWaitEvent(st_dc, ev, 0);  // the decode kernel after the zeroed check-in counter
   cudaEventDestroy(ev);
   const int S = std::min(n_psm * wp, n_dsm * wd);
-  const int total = n_psm + n_dsm;
+  // (SBS_PAIR3_NOT_CORESIDENT: test hook, the check-in can never complete)
+  const int total = n_psm + n_dsm + (std::getenv("SBS_PAIR3_NOT_CORESIDENT") ? 1 : 0);
   kp<<<n_psm, 32 * wp, sp, st_pf>>>(d_pts, n_pts, S, sync, total, d_res, slice_pf);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;

@@ -5,12 +5,13 @@ extensions (TPOT sum, TTFT percentiles, histograms) whose FP64 sums depend on
 the lane that accumulated each request.  Mode 1: both warps in one CTA;
 mode 2: the two CTAs of a cluster (SBS_SPLIT)."""
 import copy
+import json
 
 import numpy as np
 import pytest
 
 import paper_2512_16134_b200 as P
-from tests.common import CASES
+from tests.common import CASES, load_case
 
 pytestmark = pytest.mark.gpu
 COLS = ("dispatch", "prefill_start", "first_token", "completion", "status")
@@ -149,3 +150,23 @@ def test_oversized_handoff_falls_back_to_one_warp():
     if ref.available():
         want = ref.run(copy.deepcopy(c), per_request=True)["requests"][:, 7].tolist()
         assert outs[0] == want
+
+
+def test_pair3_not_coresident_falls_back_to_clusters():
+    """If the two pair-mode-3 kernels are not co-resident (forced here), both
+    give up after the bounded check-in and the host reruns the launch as 2-CTA
+    clusters: the results are still the reference's."""
+    import os
+    import subprocess
+    import sys
+    code = ("import json,sys; sys.path.insert(0,'.'); import paper_2512_16134_b200 as P; "
+            "from tests.common import CASES; g=P.run_experiment(CASES['decode_dp32'], per_request=True); "
+            "print(json.dumps(g['requests']['completion'].tolist()))")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=root, timeout=300,
+                       env=dict(os.environ, SBS_SPLIT="3", SBS_PAIR3_NOT_CORESIDENT="1", SBS_DEBUG="1"))
+    assert p.returncode == 0, p.stderr[-2000:]
+    assert "not co-resident" in p.stderr
+    got = np.array(json.loads(p.stdout.strip().splitlines()[-1]))
+    want = load_case("decode_dp32")
+    assert np.array_equal(got, want["completion"])
