@@ -2256,7 +2256,8 @@ __global__ void __launch_bounds__(256) des_dc_kernel(const DevPoint* __restrict_
 // metrics.cpp:151-152) by 8-bit MSB radix select, four ranks at once, plus
 // the log2 TTFT histogram.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) reset_kernel(const DevPoint* __restrict__ pts, int n_pts) {
+__global__ void __launch_bounds__(256) reset_kernel(const DevPoint* __restrict__ pts, int n_pts,
+                                                    DevResult* __restrict__ res) {
   // completion stamps of every replica := -1 (unset), one launch for all
   for (int pi = blockIdx.y; pi < n_pts; pi += gridDim.y) {
     const DevPoint& pt = pts[pi];
@@ -2267,6 +2268,9 @@ __global__ void __launch_bounds__(256) reset_kernel(const DevPoint* __restrict__
       c[i] = make_int4(-1, -1, -1, -1);
     if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) pt.o_comp[n - 1] = -1;
     if (pt.gcnt != nullptr && blockIdx.x == 0 && threadIdx.x == 0) pt.gcnt[63] = 0;
+#ifdef SBS_PROF
+    if (blockIdx.x == 0 && threadIdx.x < 24) res[pi].prof[threadIdx.x] = 0;  // (pair mode 3 accumulates)
+#endif
     if (pt.gchan != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {  // pair mode 3's channel
       Chan* ch = pt.gchan;
       ch->p_done = 0;
@@ -2579,9 +2583,9 @@ cudaError_t launch_finalize(const DevPoint* d_pts, int n_pts, DevResult* d_res, 
   finalize_kernel<<<n_pts, 256, 0, st>>>(d_pts, d_res);
   return cudaGetLastError();
 }
-cudaError_t launch_reset(const DevPoint* d_pts, int n_pts, cudaStream_t st) {
+cudaError_t launch_reset(const DevPoint* d_pts, int n_pts, DevResult* d_res, cudaStream_t st) {
   if (n_pts == 0) return cudaSuccess;
-  reset_kernel<<<dim3(16, n_pts < 65535 ? n_pts : 65535), 256, 0, st>>>(d_pts, n_pts);
+  reset_kernel<<<dim3(16, n_pts < 65535 ? n_pts : 65535), 256, 0, st>>>(d_pts, n_pts, d_res);
   return cudaGetLastError();
 }
 }  // namespace sbs

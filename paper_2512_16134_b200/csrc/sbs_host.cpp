@@ -41,7 +41,7 @@ cudaError_t launch_des_pair3(int variant, const DevPoint* d_pts, int n_pts, DevR
 cudaError_t launch_des_cluster(int variant, const DevPoint* d_pts, int n_pts, DevResult* d_res,
                                int smem_per_rep, cudaStream_t st);
 cudaError_t launch_finalize(const DevPoint* d_pts, int n_pts, DevResult* d_res, cudaStream_t st);
-cudaError_t launch_reset(const DevPoint* d_pts, int n_pts, cudaStream_t st);
+cudaError_t launch_reset(const DevPoint* d_pts, int n_pts, DevResult* d_res, cudaStream_t st);
 struct CopySeg {
   const unsigned char* src;
   unsigned char* dst;
@@ -907,7 +907,7 @@ void launch_all(sbs_sim& s, cudaStream_t st) {
   const int min_smem = total_blocks <= s.sm_count ? 116 * 1024 : 0;
   // completion stamps := unset, every replica in one launch (finalize_kernel
   // derives the completion-based aggregates from them)
-  CUDA_OR_THROW(sbs::launch_reset(dp, (int)s.order.size(), st));
+  CUDA_OR_THROW(sbs::launch_reset(dp, (int)s.order.size(), s.d_res, st));
   s.n_launches += 1;
   CUDA_OR_THROW(cudaEventRecord(s.ev_des[0], st));
   int used[sbs_sim::kVariants] = {};
