@@ -1449,12 +1449,17 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     uint64_t worst_b = 0;
     uint64_t lm = UINT64_MAX;
     const uint32_t tps32 = (uint32_t)tps;
+    // software-pipelined: the next unit's three loads are issued before this
+    // unit's stores, so their shared-memory latency overlaps this iteration
+    uint64_t k = 0, r = 0;
+    uint32_t st = 0;
+    if (lane < Dd) { k = s_PK[u0 + lane]; r = s_R[u0 + lane]; st = (uint32_t)s_nst[u0 + lane]; }
 #pragma unroll 1
     for (int d = lane; d < Dd; d += 32) {
       const int u = u0 + d;
-      const uint64_t k = s_PK[u];
-      const uint64_t r = s_R[u];
-      const uint32_t st = (uint32_t)s_nst[u];
+      uint64_t k_nx = 0, r_nx = 0;
+      uint32_t st_nx = 0;
+      if (d + 32 < Dd) { k_nx = s_PK[u + 32]; r_nx = s_R[u + 32]; st_nx = (uint32_t)s_nst[u + 32]; }
       const uint32_t kk = (uint32_t)k, rk = (uint32_t)r;
       const uint32_t grown = kk + tps32 * st;
       ovf |= grown < kk;
@@ -1474,6 +1479,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       const double t = __dadd_rn(__dmul_rn(dc_req, (double)B), __dmul_rn(dc_kv, (double)K));
       const uint64_t tb = (uint64_t)__double_as_longlong(t);
       worst_b = tb > worst_b ? tb : worst_b;
+      k = k_nx; r = r_nx; st = st_nx;
     }
     if (SBS_UNLIKELY(__any_sync(kFull, ovf != 0))) error = kErrEnvelope;
     double worst;
