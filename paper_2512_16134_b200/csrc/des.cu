@@ -351,7 +351,11 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   int32_t imm_dp = 0;  // RotationCursor::next_dp (baselines.h:17-20)
   int32_t ef_hidx = 0, ef_hext = 0;  // ROLE 1: handler that scheduled the live EndForward
 
-  int dflags = (lane < Dn) ? G_HEALTHY : 0;
+  // SD (one decode instance): the instance's state is kept warp-uniform (every
+  // lane applies every update), so reading it needs no shuffle
+  constexpr bool UNI = SD;
+  static_assert(!SD || ROLE == 2, "SD is the decode role's specialisation");
+  int dflags = (UNI || lane < Dn) ? G_HEALTHY : 0;
   int64_t d_step = 0;
   int64_t ds_t = kInf64;
   uint32_t ds_s = 0xffffffffu;
@@ -447,7 +451,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   // helpers (all warp-uniform)
   // =======================================================================
   auto p_flag = [&](int p, int f) -> bool { return (bcast(pflags, p) & f) != 0; };
-  auto d_flag = [&](int j, int f) -> bool { return (bcast(dflags, j) & f) != 0; };
+  auto ib = [&](auto v, int j) { if constexpr (UNI) return v; else return bcast(v, j); };
+  auto d_flag = [&](int j, int f) -> bool { return (ib(dflags, j) & f) != 0; };
 
   // maybe_die (simulation.cpp:122-126)
   auto maybe_die_p = [&](int p) {
@@ -475,6 +480,11 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   };
 
   auto recompute_other = [&]() {
+    if (ROLE == 2 && Dn == 1) {  // decode warp, one instance: its step is the only other event
+      o_t = ib(ds_t, 0); o_s = ib(ds_s, 0); o_k = kEvDS; o_i = 0;
+      odirty = false;
+      return;
+    }
     int64_t lt = ef_t;
     uint32_t ls = ef_s;
     int lk = kEvEF;
@@ -643,12 +653,12 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   // try_begin_decode_step (engine_model.cpp:153-179).  Every resident is
   // stamped (s_nst tracks them), the step time uses the maintained max.
   auto try_begin_step = [&](int j) {
-    int fl = bcast(dflags, j);
+    int fl = ib(dflags, j);
     if ((fl & G_STEP) || (fl & G_DEAD)) return;
-    if (bcast(d_res, j) == 0) return;
-    double dur = __dadd_rn(dc_base, bcast(d_worst, j));
+    if (ib(d_res, j) == 0) return;
+    double dur = __dadd_rn(dc_base, ib(d_worst, j));
     int64_t t_end = now + llround_ns(dur);
-    if (lane == j) {
+    if (UNI || lane == j) {
       d_step += 1;
       dflags |= G_STEP;
       ds_t = t_end;
@@ -664,7 +674,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     // on complete at a later step): copy its head into shared memory while the
     // step runs, so finish_step reads it without a global round trip.
     {
-      const int64_t s1 = bcast(d_step, j);
+      const int64_t s1 = ib(d_step, j);
       const int bb = j * R + (int)(s1 & (R - 1));
       const int nb = s_bcnt[bb];
       if (lane < nb && lane < kStageEntries) {
@@ -850,7 +860,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         if (!stepping) s_nst[u] += 1;  // stamped by the step that begins next
         if (per_req) o_status[id] = kStDecoding;
       }
-      if (lane == j) {
+      if (UNI || lane == j) {
         d_res += 1;
         double t = __dadd_rn(__dmul_rn(dc_req, (double)(B0 + 1)), __dmul_rn(dc_kv, (double)K1));
         d_worst = t > d_worst ? t : d_worst;
@@ -875,7 +885,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       const int64_t target = (int64_t)out - 1;
       const int64_t nsteps = tps == 1 ? target : (target + tps - 1) / tps;
       const int64_t excess = nsteps * tps - target;
-      const int64_t c = bcast(d_step, j) + nsteps;
+      const int64_t c = ib(d_step, j) + nsteps;
       const int b = j * R + (int)(c & (R - 1));
       const int cnt = s_bcnt[b];
       if (SBS_UNLIKELY(cnt >= BC)) { error = kErrOverflow; return; }
@@ -1411,7 +1421,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
   // record_kv_snapshot (simulation.cpp:486-512, metrics.cpp:50-72, 99-101)
   auto finish_step = [&](int j) {
     const int u0 = j * Dd;
-    const int64_t s = bcast(d_step, j);
+    const int64_t s = ib(d_step, j);
     const int b = j * R + (int)(s & (R - 1));
     const int n = s_bcnt[b];
     const int4* ent = g_buckets + (int64_t)b * BC;
@@ -1509,9 +1519,9 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
     }
     // (completers' excess <= n * tps and K < 2^32: single 32-bit REDUX each)
     exc = (int64_t)__reduce_add_sync(kFull, (uint32_t)exc);
-    const int64_t stamped = bcast(d_res_begin, j);
+    const int64_t stamped = ib(d_res_begin, j);
     const int64_t gen = tps * stamped - exc;
-    if (lane == j) {
+    if (UNI || lane == j) {
       d_res -= n;
       d_worst = worst;
       dflags &= ~G_STEP;
@@ -1698,8 +1708,8 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         kind = 0;
       } else if (th == td) {
         const int j = o_i;
-        const int64_t tsd = bcast(ds_ts, j);
-        const int hk = bcast(ds_hk, j), hi = bcast(ds_hi, j);
+        const int64_t tsd = ib(ds_ts, j);
+        const int hk = ib(ds_hk, j), hi = ib(ds_hi, j);
         int ef_first;
         if (rc->ts != tsd) ef_first = rc->ts < tsd;
         else if (hk == 0) ef_first = rc->h_idx < hi;
@@ -1741,7 +1751,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         now = td;
         n_events += 1;  // (ROLE 2: a register, flushed at the end)
         const int j = o_i;
-        if (lane == j) ds_t = kInf64;
+        if (UNI || lane == j) ds_t = kInf64;
         odirty = true;
         maybe_die_d(j);
         if (d_flag(j, G_DEAD)) continue;
