@@ -928,7 +928,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
       ntouched += 1;
     }
     PROF_BEGIN(10);
-    for (int t = 0; t < ntouched; ++t) try_begin_step(bcast(order_lane, t));
+    for (int t = 0; t < ntouched; ++t) try_begin_step(Dn == 1 ? 0 : bcast(order_lane, t));
     PROF_END(10);
   };
 
@@ -1734,7 +1734,7 @@ __device__ void run_replica(const DevPoint& pt, DevResult& res, unsigned char* s
         if (ndw == 0 && nk <= 32) {
           // the usual case: this record's waiters only, sorted in registers
           rkey = lane < nk ? chL->keys[(k0 + lane) % kChanKeys] : UINT64_MAX;
-          if (nk > 1) rkey = warp_sort32<true>(rkey, lane);
+          if (nk > 1) rkey = warp_sort32_n(rkey, lane, nk);  // (lanes >= nk: UINT64_MAX)
           wreg = true;
         } else {
 #pragma unroll 1

@@ -105,6 +105,18 @@ __device__ __forceinline__ uint64_t warp_sort32(uint64_t x, int lane) {
 template <bool ROLLED = false>
 __device__ __forceinline__ uint64_t warp_sort32(uint64_t x) { return warp_sort32<ROLLED>(x, lane_id()); }
 
+// Ascending sort of lanes 0..n-1 (1 < n <= 32) when lanes >= n hold
+// UINT64_MAX: only the bitonic stages up to the next power of two >= n
+// (partners never leave their block of that size; the padding stays on top).
+__device__ __forceinline__ uint64_t warp_sort32_n(uint64_t x, int lane, int n) {
+  const int m = 1 << (32 - __clz(n - 1));
+#pragma unroll 1
+  for (int k = 2; k <= m; k <<= 1)
+#pragma unroll 1
+    for (int j = k >> 1; j > 0; j >>= 1) x = bitonic_step(x, lane, k, j);
+  return x;
+}
+
 // Warp bitonic sort of n keys (ascending) in a buffer of capacity >= pow2(n)
 // (generic pointer: shared or global).  Pads with UINT64_MAX.
 template <bool ROLLED = false>
